@@ -1,0 +1,170 @@
+/*
+ * hivc_b200.h — C ABI of the B200-native HIVC per-frame reconstruction path.
+ *
+ * The reference (arXiv 2008.10273, package `hivc`, /root/reference/pkg/src/hivc)
+ * is pure Python/numpy and has no FFI of its own; these entry points are the
+ * functions its Python signatures bind to (see INTEGRATION.md for the ctypes
+ * stubs).  Each declaration names the reference interface it replaces.
+ *
+ * Conventions
+ *  - Every function returns an int status (HIVC_OK == 0).  On failure a
+ *    thread-local message is available from hivc_last_error(); the status
+ *    code names the reference exception class to raise.
+ *  - "device" pointers are CUDA device addresses (e.g. torch.cuda tensors'
+ *    data_ptr()); "host" pointers are ordinary CPU memory.
+ *  - Floating-point planes are row-major float64 (the reference computes in
+ *    float64); masks are uint8 0/1; decoded frames are uint8.
+ *  - No torch types cross this boundary.
+ */
+#ifndef HIVC_B200_H
+#define HIVC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------------ status */
+enum hivc_status {
+    HIVC_OK = 0,
+    HIVC_E_TRUNCATED = 1,          /* bitstream.Truncated           (bitstream.py:49) */
+    HIVC_E_BAD_MAGIC = 2,          /* bitstream.BadMagic            (bitstream.py:41) */
+    HIVC_E_UNSUPPORTED_VERSION = 3,/* bitstream.UnsupportedVersion  (bitstream.py:45) */
+    HIVC_E_LENGTH_MISMATCH = 4,    /* bitstream.LengthMismatch      (bitstream.py:53) */
+    HIVC_E_CODEC = 5,              /* codec.CodecError              (codec.py:69) */
+    HIVC_E_ENTROPY = 6,            /* entropy.EntropyError          (entropy.py:31) */
+    HIVC_E_SUBDIVISION = 7,        /* subdivision.SubdivisionError  (subdivision.py:21) */
+    HIVC_E_INPAINTING = 8,         /* homogeneous.InpaintingError   (homogeneous.py:19) */
+    HIVC_E_CONVERGENCE = 9,        /* homogeneous.ConvergenceError  (homogeneous.py:23) */
+    HIVC_E_FLOW = 10,              /* flow.FlowError                (flow.py:36) */
+    HIVC_E_FRAME = 11,             /* frame.FrameError              (frame.py:15) */
+    HIVC_E_QUANTIZE = 12,          /* quantize.QuantizeError        (quantize.py:16) */
+    HIVC_E_BITSTREAM = 13,         /* bitstream.BitstreamError (generic header validation, bitstream.py:37,80-91) */
+    HIVC_E_PSEUDODIFF = 14,        /* pseudodiff.PseudodiffError    (pseudodiff.py:27) */
+    HIVC_E_TRUNCATED_STREAM = 15,  /* bits.TruncatedStream          (bits.py:6) */
+    HIVC_E_ARGUMENT = 20,          /* bad call arguments (ValueError) */
+    HIVC_E_CUDA = 21,              /* CUDA runtime failure (no device, launch error, ...) */
+    HIVC_E_NOMEM = 22
+};
+
+/* Thread-local message of the last failing call on this thread. */
+const char* hivc_last_error(void);
+/* Library build string (arch, flags). */
+const char* hivc_version(void);
+
+/* ------------------------------------------------------------------ context
+ * One context = one device + one CUDA stream + device scratch.  Contexts are
+ * independent; use one per host thread (runtime.map_tasks, runtime.py:37-43).
+ */
+typedef struct hivc_ctx hivc_ctx;
+int hivc_ctx_create(int device, hivc_ctx** out);
+int hivc_ctx_destroy(hivc_ctx* ctx);
+/* cudaStream_t the context launches on (as an opaque pointer). */
+void* hivc_ctx_stream(hivc_ctx* ctx);
+/* Wait for all work queued on the context's stream. */
+int hivc_ctx_synchronize(hivc_ctx* ctx);
+/* Number of device kernels this context has launched so far. */
+int64_t hivc_ctx_launch_count(hivc_ctx* ctx);
+
+/* ------------------------------------------------------------------ container
+ * Replaces bitstream.unpack_header / read_stream (bitstream.py:102-154).
+ */
+typedef struct hivc_stream_info {
+    int32_t width, height;
+    int32_t frame_count;
+    int32_t fps_num, fps_den;
+    int32_t gop_size;
+    int32_t channels;          /* 1 gray, 3 colour (RCT) */
+    int32_t intra_levels, flow_levels, residual_levels;
+    int32_t gop_count;
+} hivc_stream_info;
+int hivc_parse_header(const uint8_t* data, size_t len, hivc_stream_info* info);
+/* Frames per GOP record (the u16 at the head of each GOP payload, codec.py:494). */
+int hivc_gop_frame_counts(const uint8_t* data, size_t len, int32_t* counts, int32_t cap, int32_t* ngops);
+
+/* ------------------------------------------------------------------ entropy (host, bit-exact)
+ * Replaces entropy.decode_symbols (entropy.py:276-291).  Writes at most `cap`
+ * symbols; *count receives the stream's symbol count (call with cap=0 to size).
+ */
+int hivc_parse_symbols(const uint8_t* data, size_t len, size_t pos,
+                       int64_t* out, size_t cap, size_t* count, size_t* next_pos);
+/* Replaces entropy.decode_signed_values (entropy.py:311-338). */
+int hivc_parse_signed_values(const uint8_t* data, size_t len, size_t pos,
+                             int64_t* out, size_t cap, size_t* count, size_t* next_pos);
+/* Replaces subdivision.deserialize_tree + SubdivisionTree.leaves (subdivision.py:183-195, 53-69)
+ * and parse_mask (198-222): preorder leaf rectangles (x, y, w, h) of a tree
+ * over a (width x height) root, read from `nbits` bits of `data` starting at
+ * bit `bit_offset` (trees of coded residual tiles are concatenated, codec.py:298-303).
+ * Writes at most `cap` leaves (4 int32 each); *nleaves gets the true count,
+ * *bits_used the bits consumed. */
+int hivc_parse_tree(const uint8_t* data, size_t nbytes, uint64_t nbits, uint64_t bit_offset,
+                    int32_t width, int32_t height,
+                    int32_t* rects, size_t cap, size_t* nleaves, uint64_t* bits_used);
+
+/* ------------------------------------------------------------------ homogeneous diffusion inpainting
+ * Replaces homogeneous.solve_homogeneous (homogeneous.py:157-212): cascadic
+ * coarse-to-fine CG, replayed step for step on the GPU (float64).
+ * f, mask, u: device pointers (h*w).  level_iters/level_sizes: host arrays of
+ * capacity >= 32 receiving (coarse->fine) per-level pixel counts and CG
+ * iterations, *nlevels their length (stats["level_iterations"]).
+ * Returns HIVC_E_CONVERGENCE in strict mode when the final relative residual
+ * exceeds tol (u is still written).
+ */
+int hivc_homog_solve(hivc_ctx* ctx, const double* f, const uint8_t* mask, int32_t h, int32_t w,
+                     double tol, int32_t max_iter, int32_t strict,
+                     double* u, int32_t* level_sizes, int32_t* level_iters, int32_t* nlevels);
+
+/* ------------------------------------------------------------------ warp
+ * Replaces flow.warp_planes (flow.py:94-127): every plane sampled at
+ * (x+u, y+v), clamped bilinear, float64.  src/dst: host arrays of `nplanes`
+ * device pointers; u, v: device pointers.
+ */
+int hivc_warp(hivc_ctx* ctx, const double* const* src, int32_t nplanes, const double* u, const double* v,
+              int32_t h, int32_t w, double* const* dst);
+
+/* ------------------------------------------------------------------ block pseudodifferential residual
+ * Replaces pseudodiff.reconstruct_blocks (pseudodiff.py:275-279):
+ * out[i] = IDCT_AAN(eig * DCT_AAN(mc[i])) + a[i].  mc/out: device (n*64),
+ * a: device (n), eig: device (64) or NULL for greens_eigenvalues_harmonic().
+ */
+int hivc_block_reconstruct(hivc_ctx* ctx, const double* mc, const double* a, const double* eig,
+                           int32_t n, double* out);
+/* Replaces pseudodiff.solve_block_coefficients_batch (pseudodiff.py:243-263)
+ * for ANY mix of mask layouts: per block the bordered (K+1)^2 system
+ * [[G_KK,1],[1^T,0]][c;a] = [f_K;0] is solved in shared memory.
+ * f_blocks: device (n*64); masks: device (n) uint64, bit (y*8+x);
+ * c_out: device (n*64) — c of block i at its K mask positions, zero elsewhere
+ * (the scattered "M c" layout reconstruct_blocks consumes); a_out: device (n). */
+int hivc_block_fit(hivc_ctx* ctx, const double* f_blocks, const uint64_t* masks, int32_t n,
+                   double* c_out, double* a_out);
+
+/* ------------------------------------------------------------------ stream decode
+ * Replaces codec.decode (codec.py:484-563) for the GOP range [gop_begin, gop_end):
+ * frames are written as uint8 planes, layout [frame][channel][h][w] (gray: the
+ * Y plane; colour: R, G, B after rct_inverse, frame.py:84-93).  `out` is a host
+ * pointer when out_on_device == 0 (pinned memory recommended) else a device
+ * pointer.  stage_seconds (nullable, 8 doubles) receives the reference timing
+ * keys: intra_solve, flow_parse, warp, residual_parse, residual_transform,
+ * finalize, total (codec.py:509-562), then the device-side span of the call
+ * measured with CUDA events (first lane start -> last lane's final copy).
+ * gop_end < 0 means "to the last GOP".
+ */
+int hivc_decode(hivc_ctx* ctx, const uint8_t* data, size_t len, int32_t gop_begin, int32_t gop_end,
+                uint8_t* out, int32_t out_on_device, double* stage_seconds);
+/* Several streams in one call (e.g. the Y, Cb, Cr gray streams of a 4:2:0
+ * video): all (stream, GOP) pairs share the decode lanes.  Per-stream arrays;
+ * gop_begin/gop_end may be NULL (whole streams). */
+int hivc_decode_multi(hivc_ctx* ctx, int32_t nstreams, const uint8_t* const* data, const size_t* len,
+                      const int32_t* gop_begin, const int32_t* gop_end, uint8_t* const* out,
+                      int32_t out_on_device, double* stage_seconds);
+/* Host<->device bytes moved by this context's decodes so far. */
+int hivc_ctx_bytes(hivc_ctx* ctx, int64_t* h2d, int64_t* d2h);
+/* Per-frame CUDA-event stage breakdown on (default) or off (pure throughput runs). */
+int hivc_ctx_set_stage_timing(hivc_ctx* ctx, int32_t enable);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HIVC_B200_H */

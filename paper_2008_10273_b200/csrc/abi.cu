@@ -1,0 +1,265 @@
+// extern "C" entry points declared in include/hivc_b200.h.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "decode.h"
+#include "inpaint.h"
+#include "parse.h"
+#include "recon.h"
+
+struct hivc_ctx {
+    hivc::Context c;
+};
+
+namespace hivc {
+static thread_local std::string g_last_error;
+void set_last_error(const std::string& m) { g_last_error = m; }
+}  // namespace hivc
+
+using hivc::guarded;
+
+extern "C" {
+
+const char* hivc_last_error(void) { return hivc::g_last_error.c_str(); }
+
+const char* hivc_version(void) {
+    return "hivc_b200 1.0 (sm_100a, float64 replay of the reference decoder, -fmad=false)";
+}
+
+int hivc_ctx_create(int device, hivc_ctx** out) {
+    return guarded([&] {
+        if (!out) hivc::fail(HIVC_E_ARGUMENT, "null out pointer");
+        int n = 0;
+        cudaError_t e = cudaGetDeviceCount(&n);
+        if (e != cudaSuccess || n == 0)
+            hivc::fail(HIVC_E_CUDA, std::string("no CUDA device available: ") + cudaGetErrorString(e));
+        if (device < 0 || device >= n) hivc::fail(HIVC_E_ARGUMENT, "bad device index");
+        CUDA_CHECK(cudaSetDevice(device));
+        cudaDeviceProp prop;
+        CUDA_CHECK(cudaGetDeviceProperties(&prop, device));
+        if (prop.major != 10)
+            hivc::fail(HIVC_E_CUDA, "this library is built for sm_100a (B200); device is sm_" +
+                                        std::to_string(prop.major) + std::to_string(prop.minor));
+        auto* c = new hivc_ctx();
+        c->c.device = device;
+        CUDA_CHECK(cudaStreamCreateWithFlags(&c->c.stream, cudaStreamNonBlocking));
+        CUDA_CHECK(cudaMalloc(&c->c.d_status, 64 * sizeof(int)));
+        *out = c;
+    });
+}
+
+int hivc_ctx_destroy(hivc_ctx* ctx) {
+    return guarded([&] { delete ctx; });
+}
+
+void* hivc_ctx_stream(hivc_ctx* ctx) { return ctx ? (void*)ctx->c.stream : nullptr; }
+
+int hivc_ctx_synchronize(hivc_ctx* ctx) {
+    return guarded([&] {
+        CUDA_CHECK(cudaSetDevice(ctx->c.device));
+        CUDA_CHECK(cudaStreamSynchronize(ctx->c.stream));
+    });
+}
+
+int64_t hivc_ctx_launch_count(hivc_ctx* ctx) { return ctx ? ctx->c.launches.load() : 0; }
+
+int hivc_parse_header(const uint8_t* data, size_t len, hivc_stream_info* info) {
+    return guarded([&] {
+        hivc::StreamHeader h = hivc::parse_header(data, len);
+        std::vector<std::pair<size_t, size_t>> gops;
+        hivc::split_gops(data, len, h, gops);
+        info->width = h.width;
+        info->height = h.height;
+        info->frame_count = h.frame_count;
+        info->fps_num = h.fps_num;
+        info->fps_den = h.fps_den;
+        info->gop_size = h.gop_size;
+        info->channels = h.channels;
+        info->intra_levels = h.intra_levels;
+        info->flow_levels = h.flow_levels;
+        info->residual_levels = h.residual_levels;
+        info->gop_count = (int32_t)gops.size();
+    });
+}
+
+int hivc_gop_frame_counts(const uint8_t* data, size_t len, int32_t* counts, int32_t cap, int32_t* ngops) {
+    return guarded([&] {
+        std::vector<int32_t> c;
+        hivc::gop_frame_counts(data, len, c);
+        *ngops = (int32_t)c.size();
+        for (int32_t i = 0; i < cap && i < (int32_t)c.size(); ++i) counts[i] = c[i];
+    });
+}
+
+static int parse_sym_common(bool signed_vals, const uint8_t* data, size_t len, size_t pos, int64_t* out, size_t cap,
+                            size_t* count, size_t* next_pos) {
+    return guarded([&] {
+        std::vector<int32_t> v;
+        size_t np = signed_vals ? hivc::decode_signed_values(data, len, pos, v) : hivc::decode_symbols(data, len, pos, v);
+        *count = v.size();
+        if (next_pos) *next_pos = np;
+        for (size_t i = 0; i < cap && i < v.size(); ++i) out[i] = v[i];
+    });
+}
+
+int hivc_parse_symbols(const uint8_t* data, size_t len, size_t pos, int64_t* out, size_t cap, size_t* count,
+                       size_t* next_pos) {
+    return parse_sym_common(false, data, len, pos, out, cap, count, next_pos);
+}
+
+int hivc_parse_signed_values(const uint8_t* data, size_t len, size_t pos, int64_t* out, size_t cap, size_t* count,
+                             size_t* next_pos) {
+    return parse_sym_common(true, data, len, pos, out, cap, count, next_pos);
+}
+
+int hivc_parse_tree(const uint8_t* data, size_t nbytes, uint64_t nbits, uint64_t bit_offset, int32_t width,
+                    int32_t height, int32_t* rects, size_t cap, size_t* nleaves, uint64_t* bits_used) {
+    return guarded([&] {
+        hivc::BitReader rd(data, nbytes, nbits);
+        rd.pos = bit_offset;
+        std::vector<hivc::Rect> leaves;
+        hivc::parse_tree_leaves(rd, width, height, leaves);
+        *nleaves = leaves.size();
+        if (bits_used) *bits_used = rd.pos - bit_offset;
+        for (size_t i = 0; i < cap && i < leaves.size(); ++i) {
+            rects[4 * i] = leaves[i].x;
+            rects[4 * i + 1] = leaves[i].y;
+            rects[4 * i + 2] = leaves[i].w;
+            rects[4 * i + 3] = leaves[i].h;
+        }
+    });
+}
+
+int hivc_homog_solve(hivc_ctx* ctx, const double* f, const uint8_t* mask, int32_t h, int32_t w, double tol,
+                     int32_t max_iter, int32_t strict, double* u, int32_t* level_sizes, int32_t* level_iters,
+                     int32_t* nlevels) {
+    return guarded([&] {
+        if (!ctx) hivc::fail(HIVC_E_ARGUMENT, "null context");
+        if (h < 1 || w < 1) hivc::fail(HIVC_E_INPAINTING, "plane/mask shape mismatch");
+        if (strict && !(tol > 0)) hivc::fail(HIVC_E_INPAINTING, "tol must be positive");
+        if (max_iter < 0) max_iter = 0;
+        hivc::Context& C = ctx->c;
+        CUDA_CHECK(cudaSetDevice(C.device));
+        // empty-mask check (homogeneous.py:177-178)
+        {
+            size_t n = (size_t)h * w;
+            // reuse the workspace byte buffer? keep it simple: reduce on host copy of the mask
+            std::vector<uint8_t> hm(n);
+            CUDA_CHECK(cudaMemcpyAsync(hm.data(), mask, n, cudaMemcpyDeviceToHost, C.stream));
+            CUDA_CHECK(cudaStreamSynchronize(C.stream));
+            bool any = false;
+            for (uint8_t b : hm)
+                if (b) {
+                    any = true;
+                    break;
+                }
+            if (!any) hivc::fail(HIVC_E_INPAINTING, "empty inpainting mask");
+        }
+        C.ws.reserve(h, w, C.device);
+        int64_t launches = 0;
+        int L = hivc::solve_homogeneous_async(C.ws, C.stream, f, mask, h, w, tol, max_iter, u, &launches);
+        std::vector<std::pair<int, int>> shapes;
+        hivc::pyramid_shapes(h, w, shapes);
+        std::vector<int> it(L);
+        CUDA_CHECK(cudaMemcpyAsync(it.data(), C.ws.iters, L * sizeof(int), cudaMemcpyDeviceToHost, C.stream));
+        CUDA_CHECK(cudaStreamSynchronize(C.stream));
+        if (nlevels) *nlevels = L;
+        for (int i = 0; i < L && i < 32; ++i) {
+            auto s = shapes[L - 1 - i];
+            if (level_sizes) level_sizes[i] = s.first * s.second;
+            if (level_iters) level_iters[i] = it[i];
+        }
+        if (strict) {
+            double rel = hivc::strict_relative_residual(C.ws, C.stream, u, f, mask, h, w, &launches);
+            if (rel >= 0 && rel > tol) {
+                char buf[128];
+                snprintf(buf, sizeof(buf), "relative residual %.3e > tol %.3e", rel, tol);
+                C.launches += launches;
+                hivc::fail(HIVC_E_CONVERGENCE, buf);
+            }
+        }
+        C.launches += launches;
+    });
+}
+
+int hivc_warp(hivc_ctx* ctx, const double* const* src, int32_t nplanes, const double* u, const double* v, int32_t h,
+              int32_t w, double* const* dst) {
+    return guarded([&] {
+        if (!ctx) hivc::fail(HIVC_E_ARGUMENT, "null context");
+        hivc::Context& C = ctx->c;
+        CUDA_CHECK(cudaSetDevice(C.device));
+        hivc::launch_warp(src, nplanes, u, v, h, w, dst, C.stream);
+        C.launches += (nplanes + 7) / 8;
+        CUDA_CHECK(cudaStreamSynchronize(C.stream));
+    });
+}
+
+int hivc_block_reconstruct(hivc_ctx* ctx, const double* mc, const double* a, const double* eig, int32_t n,
+                           double* out) {
+    return guarded([&] {
+        if (!ctx) hivc::fail(HIVC_E_ARGUMENT, "null context");
+        hivc::Context& C = ctx->c;
+        CUDA_CHECK(cudaSetDevice(C.device));
+        hivc::launch_block_reconstruct(mc, a, eig, n, out, C.stream);
+        C.launches += n > 0;
+        CUDA_CHECK(cudaStreamSynchronize(C.stream));
+    });
+}
+
+int hivc_block_fit(hivc_ctx* ctx, const double* f_blocks, const uint64_t* masks, int32_t n, double* c_out,
+                   double* a_out) {
+    return guarded([&] {
+        if (!ctx) hivc::fail(HIVC_E_ARGUMENT, "null context");
+        hivc::Context& C = ctx->c;
+        CUDA_CHECK(cudaSetDevice(C.device));
+        CUDA_CHECK(cudaMemsetAsync(C.d_status, 0, sizeof(int), C.stream));
+        hivc::launch_block_fit(f_blocks, masks, n, c_out, a_out, C.d_status, C.stream);
+        C.launches += n > 0;
+        int st = 0;
+        CUDA_CHECK(cudaMemcpyAsync(&st, C.d_status, sizeof(int), cudaMemcpyDeviceToHost, C.stream));
+        CUDA_CHECK(cudaStreamSynchronize(C.stream));
+        if (st == 1) hivc::fail(HIVC_E_PSEUDODIFF, "block mask needs at least one point");
+        if (st == 2) hivc::fail(HIVC_E_PSEUDODIFF, "singular coefficient system");
+    });
+}
+
+int hivc_decode(hivc_ctx* ctx, const uint8_t* data, size_t len, int32_t gop_begin, int32_t gop_end, uint8_t* out,
+                int32_t out_on_device, double* stage_seconds) {
+    return guarded([&] {
+        if (!ctx) hivc::fail(HIVC_E_ARGUMENT, "null context");
+        CUDA_CHECK(cudaSetDevice(ctx->c.device));
+        int gb = gop_begin, ge = gop_end;
+        hivc::decode_streams(ctx->c, 1, &data, &len, &gb, &ge, &out, out_on_device != 0, stage_seconds);
+    });
+}
+
+int hivc_decode_multi(hivc_ctx* ctx, int32_t nstreams, const uint8_t* const* data, const size_t* len,
+                      const int32_t* gop_begin, const int32_t* gop_end, uint8_t* const* out, int32_t out_on_device,
+                      double* stage_seconds) {
+    return guarded([&] {
+        if (!ctx) hivc::fail(HIVC_E_ARGUMENT, "null context");
+        if (nstreams < 1) hivc::fail(HIVC_E_ARGUMENT, "no streams");
+        CUDA_CHECK(cudaSetDevice(ctx->c.device));
+        hivc::decode_streams(ctx->c, nstreams, data, len, gop_begin, gop_end, out, out_on_device != 0, stage_seconds);
+    });
+}
+
+int hivc_ctx_bytes(hivc_ctx* ctx, int64_t* h2d, int64_t* d2h) {
+    return guarded([&] {
+        if (!ctx) hivc::fail(HIVC_E_ARGUMENT, "null context");
+        if (h2d) *h2d = ctx->c.h2d_bytes.load();
+        if (d2h) *d2h = ctx->c.d2h_bytes.load();
+    });
+}
+
+int hivc_ctx_set_stage_timing(hivc_ctx* ctx, int32_t enable) {
+    return guarded([&] {
+        if (!ctx) hivc::fail(HIVC_E_ARGUMENT, "null context");
+        ctx->c.stage_events = enable != 0;
+    });
+}
+
+}  // extern "C"

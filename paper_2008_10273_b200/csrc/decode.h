@@ -1,0 +1,62 @@
+// Stream decoder: GOP-parallel host parsing feeding per-lane CUDA streams.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <memory>
+#include <vector>
+
+#include "inpaint.h"
+#include "parse.h"
+#include "recon.h"
+
+namespace hivc {
+
+// One decode lane: a CUDA stream, a solver workspace and double-buffered
+// staging (pinned host + device) for the compact frame descriptions.
+struct Lane {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    InpaintWorkspace ws;
+    size_t plane_px = 0;
+    int chans = 0;
+    double* f[3] = {nullptr, nullptr, nullptr};
+    uint8_t* m[2] = {nullptr, nullptr};
+    double* u[3] = {nullptr, nullptr, nullptr};
+    int16_t* ring[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
+    uint8_t* host_stage[2] = {nullptr, nullptr};
+    uint8_t* dev_stage[2] = {nullptr, nullptr};
+    size_t stage_cap[2] = {0, 0};
+    cudaEvent_t staged[2] = {nullptr, nullptr};
+    uint8_t* gop_out[2] = {nullptr, nullptr};  // device frame buffers when output goes to the host
+    size_t gop_out_cap = 0;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    void reserve_planes(int h, int w, int channels);
+    void reserve_stage(int slot, size_t bytes);
+    void reserve_gop_out(size_t bytes);
+    ~Lane();
+};
+
+struct Context {
+    int device = 0;
+    cudaStream_t stream = nullptr;  // function-level API stream
+    InpaintWorkspace ws;            // function-level solver scratch
+    std::vector<std::unique_ptr<Lane>> lanes;
+    std::atomic<int64_t> launches{0};
+    std::atomic<int64_t> h2d_bytes{0}, d2h_bytes{0};
+    bool stage_events = true;  // per-frame CUDA events for the stage breakdown
+    int* d_status = nullptr;
+    ~Context();
+};
+
+// Decode GOP ranges of several streams in one pass (one lane per host thread,
+// work items = (stream, GOP)).  stage_seconds (nullable, 8 doubles): the 7
+// reference timing keys + the device-side span (first lane start -> last lane end).
+void decode_streams(Context& ctx, int nstreams, const uint8_t* const* data, const size_t* len, const int* gop_begin,
+                    const int* gop_end, uint8_t* const* out, bool out_on_device, double* stage_seconds);
+
+// Frames per GOP (u16 at the head of each GOP payload, codec.py:494).
+void gop_frame_counts(const uint8_t* data, size_t len, std::vector<int32_t>& counts);
+
+}  // namespace hivc

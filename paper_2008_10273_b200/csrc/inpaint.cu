@@ -1,0 +1,429 @@
+// Homogeneous-diffusion inpainting on the GPU: the reference's cascadic
+// conjugate-gradient scheme (homogeneous.py:55-212) replayed step for step.
+//
+//  * pyramid: 2x2 ceiling-halving restriction, any-child mask, mean of the
+//    set children (homogeneous.py:96-130) — one kernel per level;
+//  * per level one persistent kernel runs the whole CG: setup (prolongation
+//    of the coarser solution, x0 * interior, b = L(u_D) * interior,
+//    r = b - A x), then the iteration loop with both global dot products per
+//    iteration reduced in a fixed order, so every CTA takes the same
+//    alpha/beta/stop decisions and the result is bit-reproducible;
+//  * large levels run on one CTA per SM with a software grid barrier
+//    (cooperative launch); small levels run in a single CTA with
+//    __syncthreads only.
+// Float64 throughout, FMA contraction off, sums associated as in numpy.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "device.cuh"
+#include "inpaint.h"
+
+namespace hivc {
+
+constexpr int kCoarsest = 16;      // homogeneous.py:15
+constexpr double kLevelTol = 1e-4;  // homogeneous.py:16
+constexpr int kThreads = 1024;
+constexpr int kSingleCtaMaxPx = 16384;
+
+// ---------------------------------------------------------------- pyramid
+
+__global__ void restrict_kernel(const double* __restrict__ f, const uint8_t* __restrict__ m, int h, int w,
+                                double* __restrict__ fc, uint8_t* __restrict__ mc, int hc, int wc) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= hc * wc) return;
+    int cy = i / wc, cx = i % wc;
+    int r0 = 2 * cy, c0 = 2 * cx;
+    bool hr = r0 + 1 < h, hcol = c0 + 1 < w;
+    // np.add.reduceat over rows, then over columns (homogeneous.py:121-122)
+    auto at = [&](int r, int c, int kind) -> double {
+        size_t k = (size_t)r * w + c;
+        bool mk = m[k] != 0;
+        switch (kind) {
+            case 0: return mk ? 1.0 : 0.0;
+            case 1: return mk ? f[k] : 0.0;
+            case 2: return 1.0;
+            default: return f[k];
+        }
+    };
+    double tot[4];
+#pragma unroll
+    for (int kind = 0; kind < 4; ++kind) {
+        double s0 = hr ? at(r0, c0, kind) + at(r0 + 1, c0, kind) : at(r0, c0, kind);
+        double t = s0;
+        if (hcol) {
+            double s1 = hr ? at(r0, c0 + 1, kind) + at(r0 + 1, c0 + 1, kind) : at(r0, c0 + 1, kind);
+            t = s0 + s1;
+        }
+        tot[kind] = t;
+    }
+    double avg = tot[3] / tot[2];
+    bool cm = tot[0] > 0.0;
+    fc[i] = cm ? tot[1] / fmax(tot[0], 1.0) : avg;
+    mc[i] = cm ? 1 : 0;
+}
+
+// ---------------------------------------------------------------- CG level kernel
+
+struct CgParams {
+    int h, w, n;
+    const double* f;
+    const uint8_t* m;
+    const double* uc;  // coarser solution (nullptr at the coarsest level)
+    int hc, wc;
+    double* x;
+    double* r;
+    double* pa;
+    double* pb;
+    double* ap;
+    double* u;  // level solution out
+    double tol;
+    int max_iter;
+    int finest;
+    double* partials;  // [gridDim.x * 4]
+    unsigned int* bar;
+    int* iters;         // out: iterations of this level
+    double* margin;     // out: min |sqrt(rs)-tol*bn|/(tol*bn) over stop tests (parity diagnostics)
+};
+
+__device__ __forceinline__ double prolong_at(const CgParams& P, int y, int xx) {
+    // homogeneous.py:133-154, evaluated at one fine pixel
+    double ys = ((double)y + 0.5) * ((double)P.hc / (double)P.h) - 0.5;
+    double xs = ((double)xx + 0.5) * ((double)P.wc / (double)P.w) - 0.5;
+    ys = fmin(fmax(ys, 0.0), (double)(P.hc - 1));
+    xs = fmin(fmax(xs, 0.0), (double)(P.wc - 1));
+    int y0 = (int)floor(ys), x0 = (int)floor(xs);
+    int y1 = min(y0 + 1, P.hc - 1), x1 = min(x0 + 1, P.wc - 1);
+    double wy = ys - (double)y0, wx = xs - (double)x0;
+    const double* c = P.uc;
+    double c00 = __ldg(c + (size_t)y0 * P.wc + x0), c01 = __ldg(c + (size_t)y0 * P.wc + x1);
+    double c10 = __ldg(c + (size_t)y1 * P.wc + x0), c11 = __ldg(c + (size_t)y1 * P.wc + x1);
+    return (1 - wy) * ((1 - wx) * c00 + wx * c01) + wy * ((1 - wx) * c10 + wx * c11);
+}
+
+// 5-point reflecting Laplacian of a field given by an accessor (homogeneous.py:27-43).
+template <class G>
+__device__ __forceinline__ double lap_at(int y, int xx, int h, int w, double c, G get) {
+    double north = y > 0 ? get(y - 1, xx) : c;
+    double south = y < h - 1 ? get(y + 1, xx) : c;
+    double west = xx > 0 ? get(y, xx - 1) : c;
+    double east = xx < w - 1 ? get(y, xx + 1) : c;
+    return (((c * -4.0 + north) + south) + west) + east;
+}
+
+template <bool kGrid, int NV>
+__device__ __forceinline__ void reduce(double (&v)[NV], double* sh, const CgParams& P) {
+    block_sum<NV>(v, sh);
+    if (!kGrid) return;
+    if (threadIdx.x == 0)
+#pragma unroll
+        for (int k = 0; k < NV; ++k) P.partials[blockIdx.x * 4 + k] = v[k];
+    grid_barrier(P.bar, gridDim.x);
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x < 32) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            double s = 0.0;
+            for (int g = lane; g < (int)gridDim.x; g += 32) s += __ldcg(P.partials + g * 4 + k);
+            s = warp_sum(s);
+            if (lane == 0) sh[k * 32] = s;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < NV; ++k) v[k] = sh[k * 32];
+    __syncthreads();
+}
+
+template <bool kGrid>
+__global__ void __launch_bounds__(kThreads, 1) cg_level_kernel(CgParams P) {
+    __shared__ double sh[4 * 32];
+    __shared__ double s_mean;
+    __shared__ double s_vals[kCoarsest * kCoarsest];
+    const int h = P.h, w = P.w, n = P.n;
+    const int stride = gridDim.x * blockDim.x;
+    const int t0 = blockIdx.x * blockDim.x + threadIdx.x;
+    const double* __restrict__ f = P.f;
+    const uint8_t* __restrict__ m = P.m;
+
+    // coarsest level: x0 = mean(f[mask]) with numpy's pairwise sum (homogeneous.py:188)
+    if (P.uc == nullptr) {
+        if (threadIdx.x == 0) {
+            int c = 0;
+            for (int i = 0; i < n; ++i)
+                if (m[i]) s_vals[c++] = f[i];
+            s_mean = np_pairwise_sum(s_vals, c) / (double)c;
+        }
+        __syncthreads();
+    }
+    const double mean0 = P.uc == nullptr ? s_mean : 0.0;
+    auto x0_at = [&](int y, int xx) -> double { return P.uc ? prolong_at(P, y, xx) : mean0; };
+
+    // ---- setup: x = x0*interior, b = L(u_D)*interior, r = b - A x (homogeneous.py:64-77)
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};  // r.r, b.b, |f_mask|^2, #interior
+    for (int i = t0; i < n; i += stride) {
+        int y = i / w, xx = i % w;
+        bool mi = m[i] != 0;
+        double interior = mi ? 0.0 : 1.0;
+        auto ud = [&](int yy, int xq) -> double {
+            size_t k = (size_t)yy * w + xq;
+            return m[k] ? __ldg(f + k) : 0.0;
+        };
+        auto xv = [&](int yy, int xq) -> double {
+            size_t k = (size_t)yy * w + xq;
+            return x0_at(yy, xq) * (m[k] ? 0.0 : 1.0);
+        };
+        double udi = mi ? __ldg(f + i) : 0.0;
+        double xi = x0_at(y, xx) * interior;
+        double b = lap_at(y, xx, h, w, udi, ud) * interior;
+        double ax = -lap_at(y, xx, h, w, xi, xv) * interior;
+        double ri = b - ax;
+        P.x[i] = xi;
+        P.r[i] = ri;
+        P.pa[i] = ri;
+        acc[0] += ri * ri;
+        acc[1] += b * b;
+        acc[2] += mi ? udi * udi : 0.0;
+        acc[3] += interior;
+    }
+    reduce<kGrid, 4>(acc, sh, P);
+    double rs = acc[0];
+    double bn;
+    bool all_mask = acc[3] == 0.0;
+    if (P.finest && acc[2] != 0.0)
+        bn = sqrt(acc[2]);  // ||f restricted to mask|| (homogeneous.py:198)
+    else
+        bn = sqrt(acc[1]);  // ||b||
+    int it = 0;
+    double margin = 1e300;
+    double* pold = P.pa;
+    double* pnew = P.pb;
+    if (!all_mask && bn != 0.0) {
+        double beta = 0.0;  // first iteration: p = r
+        for (int k = 1; k <= P.max_iter; ++k) {
+            it = k;
+            // phase 1: p = r + beta p (fused), ap = -L(p)*interior, p.ap
+            double d[1] = {0.0};
+            for (int i = t0; i < n; i += stride) {
+                int y = i / w, xx = i % w;
+                auto pv = [&](int yy, int xq) -> double {
+                    size_t q = (size_t)yy * w + xq;
+                    return __ldcg(P.r + q) + beta * __ldcg(pold + q);
+                };
+                double pi = pv(y, xx);
+                double interior = m[i] ? 0.0 : 1.0;
+                double api = -lap_at(y, xx, h, w, pi, pv) * interior;
+                pnew[i] = pi;
+                P.ap[i] = api;
+                d[0] += pi * api;
+            }
+            reduce<kGrid, 1>(d, sh, P);
+            double pap = d[0];
+            if (pap <= 0.0 || rs < 1e-300) break;
+            double alpha = rs / pap;
+            // phase 2: x += alpha p, r -= alpha ap, r.r
+            double e[1] = {0.0};
+            for (int i = t0; i < n; i += stride) {
+                double pi = pnew[i];
+                double xi = P.x[i] + alpha * pi;
+                double ri = __ldcg(P.r + i) - alpha * P.ap[i];
+                P.x[i] = xi;
+                P.r[i] = ri;
+                e[0] += ri * ri;
+            }
+            reduce<kGrid, 1>(e, sh, P);
+            double rs1 = e[0];
+            double lhs = sqrt(rs1), rhs = P.tol * bn;
+            if (rhs > 0.0) margin = fmin(margin, fabs(lhs - rhs) / rhs);
+            if (lhs <= rhs) break;
+            beta = rs1 / rs;
+            rs = rs1;
+            double* t = pold;
+            pold = pnew;
+            pnew = t;
+        }
+    }
+    // level solution: u = u_D + x (or a copy of f when the mask is full)
+    for (int i = t0; i < n; i += stride) {
+        bool mi = m[i] != 0;
+        double udi = mi ? __ldg(f + i) : 0.0;
+        P.u[i] = all_mask ? __ldg(f + i) : udi + P.x[i];
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        *P.iters = it;
+        if (P.margin) *P.margin = margin;
+    }
+}
+
+// ---------------------------------------------------------------- strict residual check
+
+__global__ void residual_partials(const double* __restrict__ u, const double* __restrict__ f,
+                                  const uint8_t* __restrict__ m, int h, int w, double* partials) {
+    __shared__ double sh[2 * 32];
+    double acc[2] = {0.0, 0.0};
+    int n = h * w;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        int y = i / w, xx = i % w;
+        double res;
+        if (m[i]) {
+            res = u[i] - f[i];
+            acc[1] += f[i] * f[i];
+        } else {
+            res = lap_at(y, xx, h, w, u[i], [&](int yy, int xq) { return u[(size_t)yy * w + xq]; });
+        }
+        acc[0] += res * res;
+    }
+    block_sum<2>(acc, sh);
+    if (threadIdx.x == 0) {
+        partials[blockIdx.x * 2] = acc[0];
+        partials[blockIdx.x * 2 + 1] = acc[1];
+    }
+}
+
+// ---------------------------------------------------------------- host side
+
+void pyramid_shapes(int h, int w, std::vector<std::pair<int, int>>& shapes) {
+    shapes.clear();
+    shapes.push_back({h, w});
+    while (std::max(shapes.back().first, shapes.back().second) > kCoarsest) {
+        auto s = shapes.back();
+        shapes.push_back({(s.first + 1) / 2, (s.second + 1) / 2});
+    }
+}
+
+void InpaintWorkspace::reserve(int h, int w, int dev) {
+    size_t n = (size_t)h * w;
+    if (n <= cap_px && dev == device) return;
+    release();
+    device = dev;
+    cudaDeviceProp prop;
+    CUDA_CHECK(cudaGetDeviceProperties(&prop, dev));
+    num_sms = prop.multiProcessorCount;
+    int occ = 0;
+    CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cg_level_kernel<true>, kThreads, 0));
+    grid_ctas = occ >= 1 ? num_sms : 0;
+    // finest-level vectors + every coarser level's f, m, u
+    std::vector<std::pair<int, int>> shapes;
+    pyramid_shapes(h, w, shapes);
+    size_t coarse = 0;
+    for (size_t l = 1; l < shapes.size(); ++l) coarse += (size_t)shapes[l].first * shapes[l].second;
+    size_t nd = 5 * n + 2 * coarse + n /* u of level 0 scratch */;
+    CUDA_CHECK(cudaMalloc(&dbl, nd * sizeof(double)));
+    CUDA_CHECK(cudaMalloc(&bytes, coarse + 64));
+    CUDA_CHECK(cudaMalloc(&partials, (size_t)std::max(grid_ctas, 1) * 4 * sizeof(double) + 64 * sizeof(double)));
+    CUDA_CHECK(cudaMalloc(&bar, 64 * sizeof(unsigned int)));
+    CUDA_CHECK(cudaMemset(bar, 0, 64 * sizeof(unsigned int)));
+    CUDA_CHECK(cudaMalloc(&iters, 64 * sizeof(int)));
+    CUDA_CHECK(cudaMalloc(&margins, 64 * sizeof(double)));
+    cap_px = n;
+    cap_coarse = coarse;
+}
+
+void InpaintWorkspace::release() {
+    if (dbl) cudaFree(dbl);
+    if (bytes) cudaFree(bytes);
+    if (partials) cudaFree(partials);
+    if (bar) cudaFree(bar);
+    if (iters) cudaFree(iters);
+    if (margins) cudaFree(margins);
+    dbl = nullptr;
+    bytes = nullptr;
+    partials = nullptr;
+    bar = nullptr;
+    iters = nullptr;
+    margins = nullptr;
+    cap_px = 0;
+}
+
+int solve_homogeneous_async(InpaintWorkspace& ws, cudaStream_t s, const double* f, const uint8_t* m, int h, int w,
+                            double tol, int max_iter, double* u_out, int64_t* launches) {
+    std::vector<std::pair<int, int>> shapes;
+    pyramid_shapes(h, w, shapes);
+    const int L = (int)shapes.size();
+    size_t n0 = (size_t)h * w;
+    double* x = ws.dbl;
+    double* r = x + n0;
+    double* pa = r + n0;
+    double* pb = pa + n0;
+    double* ap = pb + n0;
+    double* cur = ap + n0;  // coarse f / u storage
+    uint8_t* cm = ws.bytes;
+    std::vector<const double*> lf(L);
+    std::vector<const uint8_t*> lm(L);
+    std::vector<double*> lu(L);
+    lf[0] = f;
+    lm[0] = m;
+    lu[0] = u_out;
+    for (int l = 1; l < L; ++l) {
+        size_t nl = (size_t)shapes[l].first * shapes[l].second;
+        double* fl = cur;
+        cur += nl;
+        lu[l] = cur;
+        cur += nl;
+        lf[l] = fl;
+        lm[l] = cm;
+        cm += nl;
+        int nb = (int)((nl + 255) / 256);
+        restrict_kernel<<<nb, 256, 0, s>>>(lf[l - 1], lm[l - 1], shapes[l - 1].first, shapes[l - 1].second, fl,
+                                           const_cast<uint8_t*>(lm[l]), shapes[l].first, shapes[l].second);
+        ++*launches;
+    }
+    CUDA_CHECK(cudaGetLastError());
+    for (int l = L - 1; l >= 0; --l) {
+        CgParams P;
+        P.h = shapes[l].first;
+        P.w = shapes[l].second;
+        P.n = P.h * P.w;
+        P.f = lf[l];
+        P.m = lm[l];
+        P.uc = l == L - 1 ? nullptr : lu[l + 1];
+        P.hc = l == L - 1 ? 0 : shapes[l + 1].first;
+        P.wc = l == L - 1 ? 0 : shapes[l + 1].second;
+        P.x = x;
+        P.r = r;
+        P.pa = pa;
+        P.pb = pb;
+        P.ap = ap;
+        P.u = lu[l];
+        P.tol = l == 0 ? tol : std::max(kLevelTol, tol);
+        P.max_iter = max_iter;
+        P.finest = l == 0;
+        P.partials = ws.partials;
+        P.bar = ws.bar;
+        P.iters = ws.iters + (L - 1 - l);
+        P.margin = ws.margins + (L - 1 - l);
+        if (P.n <= kSingleCtaMaxPx || ws.grid_ctas == 0) {
+            cg_level_kernel<false><<<1, kThreads, 0, s>>>(P);
+        } else {
+            void* args[] = {&P};
+            CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)cg_level_kernel<true>, dim3(ws.grid_ctas),
+                                                   dim3(kThreads), args, 0, s));
+        }
+        ++*launches;
+        CUDA_CHECK(cudaGetLastError());
+    }
+    return L;
+}
+
+double strict_relative_residual(InpaintWorkspace& ws, cudaStream_t s, const double* u, const double* f,
+                                const uint8_t* m, int h, int w, int64_t* launches) {
+    int nb = std::min(1024, (h * w + 255) / 256);
+    residual_partials<<<nb, 256, 0, s>>>(u, f, m, h, w, ws.partials);
+    ++*launches;
+    CUDA_CHECK(cudaGetLastError());
+    std::vector<double> host((size_t)nb * 2);
+    CUDA_CHECK(cudaMemcpyAsync(host.data(), ws.partials, host.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    double rr = 0.0, ff = 0.0;
+    for (int b = 0; b < nb; ++b) {
+        rr += host[2 * b];
+        ff += host[2 * b + 1];
+    }
+    double den = std::sqrt(ff);
+    double num = std::sqrt(rr);
+    // homogeneous.py:206-211
+    return den > 0 ? num / den : -1.0;
+}
+
+}  // namespace hivc

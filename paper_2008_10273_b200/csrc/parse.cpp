@@ -1,0 +1,416 @@
+// Bit-exact host parsing of HIVC payloads.  Reference citations per function.
+#include "parse.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+namespace hivc {
+
+static inline uint32_t rd_u32(const uint8_t* p) {
+    uint32_t v;
+    std::memcpy(&v, p, 4);
+    return v;
+}
+static inline uint16_t rd_u16(const uint8_t* p) {
+    uint16_t v;
+    std::memcpy(&v, p, 2);
+    return v;
+}
+
+uint64_t read_uvarint(const uint8_t* d, size_t len, size_t& pos) {  // bits.py:95-108
+    uint64_t v = 0;
+    int shift = 0;
+    while (true) {
+        if (pos >= len) fail(HIVC_E_TRUNCATED_STREAM, "varint runs past end of buffer");
+        uint8_t b = d[pos++];
+        if (shift == 63 && (b & 0x7F) > 1) v = ~0ull;  // >= 2^64: saturate (only ever fails later checks)
+        else if (shift < 64) v |= (uint64_t)(b & 0x7F) << shift;
+        if (!(b & 0x80)) return v;
+        shift += 7;
+        if (shift > 63) fail(HIVC_E_ARGUMENT, "varint too long");
+    }
+}
+
+void FseTable::build(const std::vector<uint64_t>& counts, int tl) {  // entropy.py:108-130
+    table_log = tl;
+    const uint32_t size = 1u << tl;
+    uint64_t total = 0;
+    for (uint64_t c : counts) {
+        total += c;
+        if (c > size || total > size) fail(HIVC_E_ENTROPY, "normalized counts must sum to table size");
+    }
+    if (total != size) fail(HIVC_E_ENTROPY, "normalized counts must sum to table size");
+    const uint32_t step = (size >> 1) + (size >> 3) + 3;
+    sym.assign(size, 0);
+    x.assign(size, 0);
+    nb.assign(size, 0);
+    uint32_t k = 0;
+    for (size_t s = 0; s < counts.size(); ++s)
+        for (uint64_t j = 0; j < counts[s]; ++j) sym[(k++ * step) & (size - 1)] = (uint16_t)s;
+    std::vector<uint32_t> next(counts.size());
+    for (size_t s = 0; s < counts.size(); ++s) next[s] = (uint32_t)counts[s];
+    for (uint32_t slot = 0; slot < size; ++slot) {
+        uint32_t xv = next[sym[slot]]++;
+        x[slot] = xv;
+        int bl = 32 - __builtin_clz(xv);  // xv >= 1
+        nb[slot] = (uint8_t)(tl + 1 - bl);
+    }
+}
+
+size_t decode_symbols(const uint8_t* d, size_t len, size_t pos, std::vector<int32_t>& out) {
+    // header: entropy.py:227-240
+    if (pos >= len) fail(HIVC_E_TRUNCATED_STREAM, "entropy payload truncated");
+    int tl = d[pos++];
+    if (tl < 5 || tl > 12) fail(HIVC_E_ENTROPY, "bad table_log " + std::to_string(tl));
+    uint64_t nsym = read_uvarint(d, len, pos);
+    if (nsym == 0 || nsym > (1ull << tl)) fail(HIVC_E_ENTROPY, "bad alphabet size");
+    std::vector<uint64_t> counts(nsym);
+    for (uint64_t i = 0; i < nsym; ++i) counts[i] = read_uvarint(d, len, pos);
+    // body: entropy.py:276-291
+    if (pos + 10 > len) fail(HIVC_E_TRUNCATED_STREAM, "entropy payload truncated");
+    uint32_t count = rd_u32(d + pos);
+    uint32_t state = rd_u16(d + pos + 4);
+    uint32_t bit_len = rd_u32(d + pos + 6);
+    pos += 10;
+    if (count > (1u << 28)) fail(HIVC_E_ENTROPY, "implausible symbol count " + std::to_string(count));
+    size_t nbytes = ((size_t)bit_len + 7) / 8;
+    if (pos + nbytes > len) fail(HIVC_E_TRUNCATED_STREAM, "entropy payload truncated");
+    FseTable t;
+    t.build(counts, tl);
+    out.resize(count);
+    if (count) {  // fse_decode, entropy.py:175-211
+        const uint32_t size = 1u << tl;
+        if (state < size || state >= 2 * size) fail(HIVC_E_ENTROPY, "corrupt stream: initial state out of range");
+        BitReader rd(d + pos, nbytes, bit_len);
+        const uint16_t* sym = t.sym.data();
+        const uint32_t* xs = t.x.data();
+        const uint8_t* nbs = t.nb.data();
+        for (uint32_t i = 0; i < count; ++i) {
+            uint32_t slot = state - size;
+            out[i] = sym[slot];
+            int nb = nbs[slot];
+            state = nb ? ((xs[slot] << nb) | rd.take(nb)) : xs[slot];
+        }
+        if (state != size) fail(HIVC_E_ENTROPY, "corrupt stream: final state mismatch");
+    }
+    return pos + nbytes;
+}
+
+size_t decode_signed_values(const uint8_t* d, size_t len, size_t pos, std::vector<int32_t>& out) {
+    std::vector<int32_t> cats;  // entropy.py:311-338
+    pos = decode_symbols(d, len, pos, cats);
+    if (pos + 4 > len) fail(HIVC_E_TRUNCATED_STREAM, "entropy payload truncated");
+    uint32_t bit_len = rd_u32(d + pos);
+    pos += 4;
+    size_t nbytes = ((size_t)bit_len + 7) / 8;
+    if (pos + nbytes > len) fail(HIVC_E_TRUNCATED_STREAM, "entropy payload truncated");
+    uint64_t sum = 0;
+    for (int32_t c : cats) {
+        if (c > 16) fail(HIVC_E_ENTROPY, "bad category in stream");
+        sum += (uint64_t)c;
+    }
+    if (sum != bit_len) fail(HIVC_E_ENTROPY, "extra-bits length mismatch");
+    BitReader rd(d + pos, nbytes, bit_len);
+    out.resize(cats.size());
+    for (size_t i = 0; i < cats.size(); ++i) {
+        int k = cats[i];
+        if (!k) {
+            out[i] = 0;
+            continue;
+        }
+        int32_t e = (int32_t)rd.take(k);
+        out[i] = e >= (1 << (k - 1)) ? e : e - (1 << k) + 1;  // from_category, entropy.py:52-60
+    }
+    return pos + nbytes;
+}
+
+void parse_tree_leaves(BitReader& rd, int32_t w, int32_t h, std::vector<Rect>& leaves) {
+    std::vector<Rect> st;  // subdivision.py:198-222
+    st.reserve(64);
+    st.push_back({0, 0, w, h});
+    while (!st.empty()) {
+        Rect r = st.back();
+        st.pop_back();
+        if (rd.bit()) {
+            if (r.w == 1 && r.h == 1) fail(HIVC_E_SUBDIVISION, "split of a single pixel");
+            if (r.h > r.w) {
+                int32_t a = (r.h + 1) / 2;
+                st.push_back({r.x, r.y + a, r.w, r.h - a});
+                st.push_back({r.x, r.y, r.w, a});
+            } else {
+                int32_t a = (r.w + 1) / 2;
+                st.push_back({r.x + a, r.y, r.w - a, r.h});
+                st.push_back({r.x, r.y, a, r.h});
+            }
+        } else {
+            leaves.push_back(r);
+        }
+    }
+}
+
+void parse_flow_tree(BitReader& rd, int32_t w, int32_t h, std::vector<int32_t>& nodes, int32_t& nleaves) {
+    // Same preorder walk as parse_tree_leaves (subdivision.py:183-195), but
+    // recording the split structure.  The stack carries the index of the
+    // parent whose right-child slot the popped rectangle fills (-1: none).
+    struct Item {
+        Rect r;
+        int32_t parent_right;
+    };
+    std::vector<Item> st;
+    st.push_back({{0, 0, w, h}, -1});
+    nodes.clear();
+    nleaves = 0;
+    while (!st.empty()) {
+        Item it = st.back();
+        st.pop_back();
+        int32_t idx = (int32_t)(nodes.size() / 2);
+        if (it.parent_right >= 0) nodes[2 * it.parent_right + 1] = idx;
+        const Rect& r = it.r;
+        if (rd.bit()) {
+            if (r.w == 1 && r.h == 1) fail(HIVC_E_SUBDIVISION, "cannot split a single pixel");
+            if (r.h > r.w) {
+                int32_t a = (r.h + 1) / 2;
+                nodes.push_back(((r.y + a) << 2) | 2);
+                nodes.push_back(-1);
+                st.push_back({{r.x, r.y + a, r.w, r.h - a}, idx});
+                st.push_back({{r.x, r.y, r.w, a}, -1});
+            } else {
+                int32_t a = (r.w + 1) / 2;
+                nodes.push_back(((r.x + a) << 2) | 1);
+                nodes.push_back(-1);
+                st.push_back({{r.x + a, r.y, r.w - a, r.h}, idx});
+                st.push_back({{r.x, r.y, a, r.h}, -1});
+            }
+        } else {
+            nodes.push_back(0);
+            nodes.push_back(nleaves++);
+        }
+    }
+}
+
+StreamHeader parse_header(const uint8_t* d, size_t len) {  // bitstream.py:102-121, 80-91
+    if (len < HEADER_SIZE) fail(HIVC_E_TRUNCATED, "stream shorter than header");
+    if (std::memcmp(d, "HIVC", 4) != 0) fail(HIVC_E_BAD_MAGIC, "not a compressed video stream");
+    if (d[4] != 1) fail(HIVC_E_UNSUPPORTED_VERSION, "stream version " + std::to_string(d[4]) + ", expected 1");
+    StreamHeader h;
+    h.width = rd_u16(d + 5);
+    h.height = rd_u16(d + 7);
+    h.frame_count = (int32_t)rd_u32(d + 9);
+    h.fps_num = rd_u16(d + 13);
+    h.fps_den = rd_u16(d + 15);
+    h.gop_size = d[17];
+    h.channels = d[18];
+    h.intra_levels = d[19] + 1;
+    h.flow_levels = d[20] + 1;
+    h.residual_levels = d[21];
+    if (rd_u32(d + 9) > 0x7fffffffu) fail(HIVC_E_BITSTREAM, "frame count out of range");
+    if (h.width < 1 || h.height < 1) fail(HIVC_E_BITSTREAM, "bad frame dimensions");
+    if (h.channels != 1 && h.channels != 3) fail(HIVC_E_BITSTREAM, "channels must be 1 or 3");
+    if (h.gop_size < 1) fail(HIVC_E_BITSTREAM, "gop_size out of range");
+    if (h.intra_levels < 2 || h.flow_levels < 2) fail(HIVC_E_BITSTREAM, "quantizer levels out of range");
+    if (h.residual_levels < 3 || h.residual_levels % 2 == 0)
+        fail(HIVC_E_BITSTREAM, "residual_levels must be odd and >= 3");
+    if (h.fps_num < 1 || h.fps_den < 1) fail(HIVC_E_BITSTREAM, "bad frame rate");
+    return h;
+}
+
+void split_gops(const uint8_t* d, size_t len, const StreamHeader& h, std::vector<std::pair<size_t, size_t>>& gops) {
+    size_t pos = HEADER_SIZE;  // bitstream.py:132-154
+    gops.clear();
+    while (pos < len) {
+        if (pos + 4 > len) fail(HIVC_E_TRUNCATED, "group length prefix cut short");
+        size_t n = rd_u32(d + pos);
+        pos += 4;
+        if (pos + n > len)
+            fail(HIVC_E_TRUNCATED, "group payload " + std::to_string(gops.size()) + " cut short (" +
+                                       std::to_string(len - pos) + " of " + std::to_string(n) + " bytes present)");
+        gops.push_back({pos, n});
+        pos += n;
+    }
+    size_t want = h.frame_count ? ((size_t)h.frame_count + h.gop_size - 1) / h.gop_size : 0;
+    if (gops.size() != want)
+        fail(HIVC_E_LENGTH_MISMATCH, "stream holds " + std::to_string(gops.size()) + " groups, header implies " +
+                                         std::to_string(want));
+}
+
+// ---------------------------------------------------------------- intra payload
+
+static size_t intra_tree(const uint8_t* d, size_t len, size_t pos, int32_t h, int32_t w, std::vector<int32_t>& pts,
+                         std::vector<uint64_t>& bits) {
+    // prediction._read_tree (prediction.py:149-159) + mask points in raster
+    // order (_mask_points, prediction.py:117-119)
+    if (pos + 4 > len) fail(HIVC_E_TRUNCATED_STREAM, "intra payload truncated");
+    uint32_t nbits = rd_u32(d + pos);
+    pos += 4;
+    size_t nbytes = ((size_t)nbits + 7) / 8;
+    if (pos + nbytes > len) fail(HIVC_E_TRUNCATED_STREAM, "intra payload truncated");
+    BitReader rd(d + pos, nbytes, nbits);
+    std::vector<Rect> leaves;
+    parse_tree_leaves(rd, w, h, leaves);
+    const size_t npx = (size_t)h * w;
+    bits.assign((npx + 63) / 64, 0);
+    for (const Rect& r : leaves) {
+        size_t i = (size_t)(r.y + r.h / 2) * w + (r.x + r.w / 2);
+        bits[i >> 6] |= 1ull << (i & 63);
+    }
+    pts.clear();
+    pts.reserve(leaves.size());
+    for (size_t wi = 0; wi < bits.size(); ++wi) {
+        uint64_t b = bits[wi];
+        while (b) {
+            int t = __builtin_ctzll(b);
+            pts.push_back((int32_t)(wi * 64 + t));
+            b &= b - 1;
+        }
+    }
+    return pos + nbytes;
+}
+
+static size_t intra_values(const uint8_t* d, size_t len, size_t pos, int levels, size_t npts, std::vector<double>& out) {
+    // prediction._decode_plane_values (prediction.py:133-139) + uniform_dequantize (quantize.py:78-82)
+    if (pos + 4 > len) fail(HIVC_E_TRUNCATED_STREAM, "intra payload truncated");
+    int16_t lo, hi;
+    std::memcpy(&lo, d + pos, 2);
+    std::memcpy(&hi, d + pos + 2, 2);
+    pos += 4;
+    std::vector<int32_t> idx;
+    pos = decode_symbols(d, len, pos, idx);
+    double flo = lo, fhi = hi;
+    if (!(flo < fhi)) fail(HIVC_E_QUANTIZE, "need lo < hi");
+    double step = (fhi - flo) / (double)(levels - 1);
+    // f.ravel()[points] = values (prediction.py:205): numpy broadcasts a
+    // single value, any other length mismatch is a ValueError.
+    if (idx.size() != npts && idx.size() != 1)
+        fail(HIVC_E_ARGUMENT, "shape mismatch: " + std::to_string(idx.size()) + " values for " +
+                                  std::to_string(npts) + " mask points");
+    out.resize(npts);
+    for (size_t i = 0; i < npts; ++i) out[i] = flo + (double)idx[idx.size() == 1 ? 0 : i] * step;
+    return pos;
+}
+
+size_t parse_intra(const uint8_t* d, size_t len, size_t pos, int32_t h, int32_t w, int channels, int levels,
+                   IntraJob& job, std::vector<uint64_t>& bits) {
+    // prediction.decode_intra (prediction.py:185-200)
+    pos = intra_tree(d, len, pos, h, w, job.pts[0], bits);
+    pos = intra_values(d, len, pos, levels, job.pts[0].size(), job.vals[0]);
+    job.nchan = 1;
+    if (channels == 3) {
+        pos = intra_tree(d, len, pos, h, w, job.pts[1], bits);
+        for (int c = 1; c < 3; ++c) pos = intra_values(d, len, pos, 2 * levels - 1, job.pts[1].size(), job.vals[c]);
+        job.nchan = 3;
+    }
+    return pos;
+}
+
+// ---------------------------------------------------------------- flow payload
+
+size_t parse_flow(const uint8_t* d, size_t len, size_t pos, int32_t h, int32_t w, int levels, FlowJob& job) {
+    for (int c = 0; c < 2; ++c) {  // flow._decompress_plane (flow.py:343-356)
+        if (pos + 12 > len) fail(HIVC_E_TRUNCATED_STREAM, "flow payload truncated");
+        float lo, hi;
+        std::memcpy(&lo, d + pos, 4);
+        std::memcpy(&hi, d + pos + 4, 4);
+        uint32_t nbits = rd_u32(d + pos + 8);
+        pos += 12;
+        size_t nbytes = ((size_t)nbits + 7) / 8;
+        if (pos + nbytes > len) fail(HIVC_E_TRUNCATED_STREAM, "flow payload truncated");
+        BitReader rd(d + pos, nbytes, nbits);
+        int32_t nleaves = 0;
+        parse_flow_tree(rd, w, h, job.nodes[c], nleaves);
+        pos += nbytes;
+        std::vector<int32_t> idx;
+        pos = decode_symbols(d, len, pos, idx);
+        double flo = lo, fhi = hi;
+        if (!(flo < fhi)) fail(HIVC_E_QUANTIZE, "need lo < hi");
+        double step = (fhi - flo) / (double)(levels - 1);
+        if ((int64_t)idx.size() != nleaves) fail(HIVC_E_SUBDIVISION, "leaf value count mismatch");
+        job.vals[c].resize(idx.size());
+        for (size_t i = 0; i < idx.size(); ++i) job.vals[c][i] = flo + (double)idx[i] * step;
+    }
+    for (int c = 0; c < 2; ++c)  // FlowField.__post_init__ (flow.py:45-49)
+        for (double v : job.vals[c])
+            if (!std::isfinite(v)) fail(HIVC_E_FLOW, "non-finite flow values");
+    return pos;
+}
+
+// ---------------------------------------------------------------- residual payload
+
+size_t parse_residual(const uint8_t* d, size_t len, size_t pos, int32_t h, int32_t w, int channels, ResidualJob& job) {
+    // codec._decode_residual (codec.py:248-340), parse half
+    const int32_t nbx = (w + 7) / 8, nby = (h + 7) / 8;
+    const size_t ntiles = (size_t)nbx * nby;
+    const size_t nskip = (ntiles + 7) / 8;
+    if (pos + 1 > len) fail(HIVC_E_TRUNCATED, "residual payload truncated");
+    uint8_t marker = d[pos++];
+    job.ngroups = 0;
+    if (marker == 0) {
+        job.zero = true;
+        return pos;
+    }
+    if (marker != 1) fail(HIVC_E_CODEC, "bad residual payload marker");
+    job.zero = false;
+    if (pos + 8 > len) fail(HIVC_E_TRUNCATED, "residual payload truncated");
+    uint32_t c_fp = rd_u32(d + pos), a_fp = rd_u32(d + pos + 4);
+    pos += 8;
+    if (c_fp == 0 || a_fp == 0) fail(HIVC_E_CODEC, "zero coefficient scale");
+    job.c_scale = c_fp / 65536.0;
+    job.a_scale = a_fp / 65536.0;
+    const int groups[2] = {1, 2};
+    const int ng = channels == 3 ? 2 : 1;
+    std::vector<Rect> leaves;
+    for (int gi = 0; gi < ng; ++gi) {
+        ResidualGroup& g = job.g[gi];
+        g.nplanes = groups[gi];
+        if (pos + nskip > len) fail(HIVC_E_TRUNCATED, "residual payload truncated");
+        // skip bitmap, MSB-first (np.unpackbits, codec.py:285-289)
+        const size_t nwords = (ntiles + 63) / 64;
+        g.tile_words.assign(nwords, 0);
+        g.word_prefix.assign(nwords, 0);
+        for (size_t t = 0; t < ntiles; ++t)
+            if ((d[pos + (t >> 3)] >> (7 - (t & 7))) & 1) g.tile_words[t >> 6] |= 1ull << (t & 63);
+        pos += nskip;
+        int32_t acc = 0;
+        for (size_t i = 0; i < nwords; ++i) {
+            g.word_prefix[i] = acc;
+            acc += __builtin_popcountll(g.tile_words[i]);
+        }
+        g.nblocks = acc;
+        if (pos + 4 > len) fail(HIVC_E_TRUNCATED, "residual payload truncated");
+        uint32_t tree_bits = rd_u32(d + pos);
+        pos += 4;
+        size_t tnb = ((size_t)tree_bits + 7) / 8;
+        if (pos + tnb > len) fail(HIVC_E_TRUNCATED, "residual payload truncated");
+        BitReader rd(d + pos, tnb, tree_bits);
+        pos += tnb;
+        g.block_mask.resize(g.nblocks);
+        g.block_off.resize(g.nblocks);
+        int32_t b = 0, npts = 0;
+        for (size_t wi = 0; wi < nwords; ++wi) {
+            uint64_t bits = g.tile_words[wi];
+            while (bits) {
+                size_t t = wi * 64 + __builtin_ctzll(bits);
+                bits &= bits - 1;
+                int32_t ty = (int32_t)(t / nbx), tx = (int32_t)(t % nbx);
+                int32_t bh = std::min(8, h - ty * 8), bw = std::min(8, w - tx * 8);
+                leaves.clear();
+                parse_tree_leaves(rd, bw, bh, leaves);  // parse_mask per coded tile (codec.py:300-303)
+                uint64_t m = 0;
+                for (const Rect& r : leaves) m |= 1ull << ((r.y + r.h / 2) * 8 + (r.x + r.w / 2));
+                g.block_mask[b] = m;
+                g.block_off[b] = npts;
+                npts += __builtin_popcountll(m);
+                ++b;
+            }
+        }
+        g.npoints = npts;
+        pos = decode_signed_values(d, len, pos, g.c_sym);
+        pos = decode_signed_values(d, len, pos, g.a_sym);
+        if (g.c_sym.size() != (size_t)npts * g.nplanes || g.a_sym.size() != (size_t)g.nblocks * g.nplanes)
+            fail(HIVC_E_CODEC, "residual payload inconsistent with block masks");
+    }
+    job.ngroups = ng;
+    return pos;
+}
+
+}  // namespace hivc

@@ -1,0 +1,129 @@
+"""Backward flow: warping and flow-payload decoding on the B200 (reference: flow.py).
+
+``warp_planes`` / ``bilinear_warp`` keep the reference signatures
+(flow.py:94-132) and run ``hivc_warp`` (csrc/recon.cu) in float64 with the
+reference's clamp-then-floor coordinates and tap order.  Inside
+``codec.decode`` the warp is fused with the residual and rounding and the
+dense flow field is never materialised (csrc/recon.cu: frame_kernel).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import struct
+from dataclasses import dataclass
+
+import numpy as np
+
+from paper_2008_10273_b200 import _native as N
+from paper_2008_10273_b200._tensors import back, is_cuda_tensor, ptr, to_device, torch
+from paper_2008_10273_b200.errors import FlowError, QuantizeError, SubdivisionError, TruncatedStream
+
+
+@dataclass(frozen=True)
+class FlowField:
+    u: object  # horizontal displacement, pixels
+    v: object  # vertical displacement, pixels
+
+    def __post_init__(self):  # flow.py:45-49
+        if tuple(self.u.shape) != tuple(self.v.shape):
+            raise FlowError("flow component shape mismatch")
+        if is_cuda_tensor(self.u):
+            t = torch()
+            ok = bool(t.isfinite(self.u).all()) and bool(t.isfinite(self.v).all())
+        else:
+            ok = bool(np.isfinite(self.u).all() and np.isfinite(self.v).all())
+        if not ok:
+            raise FlowError("non-finite flow values")
+
+    @property
+    def shape(self):
+        return tuple(self.u.shape)
+
+
+@dataclass(frozen=True)
+class BroxParams:  # flow.py:56-66
+    alpha: float = 40.0
+    gamma: float = 40.0
+    pyramid_scale: float = 0.5
+    min_size: int = 16
+    warps: int = 3
+    fixed_point_iters: int = 5
+    solver_iters: int = 30
+    eps: float = 1e-3
+    presmooth_sigma: float = 0.8
+
+
+def warp_planes(planes, u, v):
+    """Sample each plane at (x + u, y + v), bilinear with border clamping (flow.py:94-127)."""
+    t = torch()
+    ut = to_device(u, t.float64)
+    dev = ut.device
+    vt = to_device(v, t.float64, dev)
+    h, w = ut.shape
+    src = [to_device(p, t.float64, dev) for p in planes]
+    for s in src:
+        if tuple(s.shape) != (h, w):
+            raise ValueError("plane/flow shape mismatch")
+    dst = [t.empty_like(s) for s in src]
+    ctx = N.context(dev.index)
+    t.cuda.current_stream(dev).synchronize()
+    sp = (C.c_void_p * len(src))(*[ptr(s) for s in src])
+    dp = (C.c_void_p * len(dst))(*[ptr(d) for d in dst])
+    N.check(N.lib.hivc_warp(ctx.handle, sp, len(src), ptr(ut), ptr(vt), h, w, dp))
+    return [back(d, p) for d, p in zip(dst, planes)]
+
+
+def bilinear_warp(plane, u, v):
+    """Sample plane at (x + u, y + v) with bilinear interpolation, clamped (flow.py:130-132)."""
+    return warp_planes([plane], u, v)[0]
+
+
+def _tree_leaves(data: bytes, pos: int, nbits: int, width: int, height: int, bit_offset: int = 0, with_used=False):
+    """Preorder leaf rectangles (x, y, w, h) via the native parser (subdivision.py:183-222)."""
+    nbytes = (nbits + 7) // 8
+    buf = C.create_string_buffer(bytes(data[pos : pos + nbytes]), max(nbytes, 1))
+    n = C.c_size_t()
+    used = C.c_uint64()
+    N.check(N.lib.hivc_parse_tree(buf, nbytes, nbits, bit_offset, width, height, None, 0, C.byref(n), C.byref(used)))
+    rects = (C.c_int32 * max(4 * n.value, 1))()
+    N.check(N.lib.hivc_parse_tree(buf, nbytes, nbits, bit_offset, width, height, rects, n.value, C.byref(n),
+                                  C.byref(used)))
+    out = np.frombuffer(rects, dtype=np.int32)[: 4 * n.value].reshape(-1, 4).copy()
+    return (out, int(used.value)) if with_used else out
+
+
+def _decode_symbols(data: bytes, pos: int):
+    from paper_2008_10273_b200.entropy import decode_symbols
+
+    return decode_symbols(data, pos)
+
+
+def _decompress_plane(data: bytes, pos: int, shape, levels: int):
+    if pos + 12 > len(data):  # flow.py:343-356
+        raise TruncatedStream("flow payload truncated")
+    lo, hi, nbits = struct.unpack_from("<ffI", data, pos)
+    pos += 12
+    nbytes = (nbits + 7) // 8
+    if pos + nbytes > len(data):
+        raise TruncatedStream("flow payload truncated")
+    leaves = _tree_leaves(data, pos, nbits, shape[1], shape[0])
+    pos += nbytes
+    idx, pos = _decode_symbols(data, pos)
+    lo, hi = float(lo), float(hi)
+    if not lo < hi:
+        raise QuantizeError("need lo < hi")
+    vals = lo + idx.astype(np.float64) * ((hi - lo) / (levels - 1))
+    if len(vals) != len(leaves):
+        raise SubdivisionError("leaf value count mismatch")
+    out = np.empty(shape, dtype=np.float64)
+    for (x, y, w, h), val in zip(leaves.tolist(), vals):
+        out[y : y + h, x : x + w] = val
+    return out, pos
+
+
+def decompress_flow(data: bytes, pos: int, shape, quant_levels: int):
+    """Decode a compressed flow payload; returns (FlowField, next position) (flow.py:368-372)."""
+    u, pos = _decompress_plane(data, pos, shape, quant_levels)
+    v, pos = _decompress_plane(data, pos, shape, quant_levels)
+    return FlowField(u, v), pos

@@ -1,0 +1,97 @@
+"""The CPU oracle against the reference's own outputs (golden vectors made by
+importing the reference, tests/golden/make_golden.py / make_streams.py).
+CPU only."""
+
+import numpy as np
+import pytest
+
+from oracle import blocks, decoder, inpaint, motion, parse
+
+
+def test_oracle_decodes_config0_like_the_reference(cfg0_stream, cfg0_frames):
+    frames = decoder.decode_stream(cfg0_stream)
+    got = np.stack([f[0] for f in frames]).astype(np.uint8)
+    assert np.array_equal(got, cfg0_frames)
+
+
+@pytest.mark.parametrize("i", range(8))
+def test_oracle_homogeneous_matches_reference(golden, i):
+    f, m, u = golden[f"homog{i}_f"], golden[f"homog{i}_m"], golden[f"homog{i}_u"]
+    tol, mi, strict = golden[f"homog{i}_cfg"]
+    st = {}
+    got = inpaint.solve(f, m, tol=tol, max_iter=int(mi), strict=bool(strict), stats=st)
+    assert np.array_equal(np.array(st["level_iterations"]), golden[f"homog{i}_iters"])
+    # identical algorithm; only BLAS dot-product order may differ
+    assert np.abs(got - u).max() <= 1e-9 * max(1.0, np.abs(u).max())
+    if f"homog{i}_dense" in golden and strict:
+        assert np.sqrt(np.mean((got - golden[f"homog{i}_dense"]) ** 2)) < 1e-3
+
+
+def test_oracle_blocks_match_reference(golden):
+    assert np.array_equal(blocks.reconstruct(golden["blocks_mc"], golden["blocks_a"]), golden["blocks_rec"])
+    assert np.array_equal(blocks.greens_eig(), golden["blocks_eig"])
+    assert np.array_equal(blocks.FWD_SCALE2, golden["fscale2"])
+    assert np.array_equal(blocks.INV_SCALE2, golden["iscale2"])
+    assert np.array_equal(blocks.greens_matrix(), golden["g8"])
+
+
+def test_oracle_block_fit_matches_reference(golden):
+    f, masks = golden["fit_f"], golden["fit_masks"]
+    n = f.shape[0]
+    ks = masks.reshape(n, 64).sum(1)
+    for k in np.unique(ks):
+        sel = np.flatnonzero(ks == k)
+        c, a = blocks.fit(f[sel], masks[sel])
+        np.testing.assert_allclose(a, golden["fit_a"][sel], rtol=0, atol=1e-9)
+        cf = golden["fit_c"][sel].reshape(len(sel), 64)[masks[sel].reshape(len(sel), 64)].reshape(len(sel), k)
+        np.testing.assert_allclose(c, cf, rtol=0, atol=1e-9)
+
+
+def test_oracle_warp_matches_reference(golden):
+    out = motion.warp(list(golden["warp_planes"]), golden["warp_u"], golden["warp_v"])
+    assert np.array_equal(np.stack(out), golden["warp_out"])
+
+
+def test_oracle_entropy_matches_reference(payloads):
+    for key in payloads:
+        if key.endswith("_payload") and key.startswith("sym"):
+            name = key[: -len("_payload")]
+            out, pos = parse.decode_symbols(payloads[key].tobytes(), 0)
+            assert pos == payloads[key].size
+            assert np.array_equal(out, payloads[name + "_in"])
+        if key.endswith("_payload") and key.startswith("sv"):
+            name = key[: -len("_payload")]
+            out, pos = parse.decode_signed_values(payloads[key].tobytes(), 0)
+            assert pos == payloads[key].size
+            assert np.array_equal(out, payloads[name + "_in"])
+
+
+def test_oracle_trees_match_reference(payloads):
+    i = 0
+    while f"tree{i}_bits" in payloads:
+        h, w = payloads[f"tree{i}_shape"]
+        rd = parse.Bits(payloads[f"tree{i}_bits"].tobytes(), int(payloads[f"tree{i}_nbits"][0]))
+        leaves = parse.tree_leaves(rd, int(w), int(h))
+        assert np.array_equal(np.array(leaves).reshape(-1, 4), payloads[f"tree{i}_leaves"])
+        rd = parse.Bits(payloads[f"tree{i}_bits"].tobytes(), int(payloads[f"tree{i}_nbits"][0]))
+        assert np.array_equal(parse.tree_mask(rd, int(w), int(h)), payloads[f"tree{i}_mask"])
+        i += 1
+
+
+def test_oracle_dense_known_answers():
+    # homogeneous.py / test_homogeneous.py known answers: full mask copies,
+    # a single point gives a constant, maximum principle
+    f = np.arange(12.0).reshape(3, 4)
+    assert np.array_equal(inpaint.solve(f, np.ones((3, 4), bool)), f)
+    m = np.zeros((5, 6), bool)
+    m[2, 3] = True
+    g = np.zeros((5, 6))
+    g[2, 3] = 7.0
+    np.testing.assert_allclose(inpaint.solve(g, m), 7.0, atol=1e-6)
+    rng = np.random.default_rng(3)
+    m = rng.uniform(size=(10, 11)) < 0.2
+    m[0, 0] = True
+    f = np.where(m, rng.uniform(10, 20, (10, 11)), 0.0)
+    u = inpaint.solve(f, m)
+    assert u.min() >= f[m].min() - 1e-6 and u.max() <= f[m].max() + 1e-6
+    np.testing.assert_allclose(u, inpaint.solve_dense(f, m), atol=1e-4)
