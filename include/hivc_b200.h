@@ -161,6 +161,11 @@ int hivc_decode_multi(hivc_ctx* ctx, int32_t nstreams, const uint8_t* const* dat
                       int32_t out_on_device, double* stage_seconds);
 /* Host<->device bytes moved by this context's decodes so far. */
 int hivc_ctx_bytes(hivc_ctx* ctx, int64_t* h2d, int64_t* d2h);
+/* Accumulated statistics of timed decodes (stage timing on), 10 doubles:
+ * CG solves, sum N_l*it_l, sum N_l, cooperative level-kernel launches, their
+ * device seconds, their sum N_l*it_l, their sum N_l, P frames, P-kernel device
+ * seconds, I frames.  reset != 0 clears them. */
+int hivc_ctx_decode_stats(hivc_ctx* ctx, double* out, int32_t reset);
 /* Per-frame CUDA-event stage breakdown on (default) or off (pure throughput runs). */
 int hivc_ctx_set_stage_timing(hivc_ctx* ctx, int32_t enable);
 

@@ -70,6 +70,7 @@ _proto("hivc_decode_multi", C.c_int, C.c_void_p, C.c_int32, C.POINTER(C.c_void_p
        C.POINTER(C.c_void_p), C.c_int32, c_dbl_p)
 _proto("hivc_ctx_bytes", C.c_int, C.c_void_p, c_i64_p, c_i64_p)
 _proto("hivc_ctx_set_stage_timing", C.c_int, C.c_void_p, C.c_int32)
+_proto("hivc_ctx_decode_stats", C.c_int, C.c_void_p, c_dbl_p, C.c_int32)
 
 
 def check(status: int):

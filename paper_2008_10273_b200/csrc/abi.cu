@@ -255,6 +255,25 @@ int hivc_ctx_bytes(hivc_ctx* ctx, int64_t* h2d, int64_t* d2h) {
     });
 }
 
+int hivc_ctx_decode_stats(hivc_ctx* ctx, double* out, int32_t reset) {
+    return guarded([&] {
+        if (!ctx) hivc::fail(HIVC_E_ARGUMENT, "null context");
+        hivc::Context& C = ctx->c;
+        std::lock_guard<std::mutex> g(C.stats_mu);
+        const hivc::CgTotals& T = C.cg;
+        double v[10] = {(double)T.solves,        (double)T.pixel_iters,      (double)T.pixel_levels,
+                        (double)T.grid_launches, T.grid_seconds,             (double)T.grid_pixel_iters,
+                        (double)T.grid_pixels,   (double)C.inter_frames,     C.inter_seconds,
+                        (double)C.intra_frames};
+        std::memcpy(out, v, sizeof(v));
+        if (reset) {
+            C.cg = hivc::CgTotals{};
+            C.inter_frames = C.intra_frames = 0;
+            C.inter_seconds = 0;
+        }
+    });
+}
+
 int hivc_ctx_set_stage_timing(hivc_ctx* ctx, int32_t enable) {
     return guarded([&] {
         if (!ctx) hivc::fail(HIVC_E_ARGUMENT, "null context");

@@ -246,6 +246,8 @@ struct LaneResult {
     HostTimes ht;
     double gpu_intra = 0, gpu_inter = 0, gpu_ifinal = 0;
     int64_t h2d = 0, d2h = 0;
+    int64_t inter_frames = 0, intra_frames = 0;
+    CgTotals cg;
 };
 
 using EvPairs = std::vector<std::pair<cudaEvent_t, cudaEvent_t>>;
@@ -339,6 +341,7 @@ void decode_gop(Context& ctx, Lane& L, const StreamJob& S, int gi, bool out_on_d
             v.push_back(e);
         };
         ev_begin();
+        (J.type == 0 ? R.intra_frames : R.inter_frames) += 1;
         if (J.type == 0) {
             // intra: f = 0 with the values scattered at the mask points, then solve (prediction.py:203-208)
             int64_t launches = 0;
@@ -350,7 +353,8 @@ void decode_gop(Context& ctx, Lane& L, const StreamJob& S, int gi, bool out_on_d
                 launch_scatter(at<int32_t>(dev, o.pts[t]), at<double>(dev, o.vals[c]), (int)pts.size(), L.f[c],
                                c <= 1 ? L.m[t] : nullptr, s);
                 ++launches;
-                solve_homogeneous_async(L.ws, s, L.f[c], L.m[t], h, w, 1e-4, 160, L.u[c], &launches);
+                solve_homogeneous_async(L.ws, s, L.f[c], L.m[t], h, w, 1e-4, 160, L.u[c], &launches,
+                                        timed ? &L.probe : nullptr);
                 A.u[c] = L.u[c];
             }
             ctx.launches += launches;
@@ -397,6 +401,7 @@ void run_lane(Context& ctx, Lane& L, const std::vector<StreamJob>& streams, cons
         R.gpu_intra = drain(ev_intra);
         R.gpu_inter = drain(ev_inter);
         R.gpu_ifinal = drain(ev_ifin);
+        L.probe.harvest(R.cg);
     } catch (const Error& e) {
         R.code = e.code;
         R.msg = e.what();
@@ -513,6 +518,18 @@ void decode_streams(Context& ctx, int nstreams, const uint8_t* const* data, cons
     for (auto& r : res) {
         ctx.h2d_bytes += r.h2d;
         ctx.d2h_bytes += r.d2h;
+        std::lock_guard<std::mutex> g(ctx.stats_mu);
+        CgTotals& T = ctx.cg;
+        T.solves += r.cg.solves;
+        T.pixel_iters += r.cg.pixel_iters;
+        T.pixel_levels += r.cg.pixel_levels;
+        T.grid_launches += r.cg.grid_launches;
+        T.grid_seconds += r.cg.grid_seconds;
+        T.grid_pixel_iters += r.cg.grid_pixel_iters;
+        T.grid_pixels += r.cg.grid_pixels;
+        ctx.inter_frames += r.inter_frames;
+        ctx.inter_seconds += r.gpu_inter;
+        ctx.intra_frames += r.intra_frames;
     }
     if (stage_seconds) {
         double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};

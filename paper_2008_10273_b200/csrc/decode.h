@@ -5,6 +5,7 @@
 
 #include <atomic>
 #include <memory>
+#include <mutex>
 #include <vector>
 
 #include "inpaint.h"
@@ -32,6 +33,7 @@ struct Lane {
     uint8_t* gop_out[2] = {nullptr, nullptr};  // device frame buffers when output goes to the host
     size_t gop_out_cap = 0;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    CgProbe probe;
     void reserve_planes(int h, int w, int channels);
     void reserve_stage(int slot, size_t bytes);
     void reserve_gop_out(size_t bytes);
@@ -46,6 +48,10 @@ struct Context {
     std::atomic<int64_t> launches{0};
     std::atomic<int64_t> h2d_bytes{0}, d2h_bytes{0};
     bool stage_events = true;  // per-frame CUDA events for the stage breakdown
+    std::mutex stats_mu;
+    CgTotals cg;               // accumulated over timed decodes
+    int64_t inter_frames = 0, intra_frames = 0;
+    double inter_seconds = 0;  // device time of the fused P-frame kernels
     int* d_status = nullptr;
     ~Context();
 };

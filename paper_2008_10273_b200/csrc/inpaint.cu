@@ -85,6 +85,10 @@ struct CgParams {
     unsigned int* bar;
     int* iters;         // out: iterations of this level
     double* margin;     // out: min |sqrt(rs)-tol*bn|/(tol*bn) over stop tests (parity diagnostics)
+    // band kernel: CTA b owns rows [b*band_rows, min(h, (b+1)*band_rows))
+    int band_rows;
+    double* ex_r;  // [nbands][2][w]: first/last owned row of r
+    double* ex_p;  // [2 parity][nbands][2][w]: first/last owned row of p
 };
 
 __device__ __forceinline__ double prolong_at(const CgParams& P, int y, int xx) {
@@ -256,6 +260,172 @@ __global__ void __launch_bounds__(kThreads, 1) cg_level_kernel(CgParams P) {
     }
 }
 
+// ---------------------------------------------------------------- on-chip CG level kernel
+// One CTA per horizontal band of rows (one CTA per SM).  For the whole level
+// the band's r lives in registers and its p (plus one halo row above and
+// below) in shared memory; x is streamed through global memory.  Only the
+// first/last owned rows of r and p cross CTAs: each CTA publishes them to
+// small exchange buffers, and after the grid barrier its neighbours rebuild
+// their halo p = r + beta p from them.  Per iteration the CTA therefore moves
+// x (16 B/px) + 4 exchange rows instead of every vector, and A p is
+// recomputed from shared memory in the second phase instead of being stored.
+// Same per-pixel float64 expressions as cg_level_kernel.
+constexpr int kBandThreads = 512;
+constexpr int kBandPx = 32;  // max owned pixels per thread: r stays in registers (<= 128 regs)
+
+__global__ void __launch_bounds__(kBandThreads, 1) cg_band_kernel(CgParams P) {
+    extern __shared__ double sp[];  // (rows+2) x w : halo, owned rows, halo
+    __shared__ double sh[4 * 32];
+    const int h = P.h, w = P.w;
+    const int band = blockIdx.x, nb = gridDim.x;
+    const int y0 = band * P.band_rows;
+    const int rows = min(P.band_rows, h - y0);
+    const int npx = rows * w;
+    const int tid = threadIdx.x;
+    const double* __restrict__ f = P.f;
+    const uint8_t* __restrict__ m = P.m;
+    uint8_t* smask = reinterpret_cast<uint8_t*>(sp + (size_t)(P.band_rows + 2) * w);
+    double r[kBandPx];
+    auto sidx = [&](int yy, int xq) -> int { return (yy - y0 + 1) * w + xq; };  // smem row of global y
+
+    // ---- setup (homogeneous.py:64-77); x0 from the coarser level by prolongation
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int j = 0; j < kBandPx; ++j) {
+        int q = tid + j * kBandThreads;
+        r[j] = 0.0;
+        if (q >= npx) continue;
+        int yy = y0 + q / w, xx = q % w;
+        size_t gi = (size_t)yy * w + xx;
+        bool mi = m[gi] != 0;
+        smask[q] = mi;
+        double interior = mi ? 0.0 : 1.0;
+        auto ud = [&](int a, int b) -> double {
+            size_t k = (size_t)a * w + b;
+            return m[k] ? __ldg(f + k) : 0.0;
+        };
+        auto xv = [&](int a, int b) -> double {
+            size_t k = (size_t)a * w + b;
+            return prolong_at(P, a, b) * (m[k] ? 0.0 : 1.0);
+        };
+        double udi = mi ? __ldg(f + gi) : 0.0;
+        double xi = prolong_at(P, yy, xx) * interior;
+        double b = lap_at(yy, xx, h, w, udi, ud) * interior;
+        double ax = -lap_at(yy, xx, h, w, xi, xv) * interior;
+        double ri = b - ax;
+        P.x[gi] = xi;
+        r[j] = ri;
+        sp[sidx(yy, xx)] = ri;
+        acc[0] += ri * ri;
+        acc[1] += b * b;
+        acc[2] += mi ? udi * udi : 0.0;
+        acc[3] += interior;
+    }
+    // publish the band's boundary rows of r and p0 = r
+    auto publish = [&](double* ex, int parity_off) {
+        for (int c = tid; c < w; c += kBandThreads) {
+            ex[parity_off + ((size_t)band * 2 + 0) * w + c] = sp[sidx(y0, c)];
+            ex[parity_off + ((size_t)band * 2 + 1) * w + c] = sp[sidx(y0 + rows - 1, c)];
+        }
+    };
+    __syncthreads();
+    publish(P.ex_r, 0);
+    publish(P.ex_p, 0);
+    reduce<true, 4>(acc, sh, P);
+    double rs = acc[0];
+    const bool all_mask = acc[3] == 0.0;
+    const double bn = (P.finest && acc[2] != 0.0) ? sqrt(acc[2]) : sqrt(acc[1]);
+    const size_t pstride = (size_t)nb * 2 * w;
+    int it = 0;
+    double margin = 1e300;
+    if (!all_mask && bn != 0.0) {
+        double beta = 0.0;
+        for (int k = 1; k <= P.max_iter; ++k) {
+            it = k;
+            const size_t prev_par = (size_t)((k - 1) & 1) * pstride, cur_par = (size_t)(k & 1) * pstride;
+            // ---- phase 1: p = r + beta p on the band and its halo rows, then p.Ap
+            for (int c = tid; c < w; c += kBandThreads) {
+                if (y0 > 0) {  // last row of the band above
+                    size_t e = ((size_t)(band - 1) * 2 + 1) * w + c;
+                    sp[c] = __ldcg(P.ex_r + e) + beta * __ldcg(P.ex_p + prev_par + e);
+                }
+                if (y0 + rows < h) {  // first row of the band below
+                    size_t e = ((size_t)(band + 1) * 2 + 0) * w + c;
+                    sp[(size_t)(rows + 1) * w + c] = __ldcg(P.ex_r + e) + beta * __ldcg(P.ex_p + prev_par + e);
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < kBandPx; ++j) {
+                int q = tid + j * kBandThreads;
+                if (q < npx) sp[w + q] = r[j] + beta * sp[w + q];
+            }
+            __syncthreads();
+            double d[1] = {0.0};
+#pragma unroll
+            for (int j = 0; j < kBandPx; ++j) {
+                int q = tid + j * kBandThreads;
+                if (q >= npx) continue;
+                int yy = y0 + q / w, xx = q % w;
+                double pi = sp[w + q];
+                double interior = smask[q] ? 0.0 : 1.0;
+                double api = -lap_at(yy, xx, h, w, pi, [&](int a, int b) { return sp[sidx(a, b)]; }) * interior;
+                d[0] += pi * api;
+            }
+            for (int c = tid; c < w; c += kBandThreads) {
+                P.ex_p[cur_par + ((size_t)band * 2 + 0) * w + c] = sp[sidx(y0, c)];
+                P.ex_p[cur_par + ((size_t)band * 2 + 1) * w + c] = sp[sidx(y0 + rows - 1, c)];
+            }
+            reduce<true, 1>(d, sh, P);
+            const double pap = d[0];
+            if (pap <= 0.0 || rs < 1e-300) break;
+            const double alpha = rs / pap;
+            // ---- phase 2: x += alpha p, r -= alpha Ap (Ap recomputed from shared memory), r.r
+            double e1[1] = {0.0};
+#pragma unroll
+            for (int j = 0; j < kBandPx; ++j) {
+                int q = tid + j * kBandThreads;
+                if (q >= npx) continue;
+                int yy = y0 + q / w, xx = q % w;
+                size_t gi = (size_t)yy * w + xx;
+                double pi = sp[w + q];
+                double interior = smask[q] ? 0.0 : 1.0;
+                double api = -lap_at(yy, xx, h, w, pi, [&](int a, int b) { return sp[sidx(a, b)]; }) * interior;
+                P.x[gi] = P.x[gi] + alpha * pi;
+                r[j] = r[j] - alpha * api;
+                e1[0] += r[j] * r[j];
+            }
+            // publish r's boundary rows (read by the neighbours' next phase 1)
+#pragma unroll
+            for (int j = 0; j < kBandPx; ++j) {
+                int q = tid + j * kBandThreads;
+                if (q >= npx) continue;
+                int row = q / w, xx = q % w;
+                if (row == 0) P.ex_r[((size_t)band * 2 + 0) * w + xx] = r[j];
+                if (row == rows - 1) P.ex_r[((size_t)band * 2 + 1) * w + xx] = r[j];
+            }
+            reduce<true, 1>(e1, sh, P);
+            const double rs1 = e1[0];
+            const double lhs = sqrt(rs1), rhs = P.tol * bn;
+            if (rhs > 0.0) margin = fmin(margin, fabs(lhs - rhs) / rhs);
+            if (lhs <= rhs) break;
+            beta = rs1 / rs;
+            rs = rs1;
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < kBandPx; ++j) {
+        int q = tid + j * kBandThreads;
+        if (q >= npx) continue;
+        size_t gi = (size_t)(y0 + q / w) * w + q % w;
+        bool mi = smask[q] != 0;
+        P.u[gi] = all_mask ? __ldg(f + gi) : (mi ? __ldg(f + gi) : 0.0) + P.x[gi];
+    }
+    if (band == 0 && tid == 0) {
+        *P.iters = it;
+        if (P.margin) *P.margin = margin;
+    }
+}
+
 // ---------------------------------------------------------------- strict residual check
 
 __global__ void residual_partials(const double* __restrict__ u, const double* __restrict__ f,
@@ -294,7 +464,7 @@ void pyramid_shapes(int h, int w, std::vector<std::pair<int, int>>& shapes) {
 
 void InpaintWorkspace::reserve(int h, int w, int dev) {
     size_t n = (size_t)h * w;
-    if (n <= cap_px && dev == device) return;
+    if (n <= cap_px && (size_t)w <= cap_w && dev == device) return;
     release();
     device = dev;
     cudaDeviceProp prop;
@@ -311,13 +481,20 @@ void InpaintWorkspace::reserve(int h, int w, int dev) {
     size_t nd = 5 * n + 2 * coarse + n /* u of level 0 scratch */;
     CUDA_CHECK(cudaMalloc(&dbl, nd * sizeof(double)));
     CUDA_CHECK(cudaMalloc(&bytes, coarse + 64));
-    CUDA_CHECK(cudaMalloc(&partials, (size_t)std::max(grid_ctas, 1) * 4 * sizeof(double) + 64 * sizeof(double)));
+    // CG partials (grid_ctas x 4) and the strict-residual partials (<= 1024 blocks x 2)
+    CUDA_CHECK(cudaMalloc(&partials, (size_t)std::max(grid_ctas * 4, 2048) * sizeof(double) + 64 * sizeof(double)));
     CUDA_CHECK(cudaMalloc(&bar, 64 * sizeof(unsigned int)));
     CUDA_CHECK(cudaMemset(bar, 0, 64 * sizeof(unsigned int)));
     CUDA_CHECK(cudaMalloc(&iters, 64 * sizeof(int)));
     CUDA_CHECK(cudaMalloc(&margins, 64 * sizeof(double)));
+    // band-kernel row exchange: r (nb x 2 rows) + p (2 parities x nb x 2 rows)
+    CUDA_CHECK(cudaMalloc(&ex, (size_t)6 * std::max(num_sms, 1) * w * sizeof(double)));
     cap_px = n;
+    cap_w = w;
     cap_coarse = coarse;
+    const char* env = getenv("HIVC_CG_BAND");
+    band_enabled = !(env && env[0] == '0');
+    CUDA_CHECK(cudaFuncSetAttribute(cg_band_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
 }
 
 void InpaintWorkspace::release() {
@@ -327,6 +504,8 @@ void InpaintWorkspace::release() {
     if (bar) cudaFree(bar);
     if (iters) cudaFree(iters);
     if (margins) cudaFree(margins);
+    if (ex) cudaFree(ex);
+    ex = nullptr;
     dbl = nullptr;
     bytes = nullptr;
     partials = nullptr;
@@ -337,7 +516,7 @@ void InpaintWorkspace::release() {
 }
 
 int solve_homogeneous_async(InpaintWorkspace& ws, cudaStream_t s, const double* f, const uint8_t* m, int h, int w,
-                            double tol, int max_iter, double* u_out, int64_t* launches) {
+                            double tol, int max_iter, double* u_out, int64_t* launches, CgProbe* probe) {
     std::vector<std::pair<int, int>> shapes;
     pyramid_shapes(h, w, shapes);
     const int L = (int)shapes.size();
@@ -393,8 +572,29 @@ int solve_homogeneous_async(InpaintWorkspace& ws, cudaStream_t s, const double* 
         P.bar = ws.bar;
         P.iters = ws.iters + (L - 1 - l);
         P.margin = ws.margins + (L - 1 - l);
-        if (P.n <= kSingleCtaMaxPx || ws.grid_ctas == 0) {
+        const bool grid = !(P.n <= kSingleCtaMaxPx || ws.grid_ctas == 0);
+        CgProbe::Launch rec{};
+        if (probe && grid) {
+            CUDA_CHECK(cudaEventCreate(&rec.start));
+            CUDA_CHECK(cudaEventCreate(&rec.stop));
+            CUDA_CHECK(cudaEventRecord(rec.start, s));
+        }
+        // on-chip band kernel when a band fits registers + shared memory
+        int band_rows = (P.h + ws.num_sms - 1) / std::max(ws.num_sms, 1);
+        int nbands = (P.h + band_rows - 1) / band_rows;
+        size_t band_smem = (size_t)(band_rows + 2) * P.w * sizeof(double) + (size_t)band_rows * P.w;
+        bool band = grid && ws.band_enabled && l > 0 ? true : (grid && ws.band_enabled && P.uc != nullptr);
+        band = band && (size_t)band_rows * P.w <= (size_t)kBandPx * kBandThreads && band_smem <= 220 * 1024 &&
+               nbands <= ws.num_sms && P.uc != nullptr;
+        if (!grid) {
             cg_level_kernel<false><<<1, kThreads, 0, s>>>(P);
+        } else if (band) {
+            P.band_rows = band_rows;
+            P.ex_r = ws.ex;
+            P.ex_p = ws.ex + (size_t)2 * nbands * P.w;
+            void* args[] = {&P};
+            CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)cg_band_kernel, dim3(nbands), dim3(kBandThreads), args,
+                                                   band_smem, s));
         } else {
             void* args[] = {&P};
             CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)cg_level_kernel<true>, dim3(ws.grid_ctas),
@@ -402,8 +602,72 @@ int solve_homogeneous_async(InpaintWorkspace& ws, cudaStream_t s, const double* 
         }
         ++*launches;
         CUDA_CHECK(cudaGetLastError());
+        if (probe && grid) {
+            CUDA_CHECK(cudaEventRecord(rec.stop, s));
+            rec.pixels = P.n;
+            rec.solve = (int)probe->solves.size();
+            rec.level = L - 1 - l;
+            probe->launches.push_back(rec);
+        }
+    }
+    if (probe) {
+        // per-level iteration counts of this solve, read back after the stream syncs
+        CgProbe::Solve sv;
+        sv.nlevels = L;
+        for (int l = 0; l < L; ++l) sv.pixels[l] = (int64_t)shapes[L - 1 - l].first * shapes[L - 1 - l].second;
+        sv.host_iters = probe->alloc_iters();
+        if (sv.host_iters) CUDA_CHECK(cudaMemcpyAsync(sv.host_iters, ws.iters, L * sizeof(int), cudaMemcpyDeviceToHost, s));
+        probe->solves.push_back(sv);
     }
     return L;
+}
+
+int* CgProbe::alloc_iters() {
+    if (!host) {
+        if (cudaHostAlloc(&host, kCap * 32 * sizeof(int), cudaHostAllocDefault) != cudaSuccess) host = nullptr;
+    }
+    if (!host || used >= kCap) return nullptr;
+    return host + 32 * used++;
+}
+
+void CgProbe::reset() {
+    for (auto& l : launches) {
+        if (l.start) cudaEventDestroy(l.start);
+        if (l.stop) cudaEventDestroy(l.stop);
+    }
+    launches.clear();
+    solves.clear();
+    used = 0;
+}
+
+CgProbe::~CgProbe() {
+    reset();
+    if (host) cudaFreeHost(host);
+}
+
+void CgProbe::harvest(CgTotals& t) {
+    // after the stream synchronised: accumulate iteration-weighted pixel counts
+    // and the grid-mode launches' device time
+    std::vector<int> it_of_solve_level;
+    for (const Solve& sv : solves) {
+        t.solves += 1;
+        for (int l = 0; l < sv.nlevels; ++l) {
+            int it = sv.host_iters ? sv.host_iters[l] : 0;
+            t.pixel_iters += sv.pixels[l] * it;
+            t.pixel_levels += sv.pixels[l];
+        }
+    }
+    for (const Launch& l : launches) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, l.start, l.stop);
+        const Solve& sv = solves[l.solve];
+        int it = sv.host_iters ? sv.host_iters[l.level] : 0;
+        t.grid_launches += 1;
+        t.grid_seconds += ms * 1e-3;
+        t.grid_pixel_iters += l.pixels * it;
+        t.grid_pixels += l.pixels;
+    }
+    reset();
 }
 
 double strict_relative_residual(InpaintWorkspace& ws, cudaStream_t s, const double* u, const double* f,

@@ -25,7 +25,9 @@ struct InpaintWorkspace {
     int device = -1;
     int num_sms = 0;
     int grid_ctas = 0;  // CTAs of the cooperative (grid-barrier) CG kernel
-    size_t cap_px = 0, cap_coarse = 0;
+    size_t cap_px = 0, cap_coarse = 0, cap_w = 0;
+    double* ex = nullptr;       // band-kernel row exchange buffers
+    bool band_enabled = true;   // HIVC_CG_BAND=0 selects the streaming kernel
     double* dbl = nullptr;
     uint8_t* bytes = nullptr;
     double* partials = nullptr;
@@ -39,11 +41,46 @@ struct InpaintWorkspace {
 
 void pyramid_shapes(int h, int w, std::vector<std::pair<int, int>>& shapes);
 
+// Accumulated CG statistics (algorithmic-byte accounting for the roofline).
+struct CgTotals {
+    int64_t solves = 0;
+    int64_t pixel_iters = 0;       // sum over solves and levels of N_l * it_l
+    int64_t pixel_levels = 0;      // sum of N_l (per-level setup passes)
+    int64_t grid_launches = 0;     // cooperative (multi-CTA) level kernels
+    double grid_seconds = 0;       // their summed device time (CUDA events)
+    int64_t grid_pixel_iters = 0;  // N_l * it_l of those launches
+    int64_t grid_pixels = 0;       // N_l of those launches
+};
+
+// Optional per-solve probe: CUDA events around every cooperative level
+// kernel and an async copy of the per-level iteration counts to pinned memory.
+struct CgProbe {
+    struct Launch {
+        cudaEvent_t start = nullptr, stop = nullptr;
+        int64_t pixels = 0;
+        int solve = 0, level = 0;
+    };
+    struct Solve {
+        int nlevels = 0;
+        int64_t pixels[32] = {};
+        int* host_iters = nullptr;
+    };
+    static constexpr int kCap = 512;
+    std::vector<Launch> launches;
+    std::vector<Solve> solves;
+    int* host = nullptr;
+    int used = 0;
+    int* alloc_iters();
+    void harvest(CgTotals& t);  // call after the stream synchronised
+    void reset();
+    ~CgProbe();
+};
+
 // Queue the full cascadic solve of (f, m) on stream s; u_out receives the
 // finest-level solution.  Returns the number of pyramid levels; per-level
 // iteration counts land in ws.iters (coarse -> fine) on the device.
 int solve_homogeneous_async(InpaintWorkspace& ws, cudaStream_t s, const double* f, const uint8_t* m, int h, int w,
-                            double tol, int max_iter, double* u_out, int64_t* launches);
+                            double tol, int max_iter, double* u_out, int64_t* launches, CgProbe* probe = nullptr);
 
 // Relative residual of the inpainting equation (homogeneous.py:206-211);
 // synchronises the stream.  Returns -1 when ||f|mask|| == 0.
