@@ -166,6 +166,27 @@ int hivc_homog_solve(hivc_ctx* ctx, const double* f, const uint8_t* mask, int32_
         std::vector<int> it(L);
         CUDA_CHECK(cudaMemcpyAsync(it.data(), C.ws.iters, L * sizeof(int), cudaMemcpyDeviceToHost, C.stream));
         CUDA_CHECK(cudaStreamSynchronize(C.stream));
+        if (getenv("HIVC_CG_TRACE") && C.ws.trace) {
+            // phase timing of the finest level (CTA 0, thread 0): mean ns per phase
+            std::vector<unsigned long long> tr(256 * 8);
+            CUDA_CHECK(cudaMemcpy(tr.data(), C.ws.trace, tr.size() * 8, cudaMemcpyDeviceToHost));
+            double acc[6] = {0, 0, 0, 0, 0, 0};
+            int n = 0;
+            for (int k = 2; k < 255 && tr[(k + 1) * 8] != 0; ++k, ++n) {
+                const unsigned long long* t = &tr[k * 8];
+                acc[0] += (double)(t[1] - t[0]);
+                acc[1] += (double)(t[2] - t[1]);
+                acc[2] += (double)(t[3] - t[2]);
+                acc[3] += (double)(t[4] - t[3]);
+                acc[4] += (double)(t[5] - t[4]);
+                acc[5] += (double)(tr[(k + 1) * 8] - t[5]);
+            }
+            if (n)
+                fprintf(stderr,
+                        "[cg trace] %d iters: halo+p %.0f ns | stencil %.0f | reduce1 %.0f | phase2 %.0f | reduce2 %.0f | "
+                        "tail %.0f\n",
+                        n, acc[0] / n, acc[1] / n, acc[2] / n, acc[3] / n, acc[4] / n, acc[5] / n);
+        }
         if (nlevels) *nlevels = L;
         for (int i = 0; i < L && i < 32; ++i) {
             auto s = shapes[L - 1 - i];

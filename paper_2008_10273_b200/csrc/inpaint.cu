@@ -89,6 +89,8 @@ struct CgParams {
     int band_rows;
     double* ex_r;  // [nbands][2][w]: first/last owned row of r
     double* ex_p;  // [2 parity][nbands][2][w]: first/last owned row of p
+    unsigned long long* trace = nullptr;  // diagnostics: per-iteration phase timestamps of CTA 0
+    unsigned long long* stamp = nullptr;  // probe: globaltimer at kernel entry / exit (CTA 0)
 };
 
 __device__ __forceinline__ double prolong_at(const CgParams& P, int y, int xx) {
@@ -117,13 +119,13 @@ __device__ __forceinline__ double lap_at(int y, int xx, int h, int w, double c, 
 }
 
 template <bool kGrid, int NV>
-__device__ __forceinline__ void reduce(double (&v)[NV], double* sh, const CgParams& P) {
+__device__ __forceinline__ void reduce(double (&v)[NV], double* sh, const CgParams& P, unsigned int& epoch) {
     block_sum<NV>(v, sh);
     if (!kGrid) return;
     if (threadIdx.x == 0)
 #pragma unroll
         for (int k = 0; k < NV; ++k) P.partials[blockIdx.x * 4 + k] = v[k];
-    grid_barrier(P.bar, gridDim.x);
+    grid_barrier(P.bar, gridDim.x, epoch);
     const int lane = threadIdx.x & 31;
     if (threadIdx.x < 32) {
 #pragma unroll
@@ -145,6 +147,8 @@ __global__ void __launch_bounds__(kThreads, 1) cg_level_kernel(CgParams P) {
     __shared__ double sh[4 * 32];
     __shared__ double s_mean;
     __shared__ double s_vals[kCoarsest * kCoarsest];
+    unsigned int epoch = 0;
+    if (P.stamp && blockIdx.x == 0 && threadIdx.x == 0) P.stamp[0] = globaltimer_ns();
     const int h = P.h, w = P.w, n = P.n;
     const int stride = gridDim.x * blockDim.x;
     const int t0 = blockIdx.x * blockDim.x + threadIdx.x;
@@ -191,7 +195,7 @@ __global__ void __launch_bounds__(kThreads, 1) cg_level_kernel(CgParams P) {
         acc[2] += mi ? udi * udi : 0.0;
         acc[3] += interior;
     }
-    reduce<kGrid, 4>(acc, sh, P);
+    reduce<kGrid, 4>(acc, sh, P, epoch);
     double rs = acc[0];
     double bn;
     bool all_mask = acc[3] == 0.0;
@@ -222,7 +226,7 @@ __global__ void __launch_bounds__(kThreads, 1) cg_level_kernel(CgParams P) {
                 P.ap[i] = api;
                 d[0] += pi * api;
             }
-            reduce<kGrid, 1>(d, sh, P);
+            reduce<kGrid, 1>(d, sh, P, epoch);
             double pap = d[0];
             if (pap <= 0.0 || rs < 1e-300) break;
             double alpha = rs / pap;
@@ -236,7 +240,7 @@ __global__ void __launch_bounds__(kThreads, 1) cg_level_kernel(CgParams P) {
                 P.r[i] = ri;
                 e[0] += ri * ri;
             }
-            reduce<kGrid, 1>(e, sh, P);
+            reduce<kGrid, 1>(e, sh, P, epoch);
             double rs1 = e[0];
             double lhs = sqrt(rs1), rhs = P.tol * bn;
             if (rhs > 0.0) margin = fmin(margin, fabs(lhs - rhs) / rhs);
@@ -257,174 +261,11 @@ __global__ void __launch_bounds__(kThreads, 1) cg_level_kernel(CgParams P) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         *P.iters = it;
         if (P.margin) *P.margin = margin;
+        if (P.stamp) P.stamp[1] = globaltimer_ns();
     }
 }
 
-// ---------------------------------------------------------------- on-chip CG level kernel
-// One CTA per horizontal band of rows (one CTA per SM).  For the whole level
-// the band's r lives in registers and its p (plus one halo row above and
-// below) in shared memory; x is streamed through global memory.  Only the
-// first/last owned rows of r and p cross CTAs: each CTA publishes them to
-// small exchange buffers, and after the grid barrier its neighbours rebuild
-// their halo p = r + beta p from them.  Per iteration the CTA therefore moves
-// x (16 B/px) + 4 exchange rows instead of every vector, and A p is
-// recomputed from shared memory in the second phase instead of being stored.
-// Same per-pixel float64 expressions as cg_level_kernel.
-constexpr int kBandThreads = 512;
-constexpr int kBandPx = 32;  // max owned pixels per thread: r stays in registers (<= 128 regs)
-
-__global__ void __launch_bounds__(kBandThreads, 1) cg_band_kernel(CgParams P) {
-    extern __shared__ double sp[];  // (rows+2) x w : halo, owned rows, halo
-    __shared__ double sh[4 * 32];
-    const int h = P.h, w = P.w;
-    const int band = blockIdx.x, nb = gridDim.x;
-    const int y0 = band * P.band_rows;
-    const int rows = min(P.band_rows, h - y0);
-    const int npx = rows * w;
-    const int tid = threadIdx.x;
-    const double* __restrict__ f = P.f;
-    const uint8_t* __restrict__ m = P.m;
-    uint8_t* smask = reinterpret_cast<uint8_t*>(sp + (size_t)(P.band_rows + 2) * w);
-    double r[kBandPx];
-    auto sidx = [&](int yy, int xq) -> int { return (yy - y0 + 1) * w + xq; };  // smem row of global y
-
-    // ---- setup (homogeneous.py:64-77); x0 from the coarser level by prolongation
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-    for (int j = 0; j < kBandPx; ++j) {
-        int q = tid + j * kBandThreads;
-        r[j] = 0.0;
-        if (q >= npx) continue;
-        int yy = y0 + q / w, xx = q % w;
-        size_t gi = (size_t)yy * w + xx;
-        bool mi = m[gi] != 0;
-        smask[q] = mi;
-        double interior = mi ? 0.0 : 1.0;
-        auto ud = [&](int a, int b) -> double {
-            size_t k = (size_t)a * w + b;
-            return m[k] ? __ldg(f + k) : 0.0;
-        };
-        auto xv = [&](int a, int b) -> double {
-            size_t k = (size_t)a * w + b;
-            return prolong_at(P, a, b) * (m[k] ? 0.0 : 1.0);
-        };
-        double udi = mi ? __ldg(f + gi) : 0.0;
-        double xi = prolong_at(P, yy, xx) * interior;
-        double b = lap_at(yy, xx, h, w, udi, ud) * interior;
-        double ax = -lap_at(yy, xx, h, w, xi, xv) * interior;
-        double ri = b - ax;
-        P.x[gi] = xi;
-        r[j] = ri;
-        sp[sidx(yy, xx)] = ri;
-        acc[0] += ri * ri;
-        acc[1] += b * b;
-        acc[2] += mi ? udi * udi : 0.0;
-        acc[3] += interior;
-    }
-    // publish the band's boundary rows of r and p0 = r
-    auto publish = [&](double* ex, int parity_off) {
-        for (int c = tid; c < w; c += kBandThreads) {
-            ex[parity_off + ((size_t)band * 2 + 0) * w + c] = sp[sidx(y0, c)];
-            ex[parity_off + ((size_t)band * 2 + 1) * w + c] = sp[sidx(y0 + rows - 1, c)];
-        }
-    };
-    __syncthreads();
-    publish(P.ex_r, 0);
-    publish(P.ex_p, 0);
-    reduce<true, 4>(acc, sh, P);
-    double rs = acc[0];
-    const bool all_mask = acc[3] == 0.0;
-    const double bn = (P.finest && acc[2] != 0.0) ? sqrt(acc[2]) : sqrt(acc[1]);
-    const size_t pstride = (size_t)nb * 2 * w;
-    int it = 0;
-    double margin = 1e300;
-    if (!all_mask && bn != 0.0) {
-        double beta = 0.0;
-        for (int k = 1; k <= P.max_iter; ++k) {
-            it = k;
-            const size_t prev_par = (size_t)((k - 1) & 1) * pstride, cur_par = (size_t)(k & 1) * pstride;
-            // ---- phase 1: p = r + beta p on the band and its halo rows, then p.Ap
-            for (int c = tid; c < w; c += kBandThreads) {
-                if (y0 > 0) {  // last row of the band above
-                    size_t e = ((size_t)(band - 1) * 2 + 1) * w + c;
-                    sp[c] = __ldcg(P.ex_r + e) + beta * __ldcg(P.ex_p + prev_par + e);
-                }
-                if (y0 + rows < h) {  // first row of the band below
-                    size_t e = ((size_t)(band + 1) * 2 + 0) * w + c;
-                    sp[(size_t)(rows + 1) * w + c] = __ldcg(P.ex_r + e) + beta * __ldcg(P.ex_p + prev_par + e);
-                }
-            }
-#pragma unroll
-            for (int j = 0; j < kBandPx; ++j) {
-                int q = tid + j * kBandThreads;
-                if (q < npx) sp[w + q] = r[j] + beta * sp[w + q];
-            }
-            __syncthreads();
-            double d[1] = {0.0};
-#pragma unroll
-            for (int j = 0; j < kBandPx; ++j) {
-                int q = tid + j * kBandThreads;
-                if (q >= npx) continue;
-                int yy = y0 + q / w, xx = q % w;
-                double pi = sp[w + q];
-                double interior = smask[q] ? 0.0 : 1.0;
-                double api = -lap_at(yy, xx, h, w, pi, [&](int a, int b) { return sp[sidx(a, b)]; }) * interior;
-                d[0] += pi * api;
-            }
-            for (int c = tid; c < w; c += kBandThreads) {
-                P.ex_p[cur_par + ((size_t)band * 2 + 0) * w + c] = sp[sidx(y0, c)];
-                P.ex_p[cur_par + ((size_t)band * 2 + 1) * w + c] = sp[sidx(y0 + rows - 1, c)];
-            }
-            reduce<true, 1>(d, sh, P);
-            const double pap = d[0];
-            if (pap <= 0.0 || rs < 1e-300) break;
-            const double alpha = rs / pap;
-            // ---- phase 2: x += alpha p, r -= alpha Ap (Ap recomputed from shared memory), r.r
-            double e1[1] = {0.0};
-#pragma unroll
-            for (int j = 0; j < kBandPx; ++j) {
-                int q = tid + j * kBandThreads;
-                if (q >= npx) continue;
-                int yy = y0 + q / w, xx = q % w;
-                size_t gi = (size_t)yy * w + xx;
-                double pi = sp[w + q];
-                double interior = smask[q] ? 0.0 : 1.0;
-                double api = -lap_at(yy, xx, h, w, pi, [&](int a, int b) { return sp[sidx(a, b)]; }) * interior;
-                P.x[gi] = P.x[gi] + alpha * pi;
-                r[j] = r[j] - alpha * api;
-                e1[0] += r[j] * r[j];
-            }
-            // publish r's boundary rows (read by the neighbours' next phase 1)
-#pragma unroll
-            for (int j = 0; j < kBandPx; ++j) {
-                int q = tid + j * kBandThreads;
-                if (q >= npx) continue;
-                int row = q / w, xx = q % w;
-                if (row == 0) P.ex_r[((size_t)band * 2 + 0) * w + xx] = r[j];
-                if (row == rows - 1) P.ex_r[((size_t)band * 2 + 1) * w + xx] = r[j];
-            }
-            reduce<true, 1>(e1, sh, P);
-            const double rs1 = e1[0];
-            const double lhs = sqrt(rs1), rhs = P.tol * bn;
-            if (rhs > 0.0) margin = fmin(margin, fabs(lhs - rhs) / rhs);
-            if (lhs <= rhs) break;
-            beta = rs1 / rs;
-            rs = rs1;
-        }
-    }
-#pragma unroll
-    for (int j = 0; j < kBandPx; ++j) {
-        int q = tid + j * kBandThreads;
-        if (q >= npx) continue;
-        size_t gi = (size_t)(y0 + q / w) * w + q % w;
-        bool mi = smask[q] != 0;
-        P.u[gi] = all_mask ? __ldg(f + gi) : (mi ? __ldg(f + gi) : 0.0) + P.x[gi];
-    }
-    if (band == 0 && tid == 0) {
-        *P.iters = it;
-        if (P.margin) *P.margin = margin;
-    }
-}
+#include "cg_band.cuh"
 
 // ---------------------------------------------------------------- strict residual check
 
@@ -482,7 +323,8 @@ void InpaintWorkspace::reserve(int h, int w, int dev) {
     CUDA_CHECK(cudaMalloc(&dbl, nd * sizeof(double)));
     CUDA_CHECK(cudaMalloc(&bytes, coarse + 64));
     // CG partials (grid_ctas x 4) and the strict-residual partials (<= 1024 blocks x 2)
-    CUDA_CHECK(cudaMalloc(&partials, (size_t)std::max(grid_ctas * 4, 2048) * sizeof(double) + 64 * sizeof(double)));
+    // [0, 4096): band-setup partials at 4096 (kSetupCtas x 4)
+    CUDA_CHECK(cudaMalloc(&partials, (size_t)(4096 + kSetupCtas * 4 + 64) * sizeof(double)));
     CUDA_CHECK(cudaMalloc(&bar, 64 * sizeof(unsigned int)));
     CUDA_CHECK(cudaMemset(bar, 0, 64 * sizeof(unsigned int)));
     CUDA_CHECK(cudaMalloc(&iters, 64 * sizeof(int)));
@@ -580,19 +422,28 @@ int solve_homogeneous_async(InpaintWorkspace& ws, cudaStream_t s, const double* 
             CUDA_CHECK(cudaEventRecord(rec.start, s));
         }
         // on-chip band kernel when a band fits registers + shared memory
-        int band_rows = (P.h + ws.num_sms - 1) / std::max(ws.num_sms, 1);
-        int nbands = (P.h + band_rows - 1) / band_rows;
-        size_t band_smem = (size_t)(band_rows + 2) * P.w * sizeof(double) + (size_t)band_rows * P.w;
-        bool band = grid && ws.band_enabled && l > 0 ? true : (grid && ws.band_enabled && P.uc != nullptr);
-        band = band && (size_t)band_rows * P.w <= (size_t)kBandPx * kBandThreads && band_smem <= 220 * 1024 &&
-               nbands <= ws.num_sms && P.uc != nullptr;
+        const int band_rows = (P.h + ws.num_sms - 1) / std::max(ws.num_sms, 1);
+        const int nbands = (P.h + band_rows - 1) / band_rows;
+        const size_t band_smem = (size_t)(kBandRows + 2) * (P.w + 2) * sizeof(double) + (size_t)kBandRows * P.w;
+        const bool band = grid && ws.band_enabled && P.uc != nullptr && band_rows <= kBandRows &&
+                          P.w <= kBandCols * kBandThreads && band_smem <= 220 * 1024 && nbands <= ws.num_sms;
+        if (grid) CUDA_CHECK(cudaMemsetAsync(ws.bar, 0, sizeof(unsigned int), s));  // barrier epoch counter
+        if (probe && grid) P.stamp = probe->stamp_slot((int)probe->launches.size());
         if (!grid) {
             cg_level_kernel<false><<<1, kThreads, 0, s>>>(P);
         } else if (band) {
             P.band_rows = band_rows;
             P.ex_r = ws.ex;
             P.ex_p = ws.ex + (size_t)2 * nbands * P.w;
-            void* args[] = {&P};
+            double* setup = ws.partials + 4096;
+            if (getenv("HIVC_CG_TRACE") && l == 0) {
+                if (!ws.trace) CUDA_CHECK(cudaMalloc(&ws.trace, 256 * 8 * sizeof(unsigned long long)));
+                CUDA_CHECK(cudaMemsetAsync(ws.trace, 0, 256 * 8 * sizeof(unsigned long long), s));
+                P.trace = ws.trace;
+            }
+            cg_setup_kernel<<<kSetupCtas, 512, 0, s>>>(P, setup);
+            ++*launches;
+            void* args[] = {&P, &setup};
             CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)cg_band_kernel, dim3(nbands), dim3(kBandThreads), args,
                                                    band_smem, s));
         } else {
@@ -630,6 +481,15 @@ int* CgProbe::alloc_iters() {
     return host + 32 * used++;
 }
 
+unsigned long long* CgProbe::stamp_slot(int i) {
+    if (!stamps_dev) {
+        if (cudaMalloc(&stamps_dev, kStampCap * 2 * sizeof(unsigned long long)) != cudaSuccess) stamps_dev = nullptr;
+        if (stamps_dev) cudaMemset(stamps_dev, 0, kStampCap * 2 * sizeof(unsigned long long));
+    }
+    if (!stamps_dev || i >= kStampCap) return nullptr;
+    return stamps_dev + 2 * i;
+}
+
 void CgProbe::reset() {
     for (auto& l : launches) {
         if (l.start) cudaEventDestroy(l.start);
@@ -643,6 +503,7 @@ void CgProbe::reset() {
 CgProbe::~CgProbe() {
     reset();
     if (host) cudaFreeHost(host);
+    if (stamps_dev) cudaFree(stamps_dev);
 }
 
 void CgProbe::harvest(CgTotals& t) {
@@ -657,9 +518,22 @@ void CgProbe::harvest(CgTotals& t) {
             t.pixel_levels += sv.pixels[l];
         }
     }
-    for (const Launch& l : launches) {
+    // in-kernel globaltimer stamps give the kernel's own duration; the stream
+    // events around a cooperative launch also contain time spent queued
+    // behind other lanes' kernels, so they are only the fallback
+    std::vector<unsigned long long> st;
+    if (stamps_dev && !launches.empty()) {
+        st.resize(2 * std::min<size_t>(launches.size(), kStampCap));
+        cudaMemcpy(st.data(), stamps_dev, st.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+        cudaMemset(stamps_dev, 0, st.size() * sizeof(unsigned long long));
+    }
+    for (size_t i = 0; i < launches.size(); ++i) {
+        const Launch& l = launches[i];
         float ms = 0;
-        cudaEventElapsedTime(&ms, l.start, l.stop);
+        if (2 * i + 1 < st.size() && st[2 * i] && st[2 * i + 1] > st[2 * i])
+            ms = (float)((st[2 * i + 1] - st[2 * i]) * 1e-6);
+        else
+            cudaEventElapsedTime(&ms, l.start, l.stop);
         const Solve& sv = solves[l.solve];
         int it = sv.host_iters ? sv.host_iters[l.level] : 0;
         t.grid_launches += 1;

@@ -27,6 +27,7 @@ struct InpaintWorkspace {
     int grid_ctas = 0;  // CTAs of the cooperative (grid-barrier) CG kernel
     size_t cap_px = 0, cap_coarse = 0, cap_w = 0;
     double* ex = nullptr;       // band-kernel row exchange buffers
+    unsigned long long* trace = nullptr;  // HIVC_CG_TRACE diagnostics (finest level phase timestamps)
     bool band_enabled = true;   // HIVC_CG_BAND=0 selects the streaming kernel
     double* dbl = nullptr;
     uint8_t* bytes = nullptr;
@@ -66,11 +67,14 @@ struct CgProbe {
         int* host_iters = nullptr;
     };
     static constexpr int kCap = 512;
+    static constexpr int kStampCap = 4096;
     std::vector<Launch> launches;
     std::vector<Solve> solves;
     int* host = nullptr;
     int used = 0;
+    unsigned long long* stamps_dev = nullptr;  // [kStampCap][2] globaltimer entry/exit per launch
     int* alloc_iters();
+    unsigned long long* stamp_slot(int i);
     void harvest(CgTotals& t);  // call after the stream synchronised
     void reset();
     ~CgProbe();

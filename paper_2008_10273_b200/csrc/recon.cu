@@ -20,8 +20,8 @@
 
 namespace hivc {
 
-__device__ __forceinline__ double flow_lookup(const int32_t* __restrict__ nodes, const double* __restrict__ vals, int x,
-                                              int y) {
+// Leaf node of the flow tree containing pixel (x, y).
+__device__ __forceinline__ int flow_leaf(const int32_t* __restrict__ nodes, int x, int y) {
     int i = 0;
     int a = __ldg(nodes);
     while (a & 3) {
@@ -30,7 +30,12 @@ __device__ __forceinline__ double flow_lookup(const int32_t* __restrict__ nodes,
         i = right ? __ldg(nodes + 2 * i + 1) : i + 1;
         a = __ldg(nodes + 2 * i);
     }
-    return __ldg(vals + __ldg(nodes + 2 * i + 1));
+    return i;
+}
+
+__device__ __forceinline__ double flow_lookup(const int32_t* __restrict__ nodes, const double* __restrict__ vals, int x,
+                                              int y) {
+    return __ldg(vals + __ldg(nodes + 2 * flow_leaf(nodes, x, y) + 1));
 }
 
 template <typename RT>
@@ -69,6 +74,19 @@ __global__ void __launch_bounds__(256) frame_kernel(FrameArgs A) {
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int tx = blockIdx.x * 8 + wid;
 
+    // ---- flow: leaves are axis-aligned rectangles, so when both corners of
+    // the 64x8 strip fall in the same leaf the whole strip has one (u, v)
+    __shared__ double s_flow[2];
+    __shared__ int s_flow_uniform[2];
+    if (kInter && threadIdx.x < 2) {
+        const int c = threadIdx.x;
+        const int xa = blockIdx.x * 64, ya = ty * 8;
+        const int xb = min(xa + 63, w - 1), yb = min(ya + 7, h - 1);
+        int la = flow_leaf(A.flow.nodes[c], xa, ya);
+        int lb = flow_leaf(A.flow.nodes[c], xb, yb);
+        s_flow_uniform[c] = la == lb;
+        s_flow[c] = __ldg(A.flow.vals[c] + __ldg(A.flow.nodes[c] + 2 * la + 1));
+    }
     // ---- residual blocks of this strip
     if (lane == 0) {
         s_coded[0][wid] = 0;
@@ -107,8 +125,8 @@ __global__ void __launch_bounds__(256) frame_kernel(FrameArgs A) {
         double pred[C];
         if (kInter) {
             // flow.py:94-127 — coordinates clamped before flooring, taps summed w00..w11
-            double u = flow_lookup(A.flow.nodes[0], A.flow.vals[0], x, y);
-            double v = flow_lookup(A.flow.nodes[1], A.flow.vals[1], x, y);
+            double u = s_flow_uniform[0] ? s_flow[0] : flow_lookup(A.flow.nodes[0], A.flow.vals[0], x, y);
+            double v = s_flow_uniform[1] ? s_flow[1] : flow_lookup(A.flow.nodes[1], A.flow.vals[1], x, y);
             double sx = fmin(fmax((double)x + u, 0.0), (double)(w - 1));
             double sy = fmin(fmax((double)y + v, 0.0), (double)(h - 1));
             int x0 = (int)floor(sx), y0 = (int)floor(sy);
