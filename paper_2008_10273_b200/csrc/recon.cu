@@ -67,66 +67,43 @@ __device__ __forceinline__ void residual_block(const ResDev& R, const ResGroupDe
 template <bool kInter, int C, typename RT>
 __global__ void __launch_bounds__(256) frame_kernel(FrameArgs A) {
     __shared__ double s_res[C][8][64];
-    __shared__ int s_coded[2][8];
     const int h = A.h, w = A.w;
     const int nbx = (w + 7) >> 3;
     const int ty = blockIdx.y;
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int tx = blockIdx.x * 8 + wid;
 
-    // ---- flow: leaves are axis-aligned rectangles, so when both corners of
-    // the 64x8 strip fall in the same leaf the whole strip has one (u, v)
-    __shared__ double s_flow[2];
-    __shared__ int s_flow_uniform[2];
-    if (kInter && threadIdx.x < 2) {
-        const int c = threadIdx.x;
-        const int xa = blockIdx.x * 64, ya = ty * 8;
-        const int xb = min(xa + 63, w - 1), yb = min(ya + 7, h - 1);
-        int la = flow_leaf(A.flow.nodes[c], xa, ya);
-        int lb = flow_leaf(A.flow.nodes[c], xb, yb);
-        s_flow_uniform[c] = la == lb;
-        s_flow[c] = __ldg(A.flow.vals[c] + __ldg(A.flow.nodes[c] + 2 * la + 1));
-    }
-    // ---- residual blocks of this strip
-    if (lane == 0) {
-        s_coded[0][wid] = 0;
-        s_coded[1][wid] = 0;
-    }
-    __syncwarp();
-    if (A.res.ngroups > 0 && tx < nbx) {
-        const size_t t = (size_t)ty * nbx + tx;
-        int chan = 0;
-        for (int gi = 0; gi < A.res.ngroups; ++gi) {
-            const ResGroupDev& G = A.res.g[gi];
-            uint64_t word = __ldg(G.tile_words + (t >> 6));
-            bool coded = (word >> (t & 63)) & 1ull;
-            if (coded) {
-                int b = __ldg(G.word_prefix + (t >> 6)) + __popcll(word & ((1ull << (t & 63)) - 1ull));
-                if (lane < 8)
-                    for (int ci = 0; ci < G.nplanes; ++ci) residual_block(A.res, G, b, ci, &s_res[chan + ci][wid][0], lane);
-                if (lane == 0) s_coded[gi][wid] = 1;
-            }
-            chan += G.nplanes;
+    // One warp per 8x8 tile: lane l owns column l % 8 of rows l / 8 and l / 8 + 4.
+    // The prediction loads are issued first; the tile's residual block is
+    // rebuilt (lanes 0..7) while they are in flight; no CTA-wide barrier.
+    const int lx = lane & 7, ly = lane >> 3;
+    const int x = tx * 8 + lx;
+    const bool tile_ok = tx < nbx;
+    double pred[2][C];
+    bool live[2];
+    // ---- prediction
+    if (kInter) {
+        // flow leaves are axis-aligned rectangles: if the tile's two corners fall in
+        // the same leaf the whole tile has one (u, v); lanes 0..3 test u/v corners
+        int leaf = 0;
+        if (tile_ok && lane < 4) {
+            const int c = lane >> 1;
+            const int xc = (lane & 1) ? min(tx * 8 + 7, w - 1) : tx * 8;
+            const int yc = (lane & 1) ? min(ty * 8 + 7, h - 1) : ty * 8;
+            leaf = flow_leaf(A.flow.nodes[c], xc, yc);
         }
-    }
-    __syncthreads();
-
-    // ---- pixels: 64 x 8 strip, 2 rows per thread
-    const int px = threadIdx.x & 63;
-    const int x = blockIdx.x * 64 + px;
-    if (x >= w) return;
-    const int tile = px >> 3;
+        const int lu0 = __shfl_sync(0xffffffffu, leaf, 0), lu1 = __shfl_sync(0xffffffffu, leaf, 1);
+        const int lv0 = __shfl_sync(0xffffffffu, leaf, 2), lv1 = __shfl_sync(0xffffffffu, leaf, 3);
 #pragma unroll
-    for (int rr = 0; rr < 2; ++rr) {
-        const int row = (threadIdx.x >> 6) + 4 * rr;
-        const int y = ty * 8 + row;
-        if (y >= h) continue;
-        const size_t k = (size_t)y * w + x;
-        double pred[C];
-        if (kInter) {
+        for (int rr = 0; rr < 2; ++rr) {
+            const int y = ty * 8 + ly + 4 * rr;
+            live[rr] = tile_ok && x < w && y < h;
+            if (!live[rr]) continue;
             // flow.py:94-127 — coordinates clamped before flooring, taps summed w00..w11
-            double u = s_flow_uniform[0] ? s_flow[0] : flow_lookup(A.flow.nodes[0], A.flow.vals[0], x, y);
-            double v = s_flow_uniform[1] ? s_flow[1] : flow_lookup(A.flow.nodes[1], A.flow.vals[1], x, y);
+            double u = lu0 == lu1 ? __ldg(A.flow.vals[0] + __ldg(A.flow.nodes[0] + 2 * lu0 + 1))
+                                  : flow_lookup(A.flow.nodes[0], A.flow.vals[0], x, y);
+            double v = lv0 == lv1 ? __ldg(A.flow.vals[1] + __ldg(A.flow.nodes[1] + 2 * lv0 + 1))
+                                  : flow_lookup(A.flow.nodes[1], A.flow.vals[1], x, y);
             double sx = fmin(fmax((double)x + u, 0.0), (double)(w - 1));
             double sy = fmin(fmax((double)y + v, 0.0), (double)(h - 1));
             int x0 = (int)floor(sx), y0 = (int)floor(sy);
@@ -138,19 +115,49 @@ __global__ void __launch_bounds__(256) frame_kernel(FrameArgs A) {
 #pragma unroll
             for (int c = 0; c < C; ++c) {
                 const void* p = A.prev[c];
-                pred[c] = ((w00 * ld_plane<RT>(p, i00) + w01 * ld_plane<RT>(p, i01)) + w10 * ld_plane<RT>(p, i10)) +
-                          w11 * ld_plane<RT>(p, i11);
+                pred[rr][c] = ((w00 * ld_plane<RT>(p, i00) + w01 * ld_plane<RT>(p, i01)) + w10 * ld_plane<RT>(p, i10)) +
+                              w11 * ld_plane<RT>(p, i11);
             }
-        } else {
-#pragma unroll
-            for (int c = 0; c < C; ++c) pred[c] = __ldg(A.u[c] + k);
         }
+    } else {
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+            const int y = ty * 8 + ly + 4 * rr;
+            live[rr] = tile_ok && x < w && y < h;
+#pragma unroll
+            for (int c = 0; c < C; ++c) pred[rr][c] = live[rr] ? __ldg(A.u[c] + (size_t)y * w + x) : 0.0;
+        }
+    }
+    // ---- residual block(s) of this tile
+    bool coded[2] = {false, false};
+    if (A.res.ngroups > 0 && tile_ok) {
+        const size_t t = (size_t)ty * nbx + tx;
+        int chan = 0;
+        for (int gi = 0; gi < A.res.ngroups; ++gi) {
+            const ResGroupDev& G = A.res.g[gi];
+            uint64_t word = __ldg(G.tile_words + (t >> 6));
+            coded[gi] = (word >> (t & 63)) & 1ull;
+            if (coded[gi]) {
+                int b = __ldg(G.word_prefix + (t >> 6)) + __popcll(word & ((1ull << (t & 63)) - 1ull));
+                if (lane < 8)
+                    for (int ci = 0; ci < G.nplanes; ++ci) residual_block(A.res, G, b, ci, &s_res[chan + ci][wid][0], lane);
+            }
+            chan += G.nplanes;
+        }
+        __syncwarp();
+    }
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+        if (!live[rr]) continue;
+        const int row = ly + 4 * rr;
+        const int y = ty * 8 + row;
+        const size_t k = (size_t)y * w + x;
         int rec[C];
 #pragma unroll
         for (int c = 0; c < C; ++c) {
             const int gi = c == 0 ? 0 : 1;
-            double res = s_coded[gi][tile] ? s_res[c][tile][row * 8 + (px & 7)] : 0.0;
-            double v = rint(rint(pred[c]) + res);
+            double res = coded[gi] ? s_res[c][wid][row * 8 + lx] : 0.0;
+            double v = rint(rint(pred[rr][c]) + res);
             const double lo = (C == 3 && c > 0) ? -255.0 : 0.0;
             v = fmin(fmax(v, lo), 255.0);
             rec[c] = (int)v;
