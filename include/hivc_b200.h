@@ -140,6 +140,23 @@ int hivc_block_reconstruct(hivc_ctx* ctx, const double* mc, const double* a, con
 int hivc_block_fit(hivc_ctx* ctx, const double* f_blocks, const uint64_t* masks, int32_t n,
                    double* c_out, double* a_out);
 
+/* ------------------------------------------------------------------ Brox optic flow (encoder side)
+ * Replaces flow.flow_brox (flow.py:187-278): backward flow frame_t -> frame_prev,
+ * float64, same pyramid / warps / lagged nonlinearity / damped Jacobi / median
+ * as the reference.  frame_t, frame_prev, u, v: device float64 planes (h*w).
+ * taps_presmooth / taps_antialias: HOST arrays with scipy's normalised 1-D
+ * Gaussian taps for sigma = presmooth_sigma and 0.5 / pyramid_scale
+ * (scipy.ndimage._gaussian_kernel1d, truncate 4.0; length 2r+1).
+ */
+typedef struct hivc_brox_params {
+    double alpha, gamma, pyramid_scale;
+    int32_t min_size, warps, fixed_point_iters, solver_iters;
+    double eps, presmooth_sigma;
+} hivc_brox_params;
+int hivc_brox(hivc_ctx* ctx, const double* frame_t, const double* frame_prev, int32_t h, int32_t w,
+              const hivc_brox_params* params, const double* taps_presmooth, int32_t ntaps_presmooth,
+              const double* taps_antialias, int32_t ntaps_antialias, double* u, double* v);
+
 /* ------------------------------------------------------------------ stream decode
  * Replaces codec.decode (codec.py:484-563) for the GOP range [gop_begin, gop_end):
  * frames are written as uint8 planes, layout [frame][channel][h][w] (gray: the

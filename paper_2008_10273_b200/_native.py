@@ -69,6 +69,18 @@ _proto("hivc_decode", C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_int32, C.
 _proto("hivc_decode_multi", C.c_int, C.c_void_p, C.c_int32, C.POINTER(C.c_void_p), c_size_p, c_int_p, c_int_p,
        C.POINTER(C.c_void_p), C.c_int32, c_dbl_p)
 _proto("hivc_ctx_bytes", C.c_int, C.c_void_p, c_i64_p, c_i64_p)
+
+
+class BroxParamsC(C.Structure):
+    _fields_ = [
+        ("alpha", C.c_double), ("gamma", C.c_double), ("pyramid_scale", C.c_double),
+        ("min_size", C.c_int32), ("warps", C.c_int32), ("fixed_point_iters", C.c_int32), ("solver_iters", C.c_int32),
+        ("eps", C.c_double), ("presmooth_sigma", C.c_double),
+    ]
+
+
+_proto("hivc_brox", C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.POINTER(BroxParamsC),
+       c_dbl_p, C.c_int32, c_dbl_p, C.c_int32, C.c_void_p, C.c_void_p)
 _proto("hivc_ctx_set_stage_timing", C.c_int, C.c_void_p, C.c_int32)
 _proto("hivc_ctx_decode_stats", C.c_int, C.c_void_p, c_dbl_p, C.c_int32)
 

@@ -5,6 +5,7 @@
 #include <string>
 #include <vector>
 
+#include "brox.h"
 #include "decode.h"
 #include "inpaint.h"
 #include "parse.h"
@@ -244,6 +245,36 @@ int hivc_block_fit(hivc_ctx* ctx, const double* f_blocks, const uint64_t* masks,
         CUDA_CHECK(cudaStreamSynchronize(C.stream));
         if (st == 1) hivc::fail(HIVC_E_PSEUDODIFF, "block mask needs at least one point");
         if (st == 2) hivc::fail(HIVC_E_PSEUDODIFF, "singular coefficient system");
+    });
+}
+
+int hivc_brox(hivc_ctx* ctx, const double* frame_t, const double* frame_prev, int32_t h, int32_t w,
+              const hivc_brox_params* params, const double* taps_presmooth, int32_t ntaps_presmooth,
+              const double* taps_antialias, int32_t ntaps_antialias, double* u, double* v) {
+    return guarded([&] {
+        if (!ctx || !params) hivc::fail(HIVC_E_ARGUMENT, "null argument");
+        if (h < 2 || w < 2) hivc::fail(HIVC_E_FLOW, "flow needs planes of at least 2x2");
+        if (ntaps_presmooth > 63 || ntaps_antialias > 63 || ntaps_antialias < 1)
+            hivc::fail(HIVC_E_ARGUMENT, "Gaussian radius out of range");
+        if (!(params->pyramid_scale > 0 && params->pyramid_scale < 1))
+            hivc::fail(HIVC_E_FLOW, "pyramid_scale must lie in (0, 1)");
+        hivc::Context& C = ctx->c;
+        CUDA_CHECK(cudaSetDevice(C.device));
+        hivc::BroxParamsC P;
+        P.alpha = params->alpha;
+        P.gamma = params->gamma;
+        P.pyramid_scale = params->pyramid_scale;
+        P.min_size = params->min_size;
+        P.warps = params->warps;
+        P.fixed_point_iters = params->fixed_point_iters;
+        P.solver_iters = params->solver_iters;
+        P.eps = params->eps;
+        P.presmooth_sigma = params->presmooth_sigma;
+        int64_t launches = 0;
+        hivc::brox_flow(C.brox, C.stream, frame_t, frame_prev, h, w, P, taps_presmooth, ntaps_presmooth, taps_antialias,
+                        ntaps_antialias, u, v, &launches);
+        C.launches += launches;
+        CUDA_CHECK(cudaStreamSynchronize(C.stream));
     });
 }
 

@@ -1,0 +1,421 @@
+// Brox-style variational backward flow (encoder side), reference flow.py:187-278.
+//
+// Float64 replay of the reference: scipy's Gaussian (separable 1-D
+// correlations along y then x, reflect boundaries, symmetric accumulation
+// centre-first then outermost pair inwards), the pixel-centre bilinear
+// pyramid, clamped bilinear warp, one-sided/central differences, the lagged
+// nonlinearity (psi_d, psi_g, psi_s), half-point diffusivities with zero
+// border flux, damped Jacobi on the 2x2 systems, [-1, 1] increment clip and
+// the 3x3 'nearest' median.  Every expression keeps numpy's association and
+// FMA contraction is off, so the GPU flow matches the reference to rounding
+// of ~1 ulp (tests/test_gpu_parity.py).
+//
+// Structure-of-arrays float64 planes; one launch per stage (the 30 Jacobi
+// sweeps are 30 launches of one small kernel) — captured per level in a
+// CUDA graph by the host driver.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "brox.h"
+#include "inpaint.h"
+
+namespace hivc {
+
+namespace {
+
+constexpr int kT = 256;
+
+inline int nblk(size_t n) { return (int)std::min<size_t>((n + kT - 1) / kT, 148 * 32); }
+
+#define GRID_LOOP(i, n) for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < (n); i += (size_t)gridDim.x * blockDim.x)
+
+__constant__ double c_taps[64];
+
+// scipy.ndimage.correlate1d, mode 'reflect' (symmetric weights path)
+__global__ void gauss_axis_kernel(const double* __restrict__ src, double* __restrict__ dst, int h, int w, int r,
+                                  int axis) {
+    const size_t n = (size_t)h * w;
+    GRID_LOOP(i, n) {
+        const int y = (int)(i / w), x = (int)(i % w);
+        const int len = axis == 0 ? h : w;
+        const int pos = axis == 0 ? y : x;
+        auto at = [&](int p) -> double {
+            if (p < 0) p = -p - 1;
+            if (p >= len) p = 2 * len - p - 1;
+            return axis == 0 ? src[(size_t)p * w + x] : src[(size_t)y * w + p];
+        };
+        double acc = at(pos) * c_taps[r];
+        for (int j = -r; j < 0; ++j) acc = acc + (at(pos + j) + at(pos - j)) * c_taps[r + j];
+        dst[i] = acc;
+    }
+}
+
+// bilinear_resize (flow.py:69-86), optionally * scale (flow upsampling, flow.py:239-240)
+__global__ void resize_kernel(const double* __restrict__ src, int ih, int iw, double* __restrict__ dst, int h, int w,
+                              double scale, int use_scale) {
+    const size_t n = (size_t)h * w;
+    GRID_LOOP(i, n) {
+        const int y = (int)(i / w), x = (int)(i % w);
+        double v;
+        if (ih == h && iw == w) {
+            v = src[i];
+        } else {
+            double ys = ((double)y + 0.5) * ((double)ih / (double)h) - 0.5;
+            double xs = ((double)x + 0.5) * ((double)iw / (double)w) - 0.5;
+            ys = fmin(fmax(ys, 0.0), (double)(ih - 1));
+            xs = fmin(fmax(xs, 0.0), (double)(iw - 1));
+            int y0 = (int)floor(ys), x0 = (int)floor(xs);
+            int y1 = min(y0 + 1, ih - 1), x1 = min(x0 + 1, iw - 1);
+            double fy = ys - (double)y0, fx = xs - (double)x0;
+            double top = (1 - fx) * src[(size_t)y0 * iw + x0] + fx * src[(size_t)y0 * iw + x1];
+            double bot = (1 - fx) * src[(size_t)y1 * iw + x0] + fx * src[(size_t)y1 * iw + x1];
+            v = (1 - fy) * top + fy * bot;
+        }
+        dst[i] = use_scale ? v * scale : v;
+    }
+}
+
+__device__ __forceinline__ double ddx_at(const double* a, int y, int x, int w) {  // flow.py:135-140
+    const double* r = a + (size_t)y * w;
+    if (x == 0) return r[1] - r[0];
+    if (x == w - 1) return r[w - 1] - r[w - 2];
+    return 0.5 * (r[x + 1] - r[x - 1]);
+}
+__device__ __forceinline__ double ddy_at(const double* a, int y, int x, int h, int w) {  // flow.py:143-148
+    if (y == 0) return a[(size_t)w + x] - a[x];
+    if (y == h - 1) return a[(size_t)(h - 1) * w + x] - a[(size_t)(h - 2) * w + x];
+    return 0.5 * (a[(size_t)(y + 1) * w + x] - a[(size_t)(y - 1) * w + x]);
+}
+
+// clamped bilinear warp of tgt along (u, v) (flow.py:94-127)
+__global__ void warp1_kernel(const double* __restrict__ tgt, const double* __restrict__ u, const double* __restrict__ v,
+                             double* __restrict__ out, int h, int w) {
+    const size_t n = (size_t)h * w;
+    GRID_LOOP(k, n) {
+        const int y = (int)(k / w), x = (int)(k % w);
+        double sx = fmin(fmax((double)x + u[k], 0.0), (double)(w - 1));
+        double sy = fmin(fmax((double)y + v[k], 0.0), (double)(h - 1));
+        int x0 = (int)floor(sx), y0 = (int)floor(sy);
+        int x1 = min(x0 + 1, w - 1), y1 = min(y0 + 1, h - 1);
+        double fx = sx - (double)x0, fy = sy - (double)y0;
+        double w00 = (1 - fy) * (1 - fx), w01 = (1 - fy) * fx, w10 = fy * (1 - fx), w11 = fy * fx;
+        out[k] = ((w00 * tgt[(size_t)y0 * w + x0] + w01 * tgt[(size_t)y0 * w + x1]) + w10 * tgt[(size_t)y1 * w + x0]) +
+                 w11 * tgt[(size_t)y1 * w + x1];
+    }
+}
+
+struct Lin {  // linearisation at the current warp (flow.py:222-230)
+    double *ix, *iy, *iz, *ixx, *ixy, *iyy, *ixz, *iyz;
+};
+
+__global__ void deriv1_kernel(const double* __restrict__ wp, const double* __restrict__ ref, Lin L, int h, int w) {
+    const size_t n = (size_t)h * w;
+    GRID_LOOP(k, n) {
+        const int y = (int)(k / w), x = (int)(k % w);
+        double dxw = ddx_at(wp, y, x, w), dxr = ddx_at(ref, y, x, w);
+        double dyw = ddy_at(wp, y, x, h, w), dyr = ddy_at(ref, y, x, h, w);
+        L.ix[k] = 0.5 * (dxw + dxr);
+        L.iy[k] = 0.5 * (dyw + dyr);
+        L.iz[k] = wp[k] - ref[k];
+        L.ixz[k] = dxw - dxr;
+        L.iyz[k] = dyw - dyr;
+    }
+}
+
+__global__ void deriv2_kernel(Lin L, int h, int w) {
+    const size_t n = (size_t)h * w;
+    GRID_LOOP(k, n) {
+        const int y = (int)(k / w), x = (int)(k % w);
+        L.ixx[k] = ddx_at(L.ix, y, x, w);
+        L.ixy[k] = ddy_at(L.ix, y, x, h, w);
+        L.iyy[k] = ddy_at(L.iy, y, x, h, w);
+    }
+}
+
+struct Sys {  // per fixed-point step: 2x2 systems + diffusivity (flow.py:233-250)
+    double *psi_d, *psi_g, *psi_s, *a11, *a12, *a22, *b1f, *b2f, *su, *sv;
+};
+
+// psi_d, psi_g (pointwise) and psi_s (needs neighbours of u+du, v+dv)
+__global__ void robust_kernel(Lin L, Sys S, const double* __restrict__ u, const double* __restrict__ v,
+                              const double* __restrict__ du, const double* __restrict__ dv, int h, int w, double gamma,
+                              double eps2) {
+    const size_t n = (size_t)h * w;
+    GRID_LOOP(k, n) {
+        const int y = (int)(k / w), x = (int)(k % w);
+        double rb = (L.iz[k] + L.ix[k] * du[k]) + L.iy[k] * dv[k];
+        S.psi_d[k] = 1.0 / sqrt(rb * rb + eps2);
+        double rgx = (L.ixz[k] + L.ixx[k] * du[k]) + L.ixy[k] * dv[k];
+        double rgy = (L.iyz[k] + L.ixy[k] * du[k]) + L.iyy[k] * dv[k];
+        S.psi_g[k] = gamma / sqrt((rgx * rgx + rgy * rgy) + eps2);
+        // ut = u + du, vt = v + dv evaluated at the stencil points
+        auto ut = [&](int yy, int xx) { size_t q = (size_t)yy * w + xx; return u[q] + du[q]; };
+        auto vt = [&](int yy, int xx) { size_t q = (size_t)yy * w + xx; return v[q] + dv[q]; };
+        auto dx = [&](auto f) {
+            if (x == 0) return f(y, 1) - f(y, 0);
+            if (x == w - 1) return f(y, w - 1) - f(y, w - 2);
+            return 0.5 * (f(y, x + 1) - f(y, x - 1));
+        };
+        auto dy = [&](auto f) {
+            if (y == 0) return f(1, x) - f(0, x);
+            if (y == h - 1) return f(h - 1, x) - f(h - 2, x);
+            return 0.5 * (f(y + 1, x) - f(y - 1, x));
+        };
+        double gux = dx(ut), guy = dy(ut), gvx = dx(vt), gvy = dy(vt);
+        double g2 = ((gux * gux + guy * guy) + gvx * gvx) + gvy * gvy;
+        S.psi_s[k] = fmax(1.0 / sqrt(g2 + eps2), 0.05);
+    }
+}
+
+// half-point weights with zero border flux (flow.py:173-184), edge-padded neighbours
+struct W4 {
+    double n, s, w, e;
+};
+__device__ __forceinline__ W4 weights_at(const double* __restrict__ psi, int y, int x, int h, int w) {
+    const size_t k = (size_t)y * w + x;
+    const double c = psi[k];
+    W4 r;
+    r.n = y == 0 ? 0.0 : 0.5 * (c + psi[k - w]);
+    r.s = y == h - 1 ? 0.0 : 0.5 * (c + psi[k + w]);
+    r.w = x == 0 ? 0.0 : 0.5 * (c + psi[k - 1]);
+    r.e = x == w - 1 ? 0.0 : 0.5 * (c + psi[k + 1]);
+    return r;
+}
+// _neighbor_sums with edge padding (flow.py:162-170)
+__device__ __forceinline__ double nsum(const double* __restrict__ f, const W4& W, int y, int x, int h, int w) {
+    const size_t k = (size_t)y * w + x;
+    double fn = y == 0 ? f[k] : f[k - w];
+    double fs = y == h - 1 ? f[k] : f[k + w];
+    double fw = x == 0 ? f[k] : f[k - 1];
+    double fe = x == w - 1 ? f[k] : f[k + 1];
+    return ((W.n * fn + W.s * fs) + W.w * fw) + W.e * fe;
+}
+
+__global__ void system_kernel(Lin L, Sys S, const double* __restrict__ u, const double* __restrict__ v, int h, int w,
+                              double alpha) {
+    const size_t n = (size_t)h * w;
+    GRID_LOOP(k, n) {
+        const int y = (int)(k / w), x = (int)(k % w);
+        W4 W = weights_at(S.psi_s, y, x, h, w);
+        double wsum = ((W.n + W.s) + W.w) + W.e;
+        double pd = S.psi_d[k], pg = S.psi_g[k];
+        double ix = L.ix[k], iy = L.iy[k], iz = L.iz[k], ixx = L.ixx[k], ixy = L.ixy[k], iyy = L.iyy[k];
+        double ixz = L.ixz[k], iyz = L.iyz[k];
+        S.a11[k] = ((pd * ix) * ix + pg * (ixx * ixx + ixy * ixy)) + alpha * wsum;
+        S.a12[k] = (pd * ix) * iy + pg * (ixx * ixy + ixy * iyy);
+        S.a22[k] = ((pd * iy) * iy + pg * (ixy * ixy + iyy * iyy)) + alpha * wsum;
+        S.b1f[k] = ((-pd) * ix) * iz - pg * (ixx * ixz + ixy * iyz);
+        S.b2f[k] = ((-pd) * iy) * iz - pg * (ixy * ixz + iyy * iyz);
+        S.su[k] = nsum(u, W, y, x, h, w) - wsum * u[k];
+        S.sv[k] = nsum(v, W, y, x, h, w) - wsum * v[k];
+    }
+}
+
+// one damped Jacobi sweep of the coupled 2x2 systems (flow.py:251-262); the
+// last sweep also applies the [-1, 1] clip (flow.py:265-266)
+__global__ void jacobi_kernel(Sys S, const double* __restrict__ du, const double* __restrict__ dv,
+                              double* __restrict__ du_out, double* __restrict__ dv_out, int h, int w, double alpha,
+                              int clip) {
+    const size_t n = (size_t)h * w;
+    GRID_LOOP(k, n) {
+        const int y = (int)(k / w), x = (int)(k % w);
+        W4 W = weights_at(S.psi_s, y, x, h, w);
+        double b1 = S.b1f[k] + alpha * (S.su[k] + nsum(du, W, y, x, h, w));
+        double b2 = S.b2f[k] + alpha * (S.sv[k] + nsum(dv, W, y, x, h, w));
+        double a11 = S.a11[k], a12 = S.a12[k], a22 = S.a22[k];
+        double det = a11 * a22 - a12 * a12;
+        det = fabs(det) < 1e-12 ? 1e-12 : det;
+        double dun = (a22 * b1 - a12 * b2) / det;
+        double dvn = (a11 * b2 - a12 * b1) / det;
+        double a = 0.5 * du[k] + 0.5 * dun;
+        double b = 0.5 * dv[k] + 0.5 * dvn;
+        if (clip) {
+            a = fmin(fmax(a, -1.0), 1.0);
+            b = fmin(fmax(b, -1.0), 1.0);
+        }
+        du_out[k] = a;
+        dv_out[k] = b;
+    }
+}
+
+__device__ __forceinline__ void cswap(double& a, double& b) {
+    double lo = fmin(a, b), hi = fmax(a, b);
+    a = lo;
+    b = hi;
+}
+
+// u = median3(u + du) with 'nearest' boundaries (flow.py:269-276)
+__global__ void median_update_kernel(const double* __restrict__ u, const double* __restrict__ du,
+                                     double* __restrict__ out, int h, int w) {
+    const size_t n = (size_t)h * w;
+    GRID_LOOP(k, n) {
+        const int y = (int)(k / w), x = (int)(k % w);
+        double a[9];
+        int t = 0;
+        for (int dy = -1; dy <= 1; ++dy)
+            for (int dx = -1; dx <= 1; ++dx) {
+                int yy = min(max(y + dy, 0), h - 1), xx = min(max(x + dx, 0), w - 1);
+                size_t q = (size_t)yy * w + xx;
+                a[t++] = u[q] + du[q];
+            }
+        // median of 9 (Paeth's network)
+        cswap(a[1], a[2]); cswap(a[4], a[5]); cswap(a[7], a[8]);
+        cswap(a[0], a[1]); cswap(a[3], a[4]); cswap(a[6], a[7]);
+        cswap(a[1], a[2]); cswap(a[4], a[5]); cswap(a[7], a[8]);
+        cswap(a[0], a[3]); cswap(a[5], a[8]); cswap(a[4], a[7]);
+        cswap(a[3], a[6]); cswap(a[1], a[4]); cswap(a[2], a[5]);
+        cswap(a[4], a[7]); cswap(a[4], a[2]); cswap(a[6], a[4]);
+        cswap(a[4], a[2]);
+        out[k] = a[4];
+    }
+}
+
+__global__ void clip_kernel(double* __restrict__ a, size_t n, double bound) {
+    GRID_LOOP(k, n) a[k] = fmin(fmax(a[k], -bound), bound);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- host driver
+
+std::vector<std::pair<int, int>> brox_shapes(int h, int w, double scale, int min_size) {
+    std::vector<std::pair<int, int>> out{{h, w}};
+    while (std::min(out.back().first, out.back().second) > min_size) {  // flow.py:151-159
+        int nh = std::max((int)std::nearbyint(out.back().first * scale), min_size);
+        int nw = std::max((int)std::nearbyint(out.back().second * scale), min_size);
+        if (nh == out.back().first && nw == out.back().second) break;
+        out.push_back({nh, nw});
+    }
+    return out;
+}
+
+void BroxWorkspace::reserve(int h, int w, int levels_px) {
+    size_t n = (size_t)h * w;
+    if (n <= cap && (size_t)levels_px <= cap_pyr) return;
+    release();
+    size_t total = (size_t)kPlanes * n + 2 * (size_t)levels_px;
+    CUDA_CHECK(cudaMalloc(&base, total * sizeof(double)));
+    cap = n;
+    cap_pyr = levels_px;
+}
+
+void BroxWorkspace::release() {
+    if (base) cudaFree(base);
+    base = nullptr;
+    cap = cap_pyr = 0;
+}
+
+static void set_taps(double sigma, int& radius, cudaStream_t s, const double* host_taps, int ntaps) {
+    radius = (ntaps - 1) / 2;
+    CUDA_CHECK(cudaMemcpyToSymbolAsync(c_taps, host_taps, ntaps * sizeof(double), 0, cudaMemcpyHostToDevice, s));
+    (void)sigma;
+}
+
+void brox_flow(BroxWorkspace& ws, cudaStream_t s, const double* frame_t, const double* frame_prev, int h, int w,
+               const BroxParamsC& P, const double* taps_pre, int ntaps_pre, const double* taps_aa, int ntaps_aa,
+               double* u_out, double* v_out, int64_t* launches) {
+    auto shapes = brox_shapes(h, w, P.pyramid_scale, P.min_size);
+    const int L = (int)shapes.size();
+    int levels_px = 0;
+    std::vector<size_t> lofs(L);
+    for (int l = 0; l < L; ++l) {
+        lofs[l] = levels_px;
+        levels_px += shapes[l].first * shapes[l].second;
+    }
+    ws.reserve(h, w, levels_px);
+    const size_t N = (size_t)h * w;
+    double* pl = ws.base;
+    auto plane = [&](int i) { return pl + (size_t)i * N; };
+    double* refs = pl + (size_t)BroxWorkspace::kPlanes * N;
+    double* tgts = refs + levels_px;
+    double *tmp = plane(0), *tmp2 = plane(1);
+    double *u = plane(2), *v = plane(3), *u2 = plane(4), *v2 = plane(5);
+    double *du = plane(6), *dv = plane(7), *du2 = plane(8), *dv2 = plane(9), *wp = plane(10);
+    Lin Lz{plane(11), plane(12), plane(13), plane(14), plane(15), plane(16), plane(17), plane(18)};
+    Sys Sz{plane(19), plane(20), plane(21), plane(22), plane(23), plane(24), plane(25), plane(26), plane(27), plane(28)};
+    int r = 0;
+    auto gauss = [&](const double* src, double* dst, int hh, int ww) {
+        gauss_axis_kernel<<<nblk((size_t)hh * ww), kT, 0, s>>>(src, tmp2, hh, ww, r, 0);
+        gauss_axis_kernel<<<nblk((size_t)hh * ww), kT, 0, s>>>(tmp2, dst, hh, ww, r, 1);
+        *launches += 2;
+    };
+    // presmoothing (flow.py:197-199) into pyramid level 0
+    if (P.presmooth_sigma > 0) {
+        set_taps(P.presmooth_sigma, r, s, taps_pre, ntaps_pre);
+        gauss(frame_t, refs, h, w);
+        gauss(frame_prev, tgts, h, w);
+    } else {
+        CUDA_CHECK(cudaMemcpyAsync(refs, frame_t, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        CUDA_CHECK(cudaMemcpyAsync(tgts, frame_prev, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    }
+    // recursive pyramid (flow.py:201-208): smooth the previous level, then resample
+    set_taps(0.5 / P.pyramid_scale, r, s, taps_aa, ntaps_aa);
+    for (int l = 1; l < L; ++l) {
+        const int ph = shapes[l - 1].first, pw = shapes[l - 1].second, hh = shapes[l].first, ww = shapes[l].second;
+        for (double* pyr : {refs, tgts}) {
+            gauss(pyr + lofs[l - 1], tmp, ph, pw);
+            resize_kernel<<<nblk((size_t)hh * ww), kT, 0, s>>>(tmp, ph, pw, pyr + lofs[l], hh, ww, 1.0, 0);
+            ++*launches;
+        }
+    }
+    const double eps2 = P.eps * P.eps;
+    for (int l = L - 1; l >= 0; --l) {
+        const int hh = shapes[l].first, ww = shapes[l].second;
+        const size_t n = (size_t)hh * ww;
+        const int nb = nblk(n);
+        const double* ref = refs + lofs[l];
+        const double* tgt = tgts + lofs[l];
+        if (l == L - 1) {
+            CUDA_CHECK(cudaMemsetAsync(u, 0, n * sizeof(double), s));
+            CUDA_CHECK(cudaMemsetAsync(v, 0, n * sizeof(double), s));
+        } else {
+            const int ph = shapes[l + 1].first, pw = shapes[l + 1].second;
+            resize_kernel<<<nb, kT, 0, s>>>(u, ph, pw, u2, hh, ww, (double)ww / (double)pw, 1);
+            resize_kernel<<<nb, kT, 0, s>>>(v, ph, pw, v2, hh, ww, (double)hh / (double)ph, 1);
+            *launches += 2;
+            std::swap(u, u2);
+            std::swap(v, v2);
+        }
+        for (int wi = 0; wi < P.warps; ++wi) {
+            warp1_kernel<<<nb, kT, 0, s>>>(tgt, u, v, wp, hh, ww);
+            deriv1_kernel<<<nb, kT, 0, s>>>(wp, ref, Lz, hh, ww);
+            deriv2_kernel<<<nb, kT, 0, s>>>(Lz, hh, ww);
+            *launches += 3;
+            CUDA_CHECK(cudaMemsetAsync(du, 0, n * sizeof(double), s));
+            CUDA_CHECK(cudaMemsetAsync(dv, 0, n * sizeof(double), s));
+            for (int fp = 0; fp < P.fixed_point_iters; ++fp) {
+                robust_kernel<<<nb, kT, 0, s>>>(Lz, Sz, u, v, du, dv, hh, ww, P.gamma, eps2);
+                system_kernel<<<nb, kT, 0, s>>>(Lz, Sz, u, v, hh, ww, P.alpha);
+                *launches += 2;
+                for (int it = 0; it < P.solver_iters; ++it) {
+                    jacobi_kernel<<<nb, kT, 0, s>>>(Sz, du, dv, du2, dv2, hh, ww, P.alpha, it == P.solver_iters - 1);
+                    ++*launches;
+                    std::swap(du, du2);
+                    std::swap(dv, dv2);
+                }
+                if (P.solver_iters == 0) {  // clip still applies
+                    clip_kernel<<<nb, kT, 0, s>>>(du, n, 1.0);
+                    clip_kernel<<<nb, kT, 0, s>>>(dv, n, 1.0);
+                    *launches += 2;
+                }
+            }
+            median_update_kernel<<<nb, kT, 0, s>>>(u, du, u2, hh, ww);
+            median_update_kernel<<<nb, kT, 0, s>>>(v, dv, v2, hh, ww);
+            *launches += 2;
+            std::swap(u, u2);
+            std::swap(v, v2);
+        }
+    }
+    const double bound = (double)std::max(h, w);  // flow.py:277-278
+    clip_kernel<<<nblk(N), kT, 0, s>>>(u, N, bound);
+    clip_kernel<<<nblk(N), kT, 0, s>>>(v, N, bound);
+    *launches += 2;
+    CUDA_CHECK(cudaMemcpyAsync(u_out, u, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    CUDA_CHECK(cudaMemcpyAsync(v_out, v, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    CUDA_CHECK(cudaGetLastError());
+}
+
+}  // namespace hivc

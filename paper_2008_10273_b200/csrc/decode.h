@@ -8,6 +8,7 @@
 #include <mutex>
 #include <vector>
 
+#include "brox.h"
 #include "inpaint.h"
 #include "parse.h"
 #include "recon.h"
@@ -44,6 +45,7 @@ struct Context {
     int device = 0;
     cudaStream_t stream = nullptr;  // function-level API stream
     InpaintWorkspace ws;            // function-level solver scratch
+    BroxWorkspace brox;             // flow_brox scratch
     std::vector<std::unique_ptr<Lane>> lanes;
     std::atomic<int64_t> launches{0};
     std::atomic<int64_t> h2d_bytes{0}, d2h_bytes{0};

@@ -79,6 +79,44 @@ def bilinear_warp(plane, u, v):
     return warp_planes([plane], u, v)[0]
 
 
+def _gaussian_taps(sigma: float, truncate: float = 4.0) -> np.ndarray:
+    """scipy.ndimage's normalised 1-D Gaussian taps (gaussian_filter1d, order 0);
+    computed with numpy exactly as scipy does so the device filter is bit-identical."""
+    radius = int(truncate * float(sigma) + 0.5)
+    x = np.arange(-radius, radius + 1)
+    phi = np.exp(-0.5 / (sigma * sigma) * x ** 2)
+    return np.ascontiguousarray(phi / phi.sum(), dtype=np.float64)
+
+
+def flow_brox(frame_t, frame_prev, params: BroxParams | None = None) -> FlowField:
+    """Backward flow from frame_t to frame_prev, coarse-to-fine with warping (flow.py:187-278).
+
+    The whole estimator runs on the GPU in float64 (csrc/brox.cu).  numpy
+    inputs give a numpy FlowField; CUDA tensors keep u, v on the device.
+    """
+    if params is None:
+        params = BroxParams()
+    t = torch()
+    f1 = to_device(frame_t, t.float64)
+    f0 = to_device(frame_prev, t.float64, f1.device)
+    if tuple(f1.shape) != tuple(f0.shape) or f1.dim() != 2:
+        raise FlowError("frame shape mismatch")
+    if not (bool(t.isfinite(f1).all()) and bool(t.isfinite(f0).all())):
+        raise FlowError("non-finite input planes")
+    h, w = f1.shape
+    u = t.empty_like(f1)
+    v = t.empty_like(f1)
+    prm = N.BroxParamsC(params.alpha, params.gamma, params.pyramid_scale, params.min_size, params.warps,
+                        params.fixed_point_iters, params.solver_iters, params.eps, params.presmooth_sigma)
+    tp = _gaussian_taps(params.presmooth_sigma) if params.presmooth_sigma > 0 else np.ones(1)
+    ta = _gaussian_taps(0.5 / params.pyramid_scale)
+    ctx = N.context(f1.device.index)
+    t.cuda.current_stream(f1.device).synchronize()
+    N.check(N.lib.hivc_brox(ctx.handle, ptr(f1), ptr(f0), h, w, C.byref(prm), tp.ctypes.data_as(N.c_dbl_p), tp.size,
+                            ta.ctypes.data_as(N.c_dbl_p), ta.size, ptr(u), ptr(v)))
+    return FlowField(back(u, frame_t), back(v, frame_t))
+
+
 def _tree_leaves(data: bytes, pos: int, nbits: int, width: int, height: int, bit_offset: int = 0, with_used=False):
     """Preorder leaf rectangles (x, y, w, h) via the native parser (subdivision.py:183-222)."""
     nbytes = (nbits + 7) // 8

@@ -88,6 +88,16 @@ def main():
     g["warp_u"] = u
     g["warp_v"] = v
     g["warp_out"] = np.stack(rflow.warp_planes(planes, u, v))
+    # ---- Brox flow (flow.py:187-278), both pyramid factors of the configs
+    sys.path.insert(0, str(HERE.parent.parent))
+    from paper_2008_10273_b200.synth import synth_clip
+
+    clip = synth_clip(2, 48, 64, blobs=4, rects=2, v=3.0, seed=5)[:, 0].astype(np.float64)
+    g["brox_pair"] = clip
+    for tag, sc in (("05", 0.5), ("095", 0.95)):
+        ff = rflow.flow_brox(clip[1], clip[0], rflow.BroxParams(pyramid_scale=sc))
+        g[f"brox{tag}_u"] = ff.u
+        g[f"brox{tag}_v"] = ff.v
     np.savez_compressed(HERE / "golden.npz", **g)
 
     # ---- entropy + tree payloads (entropy.py, subdivision.py)

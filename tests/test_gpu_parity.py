@@ -186,3 +186,29 @@ def test_decode_config3_matches_reference_checksums(plane):
         assert dr.max() <= a.shape[1] and dc.max() <= a.shape[0]
         assert dr.sum() <= 64, f"frame {i}: {dr.sum()} grey levels of drift"
     assert exact >= out.shape[0] // 2
+
+
+# ---------------------------------------------------------------- Brox flow (encoder side)
+
+
+@pytest.mark.parametrize("tag,scale", [("05", 0.5), ("095", 0.95)])
+def test_flow_brox_matches_reference(golden, tag, scale):
+    from paper_2008_10273_b200.flow import BroxParams, flow_brox
+
+    pair = golden["brox_pair"]
+    ff = flow_brox(pair[1], pair[0], BroxParams(pyramid_scale=scale))
+    du = np.abs(ff.u - golden[f"brox{tag}_u"]).max()
+    dv = np.abs(ff.v - golden[f"brox{tag}_v"]).max()
+    # float64 replay of the reference: rounding-level agreement (north star: flow <= 1e-2 px)
+    assert max(du, dv) <= 1e-9, (du, dv)
+
+
+def test_flow_brox_vs_oracle_larger():
+    from oracle import brox
+    from paper_2008_10273_b200.flow import flow_brox
+    from paper_2008_10273_b200.synth import synth_clip
+
+    clip = synth_clip(2, 180, 320, blobs=8, rects=3, v=3.0, seed=0)[:, 0].astype(np.float64)
+    ru, rv = brox.brox(clip[1], clip[0])
+    ff = flow_brox(clip[1], clip[0])
+    assert max(np.abs(ff.u - ru).max(), np.abs(ff.v - rv).max()) <= 1e-6

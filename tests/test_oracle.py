@@ -95,3 +95,24 @@ def test_oracle_dense_known_answers():
     u = inpaint.solve(f, m)
     assert u.min() >= f[m].min() - 1e-6 and u.max() <= f[m].max() + 1e-6
     np.testing.assert_allclose(u, inpaint.solve_dense(f, m), atol=1e-4)
+
+
+def test_oracle_gaussian_restatement_is_scipy_bit_exact():
+    from scipy.ndimage import gaussian_filter
+
+    from oracle import brox
+
+    rng = np.random.default_rng(2)
+    for shape in ((16, 17), (48, 64), (90, 33)):
+        a = rng.uniform(0, 255, shape)
+        for s in (0.8, 1.0, 0.5 / 0.95, 2.5):
+            assert np.array_equal(brox.gaussian(a, s), gaussian_filter(a, s))
+
+
+@pytest.mark.parametrize("tag,scale", [("05", 0.5), ("095", 0.95)])
+def test_oracle_brox_matches_reference(golden, tag, scale):
+    from oracle import brox
+
+    pair = golden["brox_pair"]
+    u, v = brox.brox(pair[1], pair[0], brox.Params(pyramid_scale=scale))
+    assert np.array_equal(u, golden[f"brox{tag}_u"]) and np.array_equal(v, golden[f"brox{tag}_v"])
