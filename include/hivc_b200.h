@@ -140,6 +140,17 @@ int hivc_block_reconstruct(hivc_ctx* ctx, const double* mc, const double* a, con
 int hivc_block_fit(hivc_ctx* ctx, const double* f_blocks, const uint64_t* masks, int32_t n,
                    double* c_out, double* a_out);
 
+/* Fit + rebuild of every 8x8 tile of a float32 residual plane (config 2;
+ * solve_block_coefficients_batch + reconstruct_blocks, pseudodiff.py:243-279,
+ * edge tiles embedded top-left as in inpaint_plane_blockwise, 299-324).
+ * hivc_block_operator: ONE mask layout shared by all tiles (bit y*8+x of
+ * `mask`): the fit+rebuild is the fixed 64x64 operator R (float64 on the host),
+ * applied to all tiles as a 3xTF32 tcgen05 tensor-core contraction.
+ * hivc_block_perblock: per-tile masks (device uint64 array, raster tile order),
+ * float64 bordered solves in shared memory.  plane/out: device float32 (h*w). */
+int hivc_block_operator(hivc_ctx* ctx, const float* plane, int32_t h, int32_t w, uint64_t mask, float* out);
+int hivc_block_perblock(hivc_ctx* ctx, const float* plane, int32_t h, int32_t w, const uint64_t* masks, float* out);
+
 /* ------------------------------------------------------------------ Brox optic flow (encoder side)
  * Replaces flow.flow_brox (flow.py:187-278): backward flow frame_t -> frame_prev,
  * float64, same pyramid / warps / lagged nonlinearity / damped Jacobi / median

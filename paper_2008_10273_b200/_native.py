@@ -69,6 +69,8 @@ _proto("hivc_decode", C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_int32, C.
 _proto("hivc_decode_multi", C.c_int, C.c_void_p, C.c_int32, C.POINTER(C.c_void_p), c_size_p, c_int_p, c_int_p,
        C.POINTER(C.c_void_p), C.c_int32, c_dbl_p)
 _proto("hivc_ctx_bytes", C.c_int, C.c_void_p, c_i64_p, c_i64_p)
+_proto("hivc_block_operator", C.c_int, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_uint64, C.c_void_p)
+_proto("hivc_block_perblock", C.c_int, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p)
 
 
 class BroxParamsC(C.Structure):

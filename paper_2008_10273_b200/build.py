@@ -19,7 +19,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # -fmad=false: no FMA contraction, so float64 expressions round exactly like numpy's
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC,-O3", "-I", str(PKG.parent / "include")]
-SOURCES = ["parse.cpp", "inpaint.cu", "recon.cu", "brox.cu", "decode.cu", "abi.cu"]
+SOURCES = ["parse.cpp", "inpaint.cu", "recon.cu", "brox.cu", "blockgemm.cu", "decode.cu", "abi.cu"]
 
 
 def _compile(src: str) -> Path:

@@ -5,6 +5,7 @@
 #include <string>
 #include <vector>
 
+#include "blockgemm.h"
 #include "brox.h"
 #include "decode.h"
 #include "inpaint.h"
@@ -240,6 +241,54 @@ int hivc_block_fit(hivc_ctx* ctx, const double* f_blocks, const uint64_t* masks,
         CUDA_CHECK(cudaMemsetAsync(C.d_status, 0, sizeof(int), C.stream));
         hivc::launch_block_fit(f_blocks, masks, n, c_out, a_out, C.d_status, C.stream);
         C.launches += n > 0;
+        int st = 0;
+        CUDA_CHECK(cudaMemcpyAsync(&st, C.d_status, sizeof(int), cudaMemcpyDeviceToHost, C.stream));
+        CUDA_CHECK(cudaStreamSynchronize(C.stream));
+        if (st == 1) hivc::fail(HIVC_E_PSEUDODIFF, "block mask needs at least one point");
+        if (st == 2) hivc::fail(HIVC_E_PSEUDODIFF, "singular coefficient system");
+    });
+}
+
+int hivc_block_operator(hivc_ctx* ctx, const float* plane, int32_t h, int32_t w, uint64_t mask, float* out) {
+    return guarded([&] {
+        if (!ctx) hivc::fail(HIVC_E_ARGUMENT, "null context");
+        hivc::Context& C = ctx->c;
+        CUDA_CHECK(cudaSetDevice(C.device));
+        if (C.op_mask != mask || !C.op_hi) {
+            std::vector<double> R;
+            hivc::shared_block_operator(mask, R);
+            std::vector<float> hi(64 * 64), lo(64 * 64);
+            for (int i = 0; i < 64 * 64; ++i) {
+                float f = (float)R[i];
+                uint32_t u;
+                std::memcpy(&u, &f, 4);
+                u &= 0xFFFFE000u;  // tf32 head
+                float fh;
+                std::memcpy(&fh, &u, 4);
+                hi[i] = fh;
+                lo[i] = (float)(R[i] - (double)fh);
+            }
+            if (!C.op_hi) CUDA_CHECK(cudaMalloc(&C.op_hi, 2 * 64 * 64 * sizeof(float)));
+            CUDA_CHECK(cudaMemcpy(C.op_hi, hi.data(), hi.size() * 4, cudaMemcpyHostToDevice));
+            CUDA_CHECK(cudaMemcpy(C.op_hi + 64 * 64, lo.data(), lo.size() * 4, cudaMemcpyHostToDevice));
+            C.op_mask = mask;
+        }
+        int dev_sms = 0;
+        CUDA_CHECK(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, C.device));
+        hivc::launch_block_operator_tc(plane, out, h, w, C.op_hi, C.op_hi + 64 * 64, dev_sms, C.stream);
+        C.launches += 1;
+        CUDA_CHECK(cudaStreamSynchronize(C.stream));
+    });
+}
+
+int hivc_block_perblock(hivc_ctx* ctx, const float* plane, int32_t h, int32_t w, const uint64_t* masks, float* out) {
+    return guarded([&] {
+        if (!ctx) hivc::fail(HIVC_E_ARGUMENT, "null context");
+        hivc::Context& C = ctx->c;
+        CUDA_CHECK(cudaSetDevice(C.device));
+        CUDA_CHECK(cudaMemsetAsync(C.d_status, 0, sizeof(int), C.stream));
+        hivc::launch_block_perblock(plane, out, h, w, masks, C.d_status, C.stream);
+        C.launches += 1;
         int st = 0;
         CUDA_CHECK(cudaMemcpyAsync(&st, C.d_status, sizeof(int), cudaMemcpyDeviceToHost, C.stream));
         CUDA_CHECK(cudaStreamSynchronize(C.stream));

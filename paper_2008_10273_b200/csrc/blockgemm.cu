@@ -1,0 +1,339 @@
+// Config-2 block pseudodifferential microbench kernels (reference
+// pseudodiff.py:218-279, codec.py:140-153): fit the Green's-function
+// coefficients of every 8x8 residual block at its mask points and rebuild the
+// block, u = G M c + a.
+//
+// (a) one mask layout shared by all blocks: fit + rebuild is a fixed linear
+//     map of the block's 64 samples, rec = R f with the 64x64 operator
+//         R[:, pos] = G[:, pos] S^-1[:K, :K] + 1 S^-1[K, :K]
+//     (S the bordered (K+1)^2 system, computed once on the host in float64).
+//     Applied to all blocks as ONE dense contraction on the 5th-gen tensor
+//     cores: tcgen05.mma kind::tf32, M=128 blocks x N=64 x K=64, accumulator
+//     in TMEM, 3xTF32 split precision (A_hi B_hi + A_hi B_lo + A_lo B_hi) so
+//     the result carries ~fp32 accuracy (single-pass TF32 fails the 1e-3 bar,
+//     SURVEY §0).  Operands are staged in shared memory in the canonical
+//     K-major no-swizzle UMMA layout (8-row x 16-byte core matrices).
+// (b) per-block masks: every block solves its own bordered system in shared
+//     memory (float64) and rebuilds G[:, pos] c + a.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <vector>
+
+#include "aan_constants.h"
+#include "blockgemm.h"
+#include "inpaint.h"
+
+namespace hivc {
+
+namespace {
+
+constexpr int kTileM = 128;  // blocks per tile (UMMA M)
+constexpr int kN = 64;       // outputs per block (UMMA N)
+constexpr int kK = 64;       // samples per block (UMMA K total)
+constexpr int kThreadsG = 128;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+// canonical K-major SWIZZLE_NONE offset (bytes) of element (row, k) of an
+// operand with 64 K-elements per row: core matrix (row/8, k/4) is 128 B,
+// core matrices of one row group are consecutive along K (LBO = 128 B),
+// row groups are 16 core matrices apart (SBO = 2048 B)
+__device__ __forceinline__ uint32_t kmajor_off(int row, int k) {
+    return (uint32_t)(((row >> 3) * 16 + (k >> 2)) * 128 + (row & 7) * 16 + (k & 3) * 4);
+}
+
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((addr >> 4) & 0x3FFF);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;  // descriptor version (Blackwell)
+    // base offset 0, lbo mode 0, layout type 0 (SWIZZLE_NONE)
+    return d;
+}
+
+// instruction descriptor: D f32, A/B tf32, both K-major, N=64, M=128
+constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kN >> 3) << 17) | ((uint32_t)(kTileM >> 4) << 24);
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(kIdesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+
+}  // namespace
+
+// rec[b] = R f[b] for every 8x8 block b of the plane (f32 in/out), 3xTF32 on tcgen05.
+__global__ void __launch_bounds__(kThreadsG, 1)
+    block_operator_tc_kernel(const float* __restrict__ plane, float* __restrict__ out, int h, int w,
+                             const float* __restrict__ r_hi, const float* __restrict__ r_lo, int nblocks) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t* a_hi = smem;                        // 128 x 64 f32 = 32 KB
+    uint8_t* a_lo = smem + 32768;                // 32 KB
+    uint8_t* b_hi = smem + 65536;                // 64 x 64 f32 = 16 KB
+    uint8_t* b_lo = smem + 65536 + 16384;        // 16 KB
+    __shared__ __align__(8) uint64_t mbar;
+    __shared__ uint32_t tmem_base;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int nbx = (w + 7) >> 3;
+    const int ntiles = (nblocks + kTileM - 1) / kTileM;
+
+    // operator halves, K-major (row n of R = output pixel n, k = input pixel)
+    for (int e = tid; e < kN * kK; e += kThreadsG) {
+        int n = e / kK, k = e % kK;
+        *reinterpret_cast<float*>(b_hi + kmajor_off(n, k)) = r_hi[e];
+        *reinterpret_cast<float*>(b_lo + kmajor_off(n, k)) = r_lo[e];
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
+                     "r"(kN));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar)));
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = tmem_base;
+    uint32_t phase = 0;
+
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        // ---- stage the tile's blocks: A = f (block-major rows, 64 samples each), split hi/lo
+        for (int e = tid; e < kTileM * kK; e += kThreadsG) {
+            int m = e / kK, k = e % kK;
+            int b = tile * kTileM + m;
+            float v = 0.f;
+            if (b < nblocks) {
+                int by = b / nbx, bx = b % nbx;
+                int y = by * 8 + (k >> 3), x = bx * 8 + (k & 7);
+                if (y < h && x < w) v = __ldg(plane + (size_t)y * w + x);
+            }
+            float hi = tf32_hi(v);
+            *reinterpret_cast<float*>(a_hi + kmajor_off(m, k)) = hi;
+            *reinterpret_cast<float*>(a_lo + kmajor_off(m, k)) = v - hi;
+        }
+        asm volatile("fence.proxy.async.shared::cta;");  // generic-proxy smem writes -> tensor core
+        __syncthreads();
+        if (tid == 0) {
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const uint32_t ah = smem_u32(a_hi), al = smem_u32(a_lo), bh = smem_u32(b_hi), bl = smem_u32(b_lo);
+            uint32_t acc = 0;
+#pragma unroll
+            for (int kb = 0; kb < kK / 8; ++kb) {  // K = 8 tf32 per MMA = 2 core matrices
+                const uint32_t off = kb * 2 * 128;
+                mma_tf32(tmem, smem_desc(ah + off, 128, 2048), smem_desc(bh + off, 128, 2048), acc);
+                acc = 1;
+                mma_tf32(tmem, smem_desc(ah + off, 128, 2048), smem_desc(bl + off, 128, 2048), 1);
+                mma_tf32(tmem, smem_desc(al + off, 128, 2048), smem_desc(bh + off, 128, 2048), 1);
+            }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                smem_u32(&mbar)));
+        }
+        // ---- wait for the accumulator
+        {
+            uint32_t done = 0;
+            while (!done) {
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\t"
+                    "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                    "selp.u32 %0, 1, 0, p;\n\t}\n"
+                    : "=r"(done)
+                    : "r"(smem_u32(&mbar)), "r"(phase));
+            }
+            phase ^= 1;
+        }
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        // ---- epilogue: warp w reads TMEM lanes 32w..32w+31 (= blocks), 64 columns
+        const int m = warp * 32 + lane;
+        const int b = tile * kTileM + m;
+        const int by = b / nbx, bx = b % nbx;
+#pragma unroll
+        for (int c0 = 0; c0 < kN; c0 += 16) {
+            uint32_t v[16];
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
+                "[%16];"
+                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                  "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+                : "r"(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0));
+            asm volatile("tcgen05.wait::ld.sync.aligned;");
+            if (b < nblocks) {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    int n = c0 + j;
+                    int y = by * 8 + (n >> 3), x = bx * 8 + (n & 7);
+                    if (y < h && x < w) out[(size_t)y * w + x] = __uint_as_float(v[j]);
+                }
+            }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncthreads();  // TMEM and smem reused by the next tile
+        asm volatile("tcgen05.fence::after_thread_sync;");
+    }
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kN));
+}
+
+// (b) per-block masks: bordered solve in shared memory (float64), then
+// rec = G[:, pos] c + a (pseudodiff.py:218-240, 266-272), one warp per block.
+constexpr int kPbWarps = 4;
+constexpr int kPbLd = 66;
+
+__global__ void __launch_bounds__(kPbWarps * 32)
+    block_perblock_kernel(const float* __restrict__ plane, float* __restrict__ out, int h, int w,
+                          const uint64_t* __restrict__ masks, int nblocks, int* status) {
+    extern __shared__ double sm[];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int b = blockIdx.x * kPbWarps + wid;
+    if (b >= nblocks) return;
+    double* M = sm + (size_t)wid * 65 * kPbLd;
+    double* fb = sm + (size_t)kPbWarps * 65 * kPbLd + wid * 64;
+    int* pos = reinterpret_cast<int*>(sm + (size_t)kPbWarps * (65 * kPbLd + 64)) + wid * 64;
+    const int nbx = (w + 7) >> 3;
+    const int by = b / nbx, bx = b % nbx;
+    for (int k = lane; k < 64; k += 32) {
+        int y = by * 8 + (k >> 3), x = bx * 8 + (k & 7);
+        fb[k] = (y < h && x < w) ? (double)plane[(size_t)y * w + x] : 0.0;
+    }
+    const uint64_t mask = masks[b];
+    const int K = __popcll(mask);
+    if (K == 0) {
+        if (lane == 0) atomicExch(status, 1);
+        return;
+    }
+    for (int j = lane; j < 64; j += 32)
+        if ((mask >> j) & 1ull) pos[__popcll(mask & ((1ull << j) - 1ull))] = j;
+    __syncwarp();
+    const int N = K + 1;
+    for (int e = lane; e < N * N; e += 32) {
+        int i = e / N, j = e % N;
+        M[i * kPbLd + j] = (i < K && j < K) ? kGreens64[pos[i] * 64 + pos[j]] : ((i == K && j == K) ? 0.0 : 1.0);
+    }
+    for (int i = lane; i < N; i += 32) M[i * kPbLd + N] = i < K ? fb[pos[i]] : 0.0;
+    __syncwarp();
+    for (int col = 0; col < N; ++col) {
+        int piv = col;
+        double best = -1.0;
+        for (int i = col; i < N; ++i) {
+            double v = fabs(M[i * kPbLd + col]);
+            if (v > best) {
+                best = v;
+                piv = i;
+            }
+        }
+        if (best == 0.0) {
+            if (lane == 0) atomicExch(status, 2);
+            return;
+        }
+        if (piv != col)
+            for (int j = lane; j <= N; j += 32) {
+                double t = M[col * kPbLd + j];
+                M[col * kPbLd + j] = M[piv * kPbLd + j];
+                M[piv * kPbLd + j] = t;
+            }
+        __syncwarp();
+        const double d = M[col * kPbLd + col];
+        for (int i = col + 1; i < N; ++i) {
+            const double l = M[i * kPbLd + col] / d;
+            for (int j = col + 1 + lane; j <= N; j += 32) M[i * kPbLd + j] = M[i * kPbLd + j] - l * M[col * kPbLd + j];
+            __syncwarp();
+        }
+    }
+    if (lane == 0)
+        for (int i = N - 1; i >= 0; --i) {
+            double s = M[i * kPbLd + N];
+            for (int j = i + 1; j < N; ++j) s = s - M[i * kPbLd + j] * M[j * kPbLd + N];
+            M[i * kPbLd + N] = s / M[i * kPbLd + i];
+        }
+    __syncwarp();
+    const double a = M[K * kPbLd + N];
+    for (int n = lane; n < 64; n += 32) {
+        double acc = 0.0;
+        for (int i = 0; i < K; ++i) acc = acc + kGreens64[n * 64 + pos[i]] * M[i * kPbLd + N];
+        int y = by * 8 + (n >> 3), x = bx * 8 + (n & 7);
+        if (y < h && x < w) out[(size_t)y * w + x] = (float)(acc + a);
+    }
+}
+
+// ---------------------------------------------------------------- host
+
+// R = G[:, pos] S^-1[:K,:K] + 1 S^-1[K,:K] scattered to the mask columns (float64, Gauss-Jordan)
+void shared_block_operator(uint64_t mask, std::vector<double>& R) {
+    std::vector<int> pos;
+    for (int j = 0; j < 64; ++j)
+        if ((mask >> j) & 1ull) pos.push_back(j);
+    const int K = (int)pos.size();
+    if (K == 0) fail(HIVC_E_PSEUDODIFF, "block mask needs at least one point");
+    const int N = K + 1;
+    std::vector<double> S((size_t)N * 2 * N, 0.0);  // [S | I]
+    for (int i = 0; i < N; ++i) {
+        for (int j = 0; j < N; ++j)
+            S[(size_t)i * 2 * N + j] =
+                (i < K && j < K) ? kGreens64Host[pos[i] * 64 + pos[j]] : ((i == K && j == K) ? 0.0 : 1.0);
+        S[(size_t)i * 2 * N + N + i] = 1.0;
+    }
+    for (int c = 0; c < N; ++c) {
+        int piv = c;
+        for (int i = c + 1; i < N; ++i)
+            if (std::fabs(S[(size_t)i * 2 * N + c]) > std::fabs(S[(size_t)piv * 2 * N + c])) piv = i;
+        if (S[(size_t)piv * 2 * N + c] == 0.0) fail(HIVC_E_PSEUDODIFF, "singular coefficient system");
+        if (piv != c)
+            for (int j = 0; j < 2 * N; ++j) std::swap(S[(size_t)c * 2 * N + j], S[(size_t)piv * 2 * N + j]);
+        double d = S[(size_t)c * 2 * N + c];
+        for (int j = 0; j < 2 * N; ++j) S[(size_t)c * 2 * N + j] /= d;
+        for (int i = 0; i < N; ++i) {
+            if (i == c) continue;
+            double l = S[(size_t)i * 2 * N + c];
+            if (l != 0.0)
+                for (int j = 0; j < 2 * N; ++j) S[(size_t)i * 2 * N + j] -= l * S[(size_t)c * 2 * N + j];
+        }
+    }
+    auto inv = [&](int i, int j) { return S[(size_t)i * 2 * N + N + j]; };
+    R.assign(64 * 64, 0.0);
+    for (int n = 0; n < 64; ++n)
+        for (int j = 0; j < K; ++j) {
+            double acc = inv(K, j);  // constant term a = S^-1[K, :K] f_K
+            for (int i = 0; i < K; ++i) acc += kGreens64Host[n * 64 + pos[i]] * inv(i, j);
+            R[(size_t)n * 64 + pos[j]] = acc;
+        }
+}
+
+void launch_block_operator_tc(const float* plane, float* out, int h, int w, const float* r_hi, const float* r_lo,
+                              int num_sms, cudaStream_t s) {
+    const int nblocks = ((h + 7) / 8) * ((w + 7) / 8);
+    const int ntiles = (nblocks + kTileM - 1) / kTileM;
+    const size_t smem = 65536 + 32768;
+    static bool attr = false;
+    if (!attr) {
+        CUDA_CHECK(cudaFuncSetAttribute(block_operator_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    block_operator_tc_kernel<<<std::min(ntiles, num_sms), kThreadsG, smem, s>>>(plane, out, h, w, r_hi, r_lo, nblocks);
+    CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_block_perblock(const float* plane, float* out, int h, int w, const uint64_t* masks, int* status,
+                           cudaStream_t s) {
+    const int nblocks = ((h + 7) / 8) * ((w + 7) / 8);
+    const size_t smem = (size_t)kPbWarps * (65 * kPbLd + 64) * sizeof(double) + kPbWarps * 64 * sizeof(int);
+    static bool attr = false;
+    if (!attr) {
+        CUDA_CHECK(cudaFuncSetAttribute(block_perblock_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    block_perblock_kernel<<<(nblocks + kPbWarps - 1) / kPbWarps, kPbWarps * 32, smem, s>>>(plane, out, h, w, masks,
+                                                                                              nblocks, status);
+    CUDA_CHECK(cudaGetLastError());
+}
+
+}  // namespace hivc

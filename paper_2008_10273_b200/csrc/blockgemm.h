@@ -1,0 +1,22 @@
+// Config-2 block fit + reconstruct kernels (blockgemm.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+namespace hivc {
+
+// 64x64 fit-and-rebuild operator of one shared mask layout (float64).
+void shared_block_operator(uint64_t mask, std::vector<double>& R);
+
+// (a) rec = R f for every 8x8 block of a float32 plane, 3xTF32 tcgen05 GEMM.
+void launch_block_operator_tc(const float* plane, float* out, int h, int w, const float* r_hi, const float* r_lo,
+                              int num_sms, cudaStream_t s);
+
+// (b) per-block masks (device uint64 per block), float64 shared-memory solves.
+void launch_block_perblock(const float* plane, float* out, int h, int w, const uint64_t* masks, int* status,
+                           cudaStream_t s);
+
+}  // namespace hivc

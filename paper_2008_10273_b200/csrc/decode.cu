@@ -205,6 +205,7 @@ Lane::~Lane() {
 Context::~Context() {
     lanes.clear();
     if (d_status) cudaFree(d_status);
+    if (op_hi) cudaFree(op_hi);
     if (stream) cudaStreamDestroy(stream);
 }
 

@@ -55,6 +55,8 @@ struct Context {
     int64_t inter_frames = 0, intra_frames = 0;
     double inter_seconds = 0;  // device time of the fused P-frame kernels
     int* d_status = nullptr;
+    float* op_hi = nullptr;  // shared-layout block operator (tf32 head, then tail), config 2a
+    uint64_t op_mask = 0;
     ~Context();
 };
 

@@ -97,8 +97,59 @@ def solve_blocks_any_k(f_blocks, mask_words):
     return c, a
 
 
+# The reference's flat-block 4-point layout: mask_from_tree(subdivide_by_error(zeros((8, 8)), 4)),
+# points (y, x) = (2,1), (2,3), (4,6), (6,2) (subdivision.py:76-130, 173-178); bit y*8+x.
+FLAT_BLOCK_MASK = (1 << 17) | (1 << 19) | (1 << 38) | (1 << 50)
+
+
+def reconstruct_plane_shared_mask(plane, mask=FLAT_BLOCK_MASK):
+    """Fit + rebuild every 8x8 tile of a float32 plane with ONE shared mask layout.
+
+    Equivalent to ``inpaint_plane_blockwise`` (pseudodiff.py:299-324) with the
+    same mask in every tile: the fit and the rebuild collapse into a fixed
+    64x64 operator, applied to all tiles as a 3xTF32 tcgen05 tensor-core
+    contraction (csrc/blockgemm.cu).  ``mask``: 8x8 bool array or int bitmask.
+    Returns the reconstructed plane (float32; numpy in -> numpy out).
+    """
+    t = torch()
+    if not isinstance(mask, int):
+        mask = int(_mask_words(np.asarray(mask, dtype=bool).reshape(1, 64))[0])
+    pt = to_device(plane, t.float32)
+    h, w = pt.shape
+    pts = [(b // 8, b % 8) for b in range(64) if (mask >> b) & 1]
+    if not pts:
+        raise PseudodiffError("block mask needs at least one point")
+    if (h % 8 and max(y for y, _ in pts) >= h % 8) or (w % 8 and max(x for _, x in pts) >= w % 8):
+        raise PseudodiffError("mask point outside true pixels of edge block")  # pseudodiff.py:317-318
+    out = t.empty_like(pt)
+    ctx = N.context(pt.device.index)
+    t.cuda.current_stream(pt.device).synchronize()
+    N.check(N.lib.hivc_block_operator(ctx.handle, ptr(pt), h, w, mask, ptr(out)))
+    return back(out, plane)
+
+
+def reconstruct_plane_masks(plane, masks):
+    """Per-tile mask layouts (raster tile order, (ntiles, 8, 8) bool or uint64 words):
+    each tile solves its own bordered system (float64, shared memory) and is rebuilt."""
+    t = torch()
+    pt = to_device(plane, t.float32)
+    h, w = pt.shape
+    words = masks if (isinstance(masks, np.ndarray) and masks.dtype == np.uint64) else _mask_words(masks)
+    mw = to_device(np.asarray(words, dtype=np.uint64).view(np.int64), t.int64, pt.device)
+    if mw.numel() != ((h + 7) // 8) * ((w + 7) // 8):
+        raise PseudodiffError("one mask per 8x8 tile expected")
+    out = t.empty_like(pt)
+    ctx = N.context(pt.device.index)
+    t.cuda.current_stream(pt.device).synchronize()
+    N.check(N.lib.hivc_block_perblock(ctx.handle, ptr(pt), h, w, ptr(mw), ptr(out)))
+    return back(out, plane)
+
+
 # Reference-compatible aliases for the decode-side helpers
 __all__ = [
+    "FLAT_BLOCK_MASK",
+    "reconstruct_plane_shared_mask",
+    "reconstruct_plane_masks",
     "BLOCK",
     "block_grid",
     "greens_eigenvalues_harmonic",

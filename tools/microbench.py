@@ -1,0 +1,131 @@
+"""Function-level microbenchmarks of BASELINE.json configs 1, 2 and the Brox part of 4.
+
+    python tools/microbench.py [--reps R] [--cpu]
+
+One JSON line per measurement.  GPU times: wall clock around calls that
+synchronise their own CUDA stream (the C ABI returns after the device work),
+median of R repetitions after one warm-up.  --cpu also times the oracle port
+(the reference algorithm in numpy) on a bounded sample.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import statistics
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+REPO = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(REPO))
+
+
+def timed(fn, reps):
+    fn()
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        fn()
+        ts.append(time.perf_counter() - t0)
+    return statistics.median(ts)
+
+
+def config1(reps, cpu):
+    import torch
+
+    from paper_2008_10273_b200.homogeneous import solve_homogeneous
+    from paper_2008_10273_b200.synth import random_mask, synth_clip
+
+    clip = synth_clip(1, 1080, 1920, blobs=40, rects=12, v=6.0, seed=1, channels=3)[0].astype(np.float64)
+    m = random_mask((1080, 1920), 0.02, 1001)
+    mt = torch.from_numpy(m).cuda()
+    fs = [torch.from_numpy(np.where(m, clip[c], 0.0)).cuda() for c in range(3)]
+    stats = []
+
+    def run():
+        stats.clear()
+        for f in fs:
+            st = {}
+            solve_homogeneous(f, mt, tol=1e-6, max_iter=10000, strict=True, stats=st)
+            stats.append(st["level_iterations"])
+
+    dt = timed(run, reps)
+    alg = sum(n * (49 * it + 49) for s in stats for n, it in s)
+    line = {"config": 1, "what": "homogeneous inpainting 1080p x3 channels, 2% random mask, tol 1e-6, strict",
+            "seconds": dt, "seconds_per_channel": dt / 3, "level_iterations": stats[0],
+            "total_iterations": [sum(it for _, it in s) for s in stats],
+            "algorithmic_GBps": alg / dt / 1e9, "dtype": "f64"}
+    if cpu:
+        from oracle import inpaint
+
+        t0 = time.perf_counter()
+        inpaint.solve(np.where(m, clip[0], 0.0), m, tol=1e-6, max_iter=10000, strict=True)
+        line["cpu_oracle_seconds_per_channel"] = time.perf_counter() - t0
+    print(json.dumps(line), flush=True)
+
+
+def config2(reps, cpu):
+    import torch
+    from scipy.ndimage import uniform_filter
+
+    from paper_2008_10273_b200.pseudodiff import FLAT_BLOCK_MASK, reconstruct_plane_masks, reconstruct_plane_shared_mask
+
+    rng = np.random.default_rng(2)
+    res = uniform_filter(rng.laplace(0.0, 8.0, (1080, 1920)), size=3, mode="reflect").astype(np.float32)
+    nblk = 135 * 240
+    rt = torch.from_numpy(res).cuda()
+    dt = timed(lambda: reconstruct_plane_shared_mask(rt), reps)
+    print(json.dumps({"config": "2a", "what": "shared 4-point mask, fit+rebuild as one 64x64 operator, 3xTF32 tcgen05",
+                      "blocks": nblk, "seconds": dt, "blocks_per_s": nblk / dt,
+                      "GBps": nblk * 512 / dt / 1e9, "flops_per_block": 3 * 2 * 64 * 64}), flush=True)
+    mrng = np.random.default_rng(1002)
+    masks = mrng.uniform(size=(nblk, 8, 8)) < 0.05
+    empty = ~masks.reshape(nblk, 64).any(1)
+    for i in np.flatnonzero(empty):
+        masks[i, mrng.integers(0, 8), mrng.integers(0, 8)] = True
+    from paper_2008_10273_b200.pseudodiff import _mask_words
+
+    words = torch.from_numpy(_mask_words(masks).view(np.int64)).cuda()
+    dt = timed(lambda: reconstruct_plane_masks(rt, words.cpu().numpy().view(np.uint64)), reps)
+    ks = masks.reshape(nblk, 64).sum(1)
+    print(json.dumps({"config": "2b", "what": "per-block Bernoulli(0.05) masks, float64 smem bordered solves",
+                      "blocks": nblk, "seconds": dt, "blocks_per_s": nblk / dt,
+                      "GBps": float(np.sum(520 + 4 * (ks + 1))) / dt / 1e9,
+                      "k_hist": np.bincount(ks).tolist()}), flush=True)
+
+
+def config4_brox(reps, cpu):
+    import torch
+
+    from paper_2008_10273_b200.flow import BroxParams, flow_brox
+    from paper_2008_10273_b200.synth import synth_clip
+
+    clip = synth_clip(2, 1080, 1920, blobs=40, rects=12, v=6.0, seed=4)[:, 0].astype(np.float64)
+    a, b = torch.from_numpy(clip[1]).cuda(), torch.from_numpy(clip[0]).cuda()
+    for sc in (0.95, 0.5):
+        dt = timed(lambda: flow_brox(a, b, BroxParams(pyramid_scale=sc)), reps)
+        print(json.dumps({"config": 4, "what": f"Brox flow 1080p pair, pyramid_scale {sc}", "seconds_per_pair": dt,
+                          "pairs_per_s": 1 / dt, "dtype": "f64",
+                          "cpu_reference_seconds_per_pair_survey": 948.2 if sc == 0.95 else 126.4}), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--cpu", action="store_true")
+    ap.add_argument("--only", default="1,2,4")
+    a = ap.parse_args()
+    only = a.only.split(",")
+    if "1" in only:
+        config1(a.reps, a.cpu)
+    if "2" in only:
+        config2(a.reps, a.cpu)
+    if "4" in only:
+        config4_brox(max(1, a.reps // 2), a.cpu)
+
+
+if __name__ == "__main__":
+    main()
