@@ -84,6 +84,13 @@ int hivc_parse_header(const uint8_t* data, size_t len, hivc_stream_info* info);
 /* Frames per GOP record (the u16 at the head of each GOP payload, codec.py:494). */
 int hivc_gop_frame_counts(const uint8_t* data, size_t len, int32_t* counts, int32_t cap, int32_t* ngops);
 
+/* Host-only parse of every frame record of a stream (the parse half of
+ * codec.decode, codec.py:491-561, no GPU needed): 8 int64 per frame — type,
+ * intra mask points, flow leaves (u, v), residual marker, coded blocks and
+ * mask points of group 0, coded blocks of group 1.  *seconds: parse time. */
+int hivc_parse_stream(const uint8_t* data, size_t len, int64_t* stats, int64_t cap, int64_t* nframes,
+                      double* seconds);
+
 /* ------------------------------------------------------------------ entropy (host, bit-exact)
  * Replaces entropy.decode_symbols (entropy.py:276-291).  Writes at most `cap`
  * symbols; *count receives the stream's symbol count (call with cap=0 to size).

@@ -54,6 +54,7 @@ _proto("hivc_ctx_synchronize", C.c_int, C.c_void_p)
 _proto("hivc_ctx_launch_count", C.c_int64, C.c_void_p)
 _proto("hivc_parse_header", C.c_int, C.c_void_p, C.c_size_t, C.POINTER(StreamInfo))
 _proto("hivc_gop_frame_counts", C.c_int, C.c_void_p, C.c_size_t, c_int_p, C.c_int32, c_int_p)
+_proto("hivc_parse_stream", C.c_int, C.c_void_p, C.c_size_t, c_i64_p, C.c_int64, c_i64_p, c_dbl_p)
 _proto("hivc_parse_symbols", C.c_int, C.c_void_p, C.c_size_t, C.c_size_t, c_i64_p, C.c_size_t, c_size_p, c_size_p)
 _proto("hivc_parse_signed_values", C.c_int, C.c_void_p, C.c_size_t, C.c_size_t, c_i64_p, C.c_size_t, c_size_p, c_size_p)
 _proto("hivc_parse_tree", C.c_int, C.c_void_p, C.c_size_t, C.c_uint64, C.c_uint64, C.c_int32, C.c_int32, c_int_p,

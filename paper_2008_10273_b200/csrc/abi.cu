@@ -1,6 +1,7 @@
 // extern "C" entry points declared in include/hivc_b200.h.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -96,6 +97,16 @@ int hivc_gop_frame_counts(const uint8_t* data, size_t len, int32_t* counts, int3
     });
 }
 
+int hivc_parse_stream(const uint8_t* data, size_t len, int64_t* stats, int64_t cap, int64_t* nframes,
+                      double* seconds) {
+    return guarded([&] {
+        std::vector<int64_t> s;
+        hivc::parse_stream_stats(data, len, s, seconds);
+        *nframes = (int64_t)(s.size() / 8);
+        for (int64_t i = 0; i < cap && i < (int64_t)s.size(); ++i) stats[i] = s[i];
+    });
+}
+
 static int parse_sym_common(bool signed_vals, const uint8_t* data, size_t len, size_t pos, int64_t* out, size_t cap,
                             size_t* count, size_t* next_pos) {
     return guarded([&] {
@@ -121,7 +132,7 @@ int hivc_parse_tree(const uint8_t* data, size_t nbytes, uint64_t nbits, uint64_t
                     int32_t height, int32_t* rects, size_t cap, size_t* nleaves, uint64_t* bits_used) {
     return guarded([&] {
         hivc::BitReader rd(data, nbytes, nbits);
-        rd.pos = bit_offset;
+        rd.seek(bit_offset);
         std::vector<hivc::Rect> leaves;
         hivc::parse_tree_leaves(rd, width, height, leaves);
         *nleaves = leaves.size();
@@ -168,10 +179,29 @@ int hivc_homog_solve(hivc_ctx* ctx, const double* f, const uint8_t* mask, int32_
         std::vector<int> it(L);
         CUDA_CHECK(cudaMemcpyAsync(it.data(), C.ws.iters, L * sizeof(int), cudaMemcpyDeviceToHost, C.stream));
         CUDA_CHECK(cudaStreamSynchronize(C.stream));
-        if (getenv("HIVC_CG_TRACE") && C.ws.trace) {
+        if ((getenv("HIVC_CG_TRACE") || getenv("HIVC_CG_TRACE_CLUSTER")) && C.ws.trace) {
             // phase timing of the finest level (CTA 0, thread 0): mean ns per phase
-            std::vector<unsigned long long> tr(256 * 8);
+            std::vector<unsigned long long> tr(hivc::kTraceLen);
             CUDA_CHECK(cudaMemcpy(tr.data(), C.ws.trace, tr.size() * 8, cudaMemcpyDeviceToHost));
+            {  // arrival spread at the first reduction: max - min arrival, release - last arrival
+                double spread = 0, rel = 0;
+                int nk = 0;
+                for (int k = 2; k < 255 && tr[(k + 1) * 8] != 0; ++k) {
+                    unsigned long long lo = ~0ull, hi = 0;
+                    for (int b = 0; b < 160; ++b) {
+                        unsigned long long t = tr[2048 + k * 160 + b];
+                        if (!t) continue;
+                        lo = std::min(lo, t);
+                        hi = std::max(hi, t);
+                    }
+                    if (!hi) continue;
+                    spread += (double)(hi - lo);
+                    rel += (double)tr[k * 8 + 3] - (double)hi;
+                    ++nk;
+                }
+                if (nk) fprintf(stderr, "[cg trace] arrival spread %.0f ns | last arrival -> CTA0 released+summed %.0f ns\n",
+                                spread / nk, rel / nk);
+            }
             double acc[6] = {0, 0, 0, 0, 0, 0};
             int n = 0;
             for (int k = 2; k < 255 && tr[(k + 1) * 8] != 0; ++k, ++n) {

@@ -29,11 +29,20 @@ constexpr int kSetupCtas = 296;
 
 // Setup for the band kernel: x = x0*interior, r = b - A x (global), and the
 // per-CTA partials of r.r, b.b, |f_mask|^2, #interior (homogeneous.py:64-77).
+// setup pass 1: x = x0 * interior, x0 prolonged from the coarser level (homogeneous.py:71)
+__global__ void __launch_bounds__(512) cg_setup_x_kernel(CgParams P) {
+    const int w = P.w, n = P.n;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        P.x[i] = prolong_at(P, i / w, i % w) * (P.m[i] ? 0.0 : 1.0);
+}
+
+// setup pass 2: b = L(u_D) * interior, r = b - A x and the level partials
 __global__ void __launch_bounds__(512) cg_setup_kernel(CgParams P, double* partials) {
     __shared__ double sh[4 * 32];
     const int h = P.h, w = P.w, n = P.n;
     const double* __restrict__ f = P.f;
     const uint8_t* __restrict__ m = P.m;
+    const double* __restrict__ xg = P.x;
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         int y = i / w, xx = i % w;
@@ -43,16 +52,12 @@ __global__ void __launch_bounds__(512) cg_setup_kernel(CgParams P, double* parti
             size_t k = (size_t)yy * w + xq;
             return m[k] ? __ldg(f + k) : 0.0;
         };
-        auto xv = [&](int yy, int xq) -> double {
-            size_t k = (size_t)yy * w + xq;
-            return prolong_at(P, yy, xq) * (m[k] ? 0.0 : 1.0);
-        };
+        auto xv = [&](int yy, int xq) -> double { return xg[(size_t)yy * w + xq]; };
         double udi = mi ? __ldg(f + i) : 0.0;
-        double xi = prolong_at(P, y, xx) * interior;
+        double xi = xg[i];
         double b = lap_at(y, xx, h, w, udi, ud) * interior;
         double ax = -lap_at(y, xx, h, w, xi, xv) * interior;
         double ri = b - ax;
-        P.x[i] = xi;
         P.r[i] = ri;
         acc[0] += ri * ri;
         acc[1] += b * b;
@@ -66,8 +71,8 @@ __global__ void __launch_bounds__(512) cg_setup_kernel(CgParams P, double* parti
 
 __global__ void __launch_bounds__(kBandThreads, 1) cg_band_kernel(CgParams P, const double* __restrict__ setup) {
     extern __shared__ double sp[];  // (kBandRows + 2) x (w + 2)
-    __shared__ double sh[4 * 32];
-    unsigned int epoch = 0;
+    __shared__ double sh[2 * 4 * 32 + 8];
+    RedState red;
     const int h = P.h, w = P.w, W2 = w + 2;
     const int band = blockIdx.x, nb = gridDim.x;
     const int y0 = band * P.band_rows;
@@ -173,7 +178,7 @@ __global__ void __launch_bounds__(kBandThreads, 1) cg_band_kernel(CgParams P, co
                 P.ex_p[cur_par + ((size_t)band * 2 + 1) * w + c] = sp[rows * W2 + c + 1];
             }
             HIVC_TRACE(2);
-            reduce<true, 1>(d, sh, P, epoch);
+            grid_reduce<1>(d, sh, P, red);
             HIVC_TRACE(3);
             const double pap = d[0];
             if (pap <= 0.0 || rs < 1e-300) break;
@@ -197,7 +202,7 @@ __global__ void __launch_bounds__(kBandThreads, 1) cg_band_kernel(CgParams P, co
                 }
             }
             HIVC_TRACE(4);
-            reduce<true, 1>(e1, sh, P, epoch);
+            grid_reduce<1>(e1, sh, P, red);
             HIVC_TRACE(5);
             const double rs1 = e1[0];
             const double lhs = sqrt(rs1), rhs = P.tol * bn;

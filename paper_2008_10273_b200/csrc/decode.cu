@@ -101,7 +101,7 @@ struct Packer {
 
 struct FrameOffsets {
     size_t pts[2], vals[3];
-    size_t nodes[2], fvals[2];
+    size_t nodes[2], fvals[2], ftiles[2];
     size_t g[2][6];
 };
 
@@ -114,6 +114,7 @@ void pack_frame(Packer& pk, const FrameJob& J, FrameOffsets& o) {
         for (int c = 0; c < 2; ++c) {
             o.nodes[c] = pk.put(J.flow.nodes[c]);
             o.fvals[c] = pk.put(J.flow.vals[c]);
+            o.ftiles[c] = pk.put(J.flow.tiles[c]);
         }
     }
     for (int gi = 0; gi < J.res.ngroups; ++gi) {
@@ -207,6 +208,36 @@ Context::~Context() {
     if (d_status) cudaFree(d_status);
     if (op_hi) cudaFree(op_hi);
     if (stream) cudaStreamDestroy(stream);
+}
+
+// Host-only parse of a whole stream (no GPU): per frame 8 int64 —
+// type, intra mask points (Y), flow leaves u, flow leaves v, residual marker,
+// coded blocks (group 0), mask points (group 0), coded blocks (group 1).
+void parse_stream_stats(const uint8_t* data, size_t len, std::vector<int64_t>& stats, double* seconds) {
+    const double t0 = now_s();
+    StreamHeader hd = parse_header(data, len);
+    std::vector<std::pair<size_t, size_t>> gops;
+    split_gops(data, len, hd, gops);
+    std::vector<FrameJob> jobs;
+    std::vector<uint64_t> bits;
+    HostTimes ht;
+    stats.clear();
+    for (size_t g = 0; g < gops.size(); ++g) {
+        parse_gop(data + gops[g].first, gops[g].second, hd, (int)g, jobs, ht, bits);
+        for (const FrameJob& J : jobs) {
+            int64_t leaves[2] = {0, 0};
+            for (int c = 0; c < 2 && J.type == 1; ++c) leaves[c] = (int64_t)J.flow.vals[c].size();
+            stats.push_back(J.type);
+            stats.push_back(J.type == 0 ? (int64_t)J.intra.pts[0].size() : 0);
+            stats.push_back(leaves[0]);
+            stats.push_back(leaves[1]);
+            stats.push_back(J.res.zero ? 0 : 1);
+            stats.push_back(J.res.ngroups > 0 ? J.res.g[0].nblocks : 0);
+            stats.push_back(J.res.ngroups > 0 ? J.res.g[0].npoints : 0);
+            stats.push_back(J.res.ngroups > 1 ? J.res.g[1].nblocks : 0);
+        }
+    }
+    if (seconds) *seconds = now_s() - t0;
 }
 
 void gop_frame_counts(const uint8_t* data, size_t len, std::vector<int32_t>& counts) {
@@ -368,6 +399,7 @@ void decode_gop(Context& ctx, Lane& L, const StreamJob& S, int gi, bool out_on_d
             for (int c = 0; c < 2; ++c) {
                 A.flow.nodes[c] = at<int32_t>(dev, o.nodes[c]);
                 A.flow.vals[c] = at<double>(dev, o.fvals[c]);
+                A.flow.tiles[c] = at<uint16_t>(dev, o.ftiles[c]);
             }
             launch_frame(A, true, s);
             ctx.launches += 1;

@@ -66,6 +66,9 @@ struct Context {
 void decode_streams(Context& ctx, int nstreams, const uint8_t* const* data, const size_t* len, const int* gop_begin,
                     const int* gop_end, uint8_t* const* out, bool out_on_device, double* stage_seconds);
 
+// Host-only parse of every frame record (8 int64 per frame, see decode.cu).
+void parse_stream_stats(const uint8_t* data, size_t len, std::vector<int64_t>& stats, double* seconds);
+
 // Frames per GOP (u16 at the head of each GOP payload, codec.py:494).
 void gop_frame_counts(const uint8_t* data, size_t len, std::vector<int32_t>& counts);
 

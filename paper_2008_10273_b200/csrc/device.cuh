@@ -53,6 +53,30 @@ __device__ __forceinline__ void block_sum(double (&v)[NV], double* sh /* [NV][32
     __syncthreads();
 }
 
+// Same fixed-order block sum with ONE __syncthreads: warp partials go to one
+// of two shared buffers (alternating per call, `par`), and every thread sums
+// the warp partials itself in warp order.  Reusing a buffer two calls later is
+// safe because every thread passed the intermediate call's barrier after its
+// reads.  `sh` needs 2 * NV * 32 doubles.
+template <int NV>
+__device__ __forceinline__ void block_sum1(double (&v)[NV], double* sh, int& par) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    double* buf = sh + par * NV * 32;
+    par ^= 1;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) v[k] = warp_sum(v[k]);
+    if (lane == 0)
+#pragma unroll
+        for (int k = 0; k < NV; ++k) buf[k * 32 + wid] = v[k];
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+        double s = 0.0;
+        for (int i = 0; i < nw; ++i) s += buf[k * 32 + i];
+        v[k] = s;
+    }
+}
+
 // Software grid barrier for cooperative launches (all CTAs co-resident).
 // bar[0] is a monotonically increasing arrival counter (zeroed before the
 // launch); barrier number e completes when it reaches e * nblocks.  One
@@ -63,6 +87,21 @@ __device__ __forceinline__ unsigned int ld_acquire_gpu(const unsigned int* p) {
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+// Barrier tail for callers that already synchronised the CTA after their last
+// global writes (e.g. through block_sum1): thread 0 arrives and waits, then
+// the CTA is released.
+__device__ __forceinline__ void grid_arrive_wait(unsigned int* bar, unsigned int nblocks, unsigned int& epoch) {
+    ++epoch;
+    if (threadIdx.x == 0) {
+        unsigned int old;
+        asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(bar) : "memory");
+        const unsigned int target = epoch * nblocks;
+        while (ld_acquire_gpu(bar) < target) {
+        }
+    }
+    __syncthreads();
+}
+
 __device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int nblocks, unsigned int& epoch) {
     __syncthreads();
     ++epoch;

@@ -12,6 +12,7 @@
 //    (cooperative launch); small levels run in a single CTA with
 //    __syncthreads only.
 // Float64 throughout, FMA contraction off, sums associated as in numpy.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -142,6 +143,37 @@ __device__ __forceinline__ void reduce(double (&v)[NV], double* sh, const CgPara
     __syncthreads();
 }
 
+// Grid-wide fixed-order sum with 3 CTA barriers: block_sum1, the grid
+// arrival/wait, and the broadcast of warp 0's sum over the CTA partials.
+// sh: 2*4*32 (block_sum1 buffers) + 2*4 (broadcast buffers) doubles.
+struct RedState {
+    unsigned int epoch = 0;
+    int par = 0, bpar = 0;
+};
+template <int NV>
+__device__ __forceinline__ void grid_reduce(double (&v)[NV], double* sh, const CgParams& P, RedState& st) {
+    block_sum1<NV>(v, sh, st.par);
+    if (threadIdx.x == 0)
+#pragma unroll
+        for (int k = 0; k < NV; ++k) P.partials[blockIdx.x * 4 + k] = v[k];
+    grid_arrive_wait(P.bar, gridDim.x, st.epoch);
+    double* bc = sh + 2 * 4 * 32 + st.bpar * 4;
+    st.bpar ^= 1;
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            double s = 0.0;
+            for (int g = lane; g < (int)gridDim.x; g += 32) s += __ldcg(P.partials + g * 4 + k);
+            s = warp_sum(s);
+            if (lane == 0) bc[k] = s;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < NV; ++k) v[k] = bc[k];
+}
+
 template <bool kGrid>
 __global__ void __launch_bounds__(kThreads, 1) cg_level_kernel(CgParams P) {
     __shared__ double sh[4 * 32];
@@ -266,6 +298,9 @@ __global__ void __launch_bounds__(kThreads, 1) cg_level_kernel(CgParams P) {
 }
 
 #include "cg_band.cuh"
+#include "cg_band2.cuh"
+#include "cg_small.cuh"
+#include "cg_cluster.cuh"
 
 // ---------------------------------------------------------------- strict residual check
 
@@ -336,7 +371,39 @@ void InpaintWorkspace::reserve(int h, int w, int dev) {
     cap_coarse = coarse;
     const char* env = getenv("HIVC_CG_BAND");
     band_enabled = !(env && env[0] == '0');
+    band_variant = (env && env[0] == '1') ? 1 : 2;
+    CUDA_CHECK(cudaFuncSetAttribute(cg_band2_kernel<4, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    CUDA_CHECK(cudaFuncSetAttribute(cg_band2_kernel<8, 4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    const char* env_small = getenv("HIVC_CG_SMALL");
+    small_enabled = !(env_small && env_small[0] == '0');
     CUDA_CHECK(cudaFuncSetAttribute(cg_band_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    CUDA_CHECK(cudaFuncSetAttribute(cg_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    // 16-CTA clusters (non-portable size) for the coarse/mid levels
+    const char* env_cl = getenv("HIVC_CG_CLUSTER");
+    cluster_ok = !(env_cl && env_cl[0] == '0');
+    if (cluster_ok) {
+        cluster_ok = cudaFuncSetAttribute(cg_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+                         cudaSuccess &&
+                     cudaFuncSetAttribute(cg_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          200 * 1024) == cudaSuccess;
+        if (cluster_ok) {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(kClusterSize);
+            cfg.blockDim = dim3(kClThreads);
+            cfg.dynamicSmemBytes = 200 * 1024;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = kClusterSize;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            int nclusters = 0;
+            cluster_ok = cudaOccupancyMaxActiveClusters(&nclusters, cg_cluster_kernel, &cfg) == cudaSuccess &&
+                         nclusters > 0;
+        }
+        cudaGetLastError();  // clear a rejected attribute
+    }
 }
 
 void InpaintWorkspace::release() {
@@ -391,7 +458,84 @@ int solve_homogeneous_async(InpaintWorkspace& ws, cudaStream_t s, const double* 
         ++*launches;
     }
     CUDA_CHECK(cudaGetLastError());
-    for (int l = L - 1; l >= 0; --l) {
+    // coarse and mid levels: one thread-block-cluster launch (levels whose
+    // 16 row bands fit on chip), else one single-CTA launch for the tiny ones
+    int l_start = L - 1;
+    if (ws.cluster_ok) {
+        ClusterLevels S{};
+        size_t smem = 0;
+        int l = L - 1;
+        while (l >= 0 && S.nlev < kClMaxLevels) {
+            const int h = shapes[l].first, w = shapes[l].second;
+            const int br = (h + kClusterSize - 1) / kClusterSize;
+            const size_t need =
+                ((size_t)(br + 2) * (w + 2) + (size_t)br * w + 6 * (size_t)w) * sizeof(double) + (size_t)br * w;
+            if ((size_t)br * w > (size_t)kClPx * kClThreads || w > kClMaxW || need > 200 * 1024) break;
+            const int i = S.nlev++;
+            S.h[i] = h;
+            S.w[i] = w;
+            S.f[i] = lf[l];
+            S.m[i] = lm[l];
+            S.u[i] = lu[l];
+            S.iters[i] = ws.iters + (L - 1 - l);
+            smem = std::max(smem, need);
+            --l;
+        }
+        if (S.nlev > 0) {
+            S.uc0 = nullptr;
+            S.last_is_finest = l < 0;
+            if (getenv("HIVC_CG_TRACE_CLUSTER")) {
+                if (!ws.trace) CUDA_CHECK(cudaMalloc(&ws.trace, kTraceLen * sizeof(unsigned long long)));
+                CUDA_CHECK(cudaMemsetAsync(ws.trace, 0, kTraceLen * sizeof(unsigned long long), s));
+                S.trace = ws.trace;
+            }
+            S.tol = tol;
+            S.max_iter = max_iter;
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(kClusterSize);
+            cfg.blockDim = dim3(kClThreads);
+            cfg.dynamicSmemBytes = smem;
+            cfg.stream = s;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = kClusterSize;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            CUDA_CHECK(cudaLaunchKernelEx(&cfg, cg_cluster_kernel, S));
+            ++*launches;
+            l_start = l;
+        }
+    }
+    if (ws.small_enabled && l_start == L - 1) {
+        SmallLevels S{};
+        size_t smem = 0;
+        int l = L - 1;
+        while (l >= 0 && (size_t)shapes[l].first * shapes[l].second <= (size_t)kSmallMaxPx &&
+               S.nlev < kSmallMaxLevels) {
+            const int i = S.nlev++;
+            S.h[i] = shapes[l].first;
+            S.w[i] = shapes[l].second;
+            S.f[i] = lf[l];
+            S.m[i] = lm[l];
+            S.u[i] = lu[l];
+            S.iters[i] = ws.iters + (L - 1 - l);
+            const size_t n = (size_t)S.h[i] * S.w[i];
+            smem = std::max(smem, ((size_t)(S.h[i] + 2) * (S.w[i] + 2) + n) * sizeof(double) + n);
+            --l;
+        }
+        if (S.nlev > 0) {
+            S.last_is_finest = l < 0;
+            S.tol = tol;
+            S.max_iter = max_iter;
+            cg_small_kernel<<<1, kSmallThreads, smem, s>>>(S);
+            ++*launches;
+            CUDA_CHECK(cudaGetLastError());
+            l_start = l;
+        }
+    }
+    for (int l = l_start; l >= 0; --l) {
         CgParams P;
         P.h = shapes[l].first;
         P.w = shapes[l].second;
@@ -437,15 +581,23 @@ int solve_homogeneous_async(InpaintWorkspace& ws, cudaStream_t s, const double* 
             P.ex_p = ws.ex + (size_t)2 * nbands * P.w;
             double* setup = ws.partials + 4096;
             if (getenv("HIVC_CG_TRACE") && l == 0) {
-                if (!ws.trace) CUDA_CHECK(cudaMalloc(&ws.trace, 256 * 8 * sizeof(unsigned long long)));
-                CUDA_CHECK(cudaMemsetAsync(ws.trace, 0, 256 * 8 * sizeof(unsigned long long), s));
+                if (!ws.trace) CUDA_CHECK(cudaMalloc(&ws.trace, kTraceLen * sizeof(unsigned long long)));
+                CUDA_CHECK(cudaMemsetAsync(ws.trace, 0, kTraceLen * sizeof(unsigned long long), s));
                 P.trace = ws.trace;
             }
+            cg_setup_x_kernel<<<kSetupCtas, 512, 0, s>>>(P);
             cg_setup_kernel<<<kSetupCtas, 512, 0, s>>>(P, setup);
-            ++*launches;
+            *launches += 2;
             void* args[] = {&P, &setup};
-            CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)cg_band_kernel, dim3(nbands), dim3(kBandThreads), args,
-                                                   band_smem, s));
+            const int kc = (P.w + kBandThreads - 1) / kBandThreads;
+            const void* fn = (const void*)cg_band_kernel;
+            size_t smem_b = band_smem;
+            if (ws.band_variant == 2) {
+                smem_b = (size_t)(kBandRows + 2) * (P.w + 2) * sizeof(double);
+                fn = (band_rows <= 4 && kc <= 2) ? (const void*)cg_band2_kernel<4, 2, true>
+                                                 : (const void*)cg_band2_kernel<8, 4, false>;
+            }
+            CUDA_CHECK(cudaLaunchCooperativeKernel(fn, dim3(nbands), dim3(kBandThreads), args, smem_b, s));
         } else {
             void* args[] = {&P};
             CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)cg_level_kernel<true>, dim3(ws.grid_ctas),

@@ -19,6 +19,8 @@
 
 namespace hivc {
 
+constexpr int kTraceLen = 2048 + 256 * 160;  // HIVC_CG_TRACE: phase stamps + per-CTA arrival stamps
+
 // Device scratch for one solve at a time (per stream): finest-level CG
 // vectors x, r, p (two buffers), A p, plus every coarser level's f, mask, u.
 struct InpaintWorkspace {
@@ -29,6 +31,9 @@ struct InpaintWorkspace {
     double* ex = nullptr;       // band-kernel row exchange buffers
     unsigned long long* trace = nullptr;  // HIVC_CG_TRACE diagnostics (finest level phase timestamps)
     bool band_enabled = true;   // HIVC_CG_BAND=0 selects the streaming kernel
+    int band_variant = 2;       // HIVC_CG_BAND=1: row-mapped band kernel; default: column-streaming
+    bool small_enabled = true;  // HIVC_CG_SMALL=0: one single-CTA launch per coarse level instead
+    bool cluster_ok = false;    // 16-CTA cluster kernel for coarse/mid levels (HIVC_CG_CLUSTER=0 disables)
     double* dbl = nullptr;
     uint8_t* bytes = nullptr;
     double* partials = nullptr;

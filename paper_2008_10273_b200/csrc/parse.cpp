@@ -7,6 +7,20 @@
 
 namespace hivc {
 
+// bit-reversed bytes: MSB-first bitmap byte -> LSB-first tile bits
+static const struct BitRev {
+    uint8_t t[256];
+    constexpr BitRev() : t() {
+        for (int i = 0; i < 256; ++i) {
+            int r = 0;
+            for (int b = 0; b < 8; ++b)
+                if (i & (1 << b)) r |= 1 << (7 - b);
+            t[i] = (uint8_t)r;
+        }
+    }
+    uint8_t operator[](int i) const { return t[i]; }
+} kBitReverse;
+
 static inline uint32_t rd_u32(const uint8_t* p) {
     uint32_t v;
     std::memcpy(&v, p, 4);
@@ -126,30 +140,12 @@ size_t decode_signed_values(const uint8_t* d, size_t len, size_t pos, std::vecto
 }
 
 void parse_tree_leaves(BitReader& rd, int32_t w, int32_t h, std::vector<Rect>& leaves) {
-    std::vector<Rect> st;  // subdivision.py:198-222
-    st.reserve(64);
-    st.push_back({0, 0, w, h});
-    while (!st.empty()) {
-        Rect r = st.back();
-        st.pop_back();
-        if (rd.bit()) {
-            if (r.w == 1 && r.h == 1) fail(HIVC_E_SUBDIVISION, "split of a single pixel");
-            if (r.h > r.w) {
-                int32_t a = (r.h + 1) / 2;
-                st.push_back({r.x, r.y + a, r.w, r.h - a});
-                st.push_back({r.x, r.y, r.w, a});
-            } else {
-                int32_t a = (r.w + 1) / 2;
-                st.push_back({r.x + a, r.y, r.w - a, r.h});
-                st.push_back({r.x, r.y, a, r.h});
-            }
-        } else {
-            leaves.push_back(r);
-        }
-    }
+    walk_tree(rd, w, h, [&](int32_t x, int32_t y, int32_t rw, int32_t rh) { leaves.push_back({x, y, rw, rh}); });
 }
 
-void parse_flow_tree(BitReader& rd, int32_t w, int32_t h, std::vector<int32_t>& nodes, int32_t& nleaves) {
+void parse_flow_tree(BitReader& rd, int32_t w, int32_t h, std::vector<int32_t>& nodes, int32_t& nleaves,
+                     std::vector<Rect>* leaves) {
+    if (leaves) leaves->clear();
     // Same preorder walk as parse_tree_leaves (subdivision.py:183-195), but
     // recording the split structure.  The stack carries the index of the
     // parent whose right-child slot the popped rectangle fills (-1: none).
@@ -185,6 +181,29 @@ void parse_flow_tree(BitReader& rd, int32_t w, int32_t h, std::vector<int32_t>& 
         } else {
             nodes.push_back(0);
             nodes.push_back(nleaves++);
+            if (leaves) leaves->push_back(r);
+        }
+    }
+}
+
+// Tile -> covering leaf map (0xFFFF: tile straddles leaves).  Leaves tile the
+// plane, so a tile is either inside one leaf or mixed.
+static void flow_tile_map(const std::vector<Rect>& leaves, int32_t w, int32_t h, std::vector<uint16_t>& tiles) {
+    const int nbx = (w + 7) / 8, nby = (h + 7) / 8;
+    tiles.assign((size_t)nbx * nby, 0xFFFF);
+    if (leaves.size() >= 0xFFFF) return;  // all mixed: per-pixel walk
+    for (size_t li = 0; li < leaves.size(); ++li) {
+        const Rect& r = leaves[li];
+        // tiles entirely inside the leaf (edge tiles are clipped to the plane)
+        const int tx0 = (r.x + 7) / 8, ty0 = (r.y + 7) / 8;
+        for (int ty = ty0; ty < nby; ++ty) {
+            const int y0 = ty * 8, y1 = std::min(h, y0 + 8);
+            if (y1 > r.y + r.h) break;
+            for (int tx = tx0; tx < nbx; ++tx) {
+                const int x0 = tx * 8, x1 = std::min(w, x0 + 8);
+                if (x1 > r.x + r.w) break;
+                tiles[(size_t)ty * nbx + tx] = (uint16_t)li;
+            }
         }
     }
 }
@@ -246,16 +265,16 @@ static size_t intra_tree(const uint8_t* d, size_t len, size_t pos, int32_t h, in
     size_t nbytes = ((size_t)nbits + 7) / 8;
     if (pos + nbytes > len) fail(HIVC_E_TRUNCATED_STREAM, "intra payload truncated");
     BitReader rd(d + pos, nbytes, nbits);
-    std::vector<Rect> leaves;
-    parse_tree_leaves(rd, w, h, leaves);
     const size_t npx = (size_t)h * w;
     bits.assign((npx + 63) / 64, 0);
-    for (const Rect& r : leaves) {
-        size_t i = (size_t)(r.y + r.h / 2) * w + (r.x + r.w / 2);
+    size_t nleaves = 0;
+    walk_tree(rd, w, h, [&](int32_t x, int32_t y, int32_t rw, int32_t rh) {
+        const size_t i = (size_t)(y + rh / 2) * w + (x + rw / 2);
         bits[i >> 6] |= 1ull << (i & 63);
-    }
+        ++nleaves;
+    });
     pts.clear();
-    pts.reserve(leaves.size());
+    pts.reserve(nleaves);
     for (size_t wi = 0; wi < bits.size(); ++wi) {
         uint64_t b = bits[wi];
         while (b) {
@@ -317,7 +336,9 @@ size_t parse_flow(const uint8_t* d, size_t len, size_t pos, int32_t h, int32_t w
         if (pos + nbytes > len) fail(HIVC_E_TRUNCATED_STREAM, "flow payload truncated");
         BitReader rd(d + pos, nbytes, nbits);
         int32_t nleaves = 0;
-        parse_flow_tree(rd, w, h, job.nodes[c], nleaves);
+        std::vector<Rect> leaves;
+        parse_flow_tree(rd, w, h, job.nodes[c], nleaves, &leaves);
+        flow_tile_map(leaves, w, h, job.tiles[c]);
         pos += nbytes;
         std::vector<int32_t> idx;
         pos = decode_symbols(d, len, pos, idx);
@@ -367,8 +388,12 @@ size_t parse_residual(const uint8_t* d, size_t len, size_t pos, int32_t h, int32
         const size_t nwords = (ntiles + 63) / 64;
         g.tile_words.assign(nwords, 0);
         g.word_prefix.assign(nwords, 0);
-        for (size_t t = 0; t < ntiles; ++t)
-            if ((d[pos + (t >> 3)] >> (7 - (t & 7))) & 1) g.tile_words[t >> 6] |= 1ull << (t & 63);
+        for (size_t byte = 0; byte < nskip; ++byte) {  // tile 8j+i = bit 7-i of byte j
+            uint64_t v = kBitReverse[d[pos + byte]];
+            if (!v) continue;
+            if (byte == nskip - 1 && (ntiles & 7)) v &= (1u << (ntiles & 7)) - 1u;  // np.unpackbits(...)[:ntiles]
+            g.tile_words[byte >> 3] |= v << ((byte & 7) * 8);
+        }
         pos += nskip;
         int32_t acc = 0;
         for (size_t i = 0; i < nwords; ++i) {
@@ -393,10 +418,10 @@ size_t parse_residual(const uint8_t* d, size_t len, size_t pos, int32_t h, int32
                 bits &= bits - 1;
                 int32_t ty = (int32_t)(t / nbx), tx = (int32_t)(t % nbx);
                 int32_t bh = std::min(8, h - ty * 8), bw = std::min(8, w - tx * 8);
-                leaves.clear();
-                parse_tree_leaves(rd, bw, bh, leaves);  // parse_mask per coded tile (codec.py:300-303)
-                uint64_t m = 0;
-                for (const Rect& r : leaves) m |= 1ull << ((r.y + r.h / 2) * 8 + (r.x + r.w / 2));
+                uint64_t m = 0;  // parse_mask per coded tile (codec.py:300-303)
+                walk_tree(rd, bw, bh, [&](int32_t x, int32_t y, int32_t rw, int32_t rh) {
+                    m |= 1ull << ((y + rh / 2) * 8 + (x + rw / 2));
+                });
                 g.block_mask[b] = m;
                 g.block_off[b] = npts;
                 npts += __builtin_popcountll(m);

@@ -15,32 +15,93 @@
 
 namespace hivc {
 
-// MSB-first reader with a hard bit limit (reference bits.py:41-78).
+// MSB-first reader with a hard bit limit (reference bits.py:41-78), with a
+// 64-bit look-ahead buffer: the next `avail` bits sit at the top of `buf`.
 struct BitReader {
     const uint8_t* d;
     size_t nbytes;
     uint64_t limit;
     uint64_t pos = 0;
+    uint64_t buf = 0;
+    int avail = 0;
+    size_t next = 0;
     BitReader(const uint8_t* data, size_t nb, uint64_t nbits) : d(data), nbytes(nb), limit(nbits) {
         if (nbits > (uint64_t)nb * 8) fail(HIVC_E_TRUNCATED_STREAM, "bit length exceeds buffer");
     }
+    inline void refill() {
+        while (avail <= 56 && next < nbytes) {
+            buf |= (uint64_t)d[next++] << (56 - avail);
+            avail += 8;
+        }
+    }
+    void seek(uint64_t bitpos) {  // absolute bit position
+        pos = bitpos;
+        next = (size_t)(bitpos >> 3);
+        buf = 0;
+        avail = 0;
+        refill();
+        const int drop = (int)(bitpos & 7);
+        if (drop && avail >= drop) {
+            buf <<= drop;
+            avail -= drop;
+        }
+    }
     inline uint32_t bit() {
-        if (pos + 1 > limit) fail(HIVC_E_TRUNCATED_STREAM, "bit stream exhausted");
-        uint32_t b = (d[pos >> 3] >> (7 - (pos & 7))) & 1u;
+        if (pos >= limit) fail(HIVC_E_TRUNCATED_STREAM, "bit stream exhausted");
+        if (avail == 0) refill();
+        const uint32_t b = (uint32_t)(buf >> 63);
+        buf <<= 1;
+        --avail;
         ++pos;
         return b;
     }
     inline uint32_t take(int n) {  // n <= 32
         if (n == 0) return 0;
         if (pos + (uint64_t)n > limit) fail(HIVC_E_TRUNCATED_STREAM, "bit stream exhausted");
-        uint64_t byte = pos >> 3;
-        int off = (int)(pos & 7);
-        uint64_t v = 0;
-        for (int i = 0; i < 5; ++i) v = (v << 8) | (byte + i < nbytes ? d[byte + i] : 0u);
+        if (avail < n) refill();
+        const uint32_t v = (uint32_t)(buf >> (64 - n));
+        buf <<= n;
+        avail -= n;
         pos += (uint64_t)n;
-        return (uint32_t)((v >> (40 - off - n)) & ((1ull << n) - 1));
+        return v;
     }
 };
+
+// Preorder walk of one serialised subdivision tree (subdivision.py:198-222):
+// bit 1 halves the longer side (ties halve the width, first half rounded up),
+// bit 0 is a leaf -> on_leaf(x, y, w, h).  The explicit stack never holds
+// more than (tree depth + 1) rectangles.
+template <class F>
+inline void walk_tree(BitReader& rd, int32_t w, int32_t h, F&& on_leaf) {
+    int32_t st[4 * 130];
+    int sp = 0;
+    st[0] = 0;
+    st[1] = 0;
+    st[2] = w;
+    st[3] = h;
+    sp = 1;
+    while (sp) {
+        --sp;
+        const int32_t x = st[4 * sp], y = st[4 * sp + 1], rw = st[4 * sp + 2], rh = st[4 * sp + 3];
+        if (rd.bit()) {
+            if (rw == 1 && rh == 1) fail(HIVC_E_SUBDIVISION, "split of a single pixel");
+            if (sp + 2 > 130) fail(HIVC_E_SUBDIVISION, "subdivision tree too deep");
+            int32_t* a = st + 4 * sp;
+            if (rh > rw) {
+                const int32_t t = (rh + 1) / 2;
+                a[0] = x, a[1] = y + t, a[2] = rw, a[3] = rh - t;  // second child, popped last
+                a[4] = x, a[5] = y, a[6] = rw, a[7] = t;
+            } else {
+                const int32_t t = (rw + 1) / 2;
+                a[0] = x + t, a[1] = y, a[2] = rw - t, a[3] = rh;
+                a[4] = x, a[5] = y, a[6] = t, a[7] = rh;
+            }
+            sp += 2;
+        } else {
+            on_leaf(x, y, rw, rh);
+        }
+    }
+}
 
 uint64_t read_uvarint(const uint8_t* d, size_t len, size_t& pos);
 
@@ -68,7 +129,8 @@ void parse_tree_leaves(BitReader& rd, int32_t w, int32_t h, std::vector<Rect>& l
 // code = nodes[2i] (0 leaf, 1 split on x, 2 split on y) in the low 2 bits and
 // the absolute split coordinate above; nodes[2i+1] = right child index for a
 // split (the left child is i+1) or the leaf's value index.
-void parse_flow_tree(BitReader& rd, int32_t w, int32_t h, std::vector<int32_t>& nodes, int32_t& nleaves);
+void parse_flow_tree(BitReader& rd, int32_t w, int32_t h, std::vector<int32_t>& nodes, int32_t& nleaves,
+                     std::vector<Rect>* leaves = nullptr);
 
 struct StreamHeader {
     int32_t width, height, frame_count, fps_num, fps_den, gop_size, channels;
@@ -94,6 +156,9 @@ size_t parse_intra(const uint8_t* d, size_t len, size_t pos, int32_t h, int32_t 
 struct FlowJob {
     std::vector<int32_t> nodes[2];   // u, v trees
     std::vector<double> vals[2];
+    // per 8x8 tile: index of the leaf covering the whole tile, 0xFFFF when the
+    // tile straddles a leaf boundary (then the device walks the tree per pixel)
+    std::vector<uint16_t> tiles[2];
 };
 // flow.decompress_flow (flow.py:343-372); returns next pos.
 size_t parse_flow(const uint8_t* d, size_t len, size_t pos, int32_t h, int32_t w, int levels, FlowJob& job);

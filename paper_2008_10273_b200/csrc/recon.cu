@@ -83,27 +83,18 @@ __global__ void __launch_bounds__(256) frame_kernel(FrameArgs A) {
     bool live[2];
     // ---- prediction
     if (kInter) {
-        // flow leaves are axis-aligned rectangles: if the tile's two corners fall in
-        // the same leaf the whole tile has one (u, v); lanes 0..3 test u/v corners
-        int leaf = 0;
-        if (tile_ok && lane < 4) {
-            const int c = lane >> 1;
-            const int xc = (lane & 1) ? min(tx * 8 + 7, w - 1) : tx * 8;
-            const int yc = (lane & 1) ? min(ty * 8 + 7, h - 1) : ty * 8;
-            leaf = flow_leaf(A.flow.nodes[c], xc, yc);
-        }
-        const int lu0 = __shfl_sync(0xffffffffu, leaf, 0), lu1 = __shfl_sync(0xffffffffu, leaf, 1);
-        const int lv0 = __shfl_sync(0xffffffffu, leaf, 2), lv1 = __shfl_sync(0xffffffffu, leaf, 3);
+        // the host rasterised each flow tree to tiles: most tiles lie inside one
+        // leaf (one (u, v) for the tile); tiles on a leaf boundary walk the tree
+        const size_t tt = (size_t)ty * nbx + (tile_ok ? tx : 0);
+        const int lu = __ldg(A.flow.tiles[0] + tt), lv = __ldg(A.flow.tiles[1] + tt);
 #pragma unroll
         for (int rr = 0; rr < 2; ++rr) {
             const int y = ty * 8 + ly + 4 * rr;
             live[rr] = tile_ok && x < w && y < h;
             if (!live[rr]) continue;
             // flow.py:94-127 — coordinates clamped before flooring, taps summed w00..w11
-            double u = lu0 == lu1 ? __ldg(A.flow.vals[0] + __ldg(A.flow.nodes[0] + 2 * lu0 + 1))
-                                  : flow_lookup(A.flow.nodes[0], A.flow.vals[0], x, y);
-            double v = lv0 == lv1 ? __ldg(A.flow.vals[1] + __ldg(A.flow.nodes[1] + 2 * lv0 + 1))
-                                  : flow_lookup(A.flow.nodes[1], A.flow.vals[1], x, y);
+            double u = lu != 0xFFFF ? __ldg(A.flow.vals[0] + lu) : flow_lookup(A.flow.nodes[0], A.flow.vals[0], x, y);
+            double v = lv != 0xFFFF ? __ldg(A.flow.vals[1] + lv) : flow_lookup(A.flow.nodes[1], A.flow.vals[1], x, y);
             double sx = fmin(fmax((double)x + u, 0.0), (double)(w - 1));
             double sy = fmin(fmax((double)y + v, 0.0), (double)(h - 1));
             int x0 = (int)floor(sx), y0 = (int)floor(sy);

@@ -29,6 +29,7 @@ struct ResDev {
 struct FlowDev {
     const int32_t* nodes[2] = {nullptr, nullptr};  // u, v trees (parse.h: parse_flow_tree)
     const double* vals[2] = {nullptr, nullptr};
+    const uint16_t* tiles[2] = {nullptr, nullptr};  // per-tile covering leaf, 0xFFFF = mixed
 };
 
 struct FrameArgs {
