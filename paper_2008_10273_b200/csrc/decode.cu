@@ -175,7 +175,13 @@ void Lane::reserve_stage(int slot, size_t bytes) {
 }
 
 void Lane::reserve_gop_out(size_t bytes) {
+    if (!copy) {
+        CUDA_CHECK(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking));
+        for (auto& e : frame_ev) CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        for (auto& e : out_free) CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
     if (bytes <= gop_out_cap) return;
+    CUDA_CHECK(cudaStreamSynchronize(copy));
     for (int k = 0; k < 2; ++k) {
         if (gop_out[k]) cudaFree(gop_out[k]);
         CUDA_CHECK(cudaMalloc(&gop_out[k], bytes));
@@ -185,6 +191,7 @@ void Lane::reserve_gop_out(size_t bytes) {
 
 Lane::~Lane() {
     if (stream) cudaStreamSynchronize(stream);
+    if (copy) cudaStreamSynchronize(copy);
     for (int c = 0; c < 3; ++c) {
         if (f[c]) cudaFree(f[c]);
         if (u[c]) cudaFree(u[c]);
@@ -198,8 +205,12 @@ Lane::~Lane() {
         if (staged[t]) cudaEventDestroy(staged[t]);
         if (gop_out[t]) cudaFree(gop_out[t]);
     }
-    for (auto& e : ev)
+    if (copy) cudaStreamSynchronize(copy);
+    for (auto& e : frame_ev)
         if (e) cudaEventDestroy(e);
+    for (auto& e : out_free)
+        if (e) cudaEventDestroy(e);
+    if (copy) cudaStreamDestroy(copy);
     if (stream) cudaStreamDestroy(stream);
 }
 
@@ -323,6 +334,8 @@ void decode_gop(Context& ctx, Lane& L, const StreamJob& S, int gi, bool out_on_d
     CUDA_CHECK(cudaEventRecord(L.staged[slot], s));
     const uint8_t* dev = L.dev_stage[slot];
     uint8_t* gop_dev = out_on_device ? S.out + S.frame_base[gi] * frame_bytes : L.gop_out[slot];
+    uint8_t* gop_host = out_on_device ? nullptr : S.out + S.frame_base[gi] * frame_bytes;
+    if (!out_on_device) CUDA_CHECK(cudaStreamWaitEvent(s, L.out_free[slot], 0));  // copies out of this slot done
     for (size_t fi = 0; fi < jobs.size(); ++fi) {
         const FrameJob& J = jobs[fi];
         const FrameOffsets& o = offs[fi];
@@ -405,12 +418,15 @@ void decode_gop(Context& ctx, Lane& L, const StreamJob& S, int gi, bool out_on_d
             ctx.launches += 1;
             ev_end(ev_inter);
         }
+        if (!out_on_device) {  // frame fi is final: copy it out while fi+1 decodes
+            cudaEvent_t fe = L.frame_ev[L.frame_ev_next++ % Lane::kFrameEv];
+            CUDA_CHECK(cudaEventRecord(fe, s));
+            CUDA_CHECK(cudaStreamWaitEvent(L.copy, fe, 0));
+            CUDA_CHECK(cudaMemcpyAsync(gop_host + fi * frame_bytes, fr, frame_bytes, cudaMemcpyDeviceToHost, L.copy));
+            R.d2h += (int64_t)frame_bytes;
+        }
     }
-    if (!out_on_device) {
-        size_t nb = jobs.size() * frame_bytes;
-        CUDA_CHECK(cudaMemcpyAsync(S.out + S.frame_base[gi] * frame_bytes, gop_dev, nb, cudaMemcpyDeviceToHost, s));
-        R.d2h += (int64_t)nb;
-    }
+    if (!out_on_device) CUDA_CHECK(cudaEventRecord(L.out_free[slot], L.copy));
     slot ^= 1;
 }
 
@@ -429,6 +445,8 @@ void run_lane(Context& ctx, Lane& L, const std::vector<StreamJob>& streams, cons
             decode_gop(ctx, L, streams[it.stream], it.gop, out_on_device, timed, R, jobs, bits, slot, ev_intra,
                        ev_inter, ev_ifin);
         }
+        if (!out_on_device && !items.empty())  // the span ends with the last D2H copy
+            CUDA_CHECK(cudaStreamWaitEvent(L.stream, L.out_free[slot ^ 1], 0));
         CUDA_CHECK(cudaEventRecord(done, L.stream));
         CUDA_CHECK(cudaStreamSynchronize(L.stream));
         R.gpu_intra = drain(ev_intra);
@@ -440,11 +458,13 @@ void run_lane(Context& ctx, Lane& L, const std::vector<StreamJob>& streams, cons
         R.msg = e.what();
         cudaEventRecord(done, L.stream);
         cudaStreamSynchronize(L.stream);
+        if (L.copy) cudaStreamSynchronize(L.copy);
     } catch (const std::exception& e) {
         R.code = HIVC_E_ARGUMENT;
         R.msg = e.what();
         cudaEventRecord(done, L.stream);
         cudaStreamSynchronize(L.stream);
+        if (L.copy) cudaStreamSynchronize(L.copy);
     }
 }
 

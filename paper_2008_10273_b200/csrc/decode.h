@@ -33,7 +33,13 @@ struct Lane {
     cudaEvent_t staged[2] = {nullptr, nullptr};
     uint8_t* gop_out[2] = {nullptr, nullptr};  // device frame buffers when output goes to the host
     size_t gop_out_cap = 0;
-    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    // host output: each finished frame is copied D2H on `copy` while the lane
+    // stream decodes the next one; out_free[slot] = last copy out of gop_out[slot]
+    cudaStream_t copy = nullptr;
+    static constexpr int kFrameEv = 8;
+    cudaEvent_t frame_ev[kFrameEv] = {};
+    cudaEvent_t out_free[2] = {nullptr, nullptr};
+    int frame_ev_next = 0;
     CgProbe probe;
     void reserve_planes(int h, int w, int channels);
     void reserve_stage(int slot, size_t bytes);
