@@ -9,7 +9,10 @@
 // inter: fused warp/residual/finalize (recon.cu).  Parsing of GOP k+1
 // overlaps the GPU work of GOP k (double-buffered staging).
 #include <algorithm>
+#include <atomic>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <thread>
@@ -41,16 +44,23 @@ struct HostTimes {
     double intra_parse = 0, flow_parse = 0, residual_parse = 0;
 };
 
-void parse_gop(const uint8_t* p, size_t n, const StreamHeader& hd, int gi, std::vector<FrameJob>& jobs, HostTimes& ht,
-               std::vector<uint64_t>& bits) {
-    const std::string gs = std::to_string(gi);
-    if (n < 2) fail(HIVC_E_TRUNCATED, "group " + gs + " payload too small");
-    uint16_t nframes;
-    std::memcpy(&nframes, p, 2);
-    size_t pos = 2;
-    jobs.resize(nframes);
-    for (int fi = 0; fi < nframes; ++fi) {
-        FrameJob& J = jobs[fi];
+// Frame records of one GOP payload, parsed one at a time (codec.decode's frame
+// loop, codec.py:496-556; record layout bitstream.py:157-196).
+struct GopCursor {
+    const uint8_t* p;
+    size_t n, pos = 2;
+    const StreamHeader& hd;
+    std::string gs;
+    int nframes = 0, next = 0;
+    GopCursor(const uint8_t* data, size_t len, const StreamHeader& h, int gi)
+        : p(data), n(len), hd(h), gs(std::to_string(gi)) {
+        if (n < 2) fail(HIVC_E_TRUNCATED, "group " + gs + " payload too small");
+        uint16_t nf;
+        std::memcpy(&nf, p, 2);
+        nframes = nf;
+    }
+    void parse(FrameJob& J, HostTimes& ht, std::vector<uint64_t>& bits) {
+        const int fi = next++;
         if (pos + 5 > n) fail(HIVC_E_TRUNCATED, "frame record cut short in group " + gs);
         uint8_t ftype = p[pos];
         uint32_t plen = rd_u32(p + pos + 1);
@@ -81,7 +91,17 @@ void parse_gop(const uint8_t* p, size_t n, const StreamHeader& hd, int gi, std::
         if (used != rlen) fail(HIVC_E_CODEC, "residual payload length mismatch in group " + gs);
         pos += rlen;
     }
-    if (pos != n) fail(HIVC_E_CODEC, "trailing bytes in group " + gs);
+    void finish() const {
+        if (pos != n) fail(HIVC_E_CODEC, "trailing bytes in group " + gs);
+    }
+};
+
+void parse_gop(const uint8_t* p, size_t n, const StreamHeader& hd, int gi, std::vector<FrameJob>& jobs, HostTimes& ht,
+               std::vector<uint64_t>& bits) {
+    GopCursor cur(p, n, hd, gi);
+    jobs.resize(cur.nframes);
+    for (int fi = 0; fi < cur.nframes; ++fi) cur.parse(jobs[fi], ht, bits);
+    cur.finish();
 }
 
 // Bump allocator over the pinned staging buffer.
@@ -200,10 +220,12 @@ Lane::~Lane() {
     }
     for (int t = 0; t < 2; ++t) {
         if (m[t]) cudaFree(m[t]);
+        if (gop_out[t]) cudaFree(gop_out[t]);
+    }
+    for (int t = 0; t < kStage; ++t) {
         if (host_stage[t]) cudaFreeHost(host_stage[t]);
         if (dev_stage[t]) cudaFree(dev_stage[t]);
         if (staged[t]) cudaEventDestroy(staged[t]);
-        if (gop_out[t]) cudaFree(gop_out[t]);
     }
     if (copy) cudaStreamSynchronize(copy);
     for (auto& e : frame_ev)
@@ -291,16 +313,29 @@ struct LaneResult {
     int64_t h2d = 0, d2h = 0;
     int64_t inter_frames = 0, intra_frames = 0;
     CgTotals cg;
+    std::string timeline;  // HIVC_TIMELINE rows: kind,stream,gop,frame,t0_us,t1_us (from the decode origin)
 };
 
-using EvPairs = std::vector<std::pair<cudaEvent_t, cudaEvent_t>>;
+struct EvRec {
+    cudaEvent_t first = nullptr, second = nullptr;
+    int stream = 0, gop = 0, frame = 0;
+};
+using EvPairs = std::vector<EvRec>;
 
-double drain(EvPairs& v) {
+double drain(EvPairs& v, cudaEvent_t origin, char kind, std::string* timeline) {
     double t = 0;
     for (auto& e : v) {
         float ms = 0;
         cudaEventElapsedTime(&ms, e.first, e.second);
         t += ms * 1e-3;
+        if (timeline) {
+            float a = 0, b = 0;
+            cudaEventElapsedTime(&a, origin, e.first);
+            cudaEventElapsedTime(&b, origin, e.second);
+            char line[128];
+            std::snprintf(line, sizeof line, "%c,%d,%d,%d,%.1f,%.1f\n", kind, e.stream, e.gop, e.frame, a * 1e3, b * 1e3);
+            *timeline += line;
+        }
         cudaEventDestroy(e.first);
         cudaEventDestroy(e.second);
     }
@@ -315,115 +350,129 @@ void decode_gop(Context& ctx, Lane& L, const StreamJob& S, int gi, bool out_on_d
     const int h = hd.height, w = hd.width, C = hd.channels;
     const size_t N = (size_t)h * w;
     const size_t frame_bytes = N * C;
-    parse_gop(S.data + S.gops[gi].first, S.gops[gi].second, hd, gi, jobs, R.ht, bits);
-    // pack the compact frame descriptions: measure, then write into pinned staging
-    Packer pk;
-    std::vector<FrameOffsets> offs(jobs.size());
-    for (size_t fi = 0; fi < jobs.size(); ++fi) pack_frame(pk, jobs[fi], offs[fi]);
-    size_t total = pk.off + 16;
-    if (L.staged[slot]) CUDA_CHECK(cudaEventSynchronize(L.staged[slot]));
-    L.reserve_stage(slot, total);
-    pk.base = L.host_stage[slot];
-    pk.off = 0;
-    pk.measure = false;
-    for (size_t fi = 0; fi < jobs.size(); ++fi) pack_frame(pk, jobs[fi], offs[fi]);
+    GopCursor cur(S.data + S.gops[gi].first, S.gops[gi].second, hd, gi);
+    const int nf = cur.nframes;
+    if ((int)jobs.size() < nf) jobs.resize(nf);
     cudaStream_t s = L.stream;
-    CUDA_CHECK(cudaMemcpyAsync(L.dev_stage[slot], L.host_stage[slot], pk.off, cudaMemcpyHostToDevice, s));
-    R.h2d += (int64_t)pk.off;
-    if (!L.staged[slot]) CUDA_CHECK(cudaEventCreateWithFlags(&L.staged[slot], cudaEventDisableTiming));
-    CUDA_CHECK(cudaEventRecord(L.staged[slot], s));
-    const uint8_t* dev = L.dev_stage[slot];
     uint8_t* gop_dev = out_on_device ? S.out + S.frame_base[gi] * frame_bytes : L.gop_out[slot];
     uint8_t* gop_host = out_on_device ? nullptr : S.out + S.frame_base[gi] * frame_bytes;
     if (!out_on_device) CUDA_CHECK(cudaStreamWaitEvent(s, L.out_free[slot], 0));  // copies out of this slot done
-    for (size_t fi = 0; fi < jobs.size(); ++fi) {
-        const FrameJob& J = jobs[fi];
-        const FrameOffsets& o = offs[fi];
-        FrameArgs A;
-        A.h = h;
-        A.w = w;
-        A.channels = C;
-        uint8_t* fr = gop_dev + fi * frame_bytes;
-        uint8_t* frprev = fi ? gop_dev + (fi - 1) * frame_bytes : nullptr;
-        for (int c = 0; c < C; ++c) {
-            if (C == 1) {
-                A.recon[c] = fr;  // gray: the reconstruction IS the output frame
-                A.prev[c] = frprev;
-            } else {
-                A.recon[c] = L.ring[fi & 1][c];
-                A.prev[c] = L.ring[(fi + 1) & 1][c];
-                A.rgb[c] = fr + c * N;
-            }
-        }
-        ResDev& RD = A.res;
-        RD.ngroups = J.res.zero ? 0 : J.res.ngroups;
-        RD.dz_step = 127.0 / (double)((hd.residual_levels - 1) / 2);  // quantize.py:43-47
-        RD.c_scale = J.res.c_scale;
-        RD.a_scale = J.res.a_scale;
-        for (int g = 0; g < RD.ngroups; ++g) {
-            const ResidualGroup& G = J.res.g[g];
-            ResGroupDev& D = RD.g[g];
-            D.nplanes = G.nplanes;
-            D.nblocks = G.nblocks;
-            D.npoints = G.npoints;
-            D.tile_words = at<uint64_t>(dev, o.g[g][0]);
-            D.word_prefix = at<int32_t>(dev, o.g[g][1]);
-            D.block_mask = at<uint64_t>(dev, o.g[g][2]);
-            D.block_off = at<int32_t>(dev, o.g[g][3]);
-            D.c_sym = at<int32_t>(dev, o.g[g][4]);
-            D.a_sym = at<int32_t>(dev, o.g[g][5]);
-        }
-        std::pair<cudaEvent_t, cudaEvent_t> e{nullptr, nullptr};
-        auto ev_begin = [&]() {
-            if (!timed) return;
-            CUDA_CHECK(cudaEventCreate(&e.first));
-            CUDA_CHECK(cudaEventCreate(&e.second));
-            CUDA_CHECK(cudaEventRecord(e.first, s));
-        };
-        auto ev_end = [&](EvPairs& v) {
-            if (!timed) return;
-            CUDA_CHECK(cudaEventRecord(e.second, s));
-            v.push_back(e);
-        };
-        ev_begin();
-        (J.type == 0 ? R.intra_frames : R.inter_frames) += 1;
-        if (J.type == 0) {
-            // intra: f = 0 with the values scattered at the mask points, then solve (prediction.py:203-208)
-            int64_t launches = 0;
+    // Parse and ship in chunks: the I-frame alone, so its solve runs while the
+    // host parses the P frames, then kChunk P frames at a time.
+    constexpr int kChunk = 2;
+    FrameOffsets offs[kChunk];
+    size_t fi = 0;
+    while ((int)fi < nf) {
+        const int cnt = fi == 0 ? 1 : std::min(kChunk, nf - (int)fi);
+        for (int k = 0; k < cnt; ++k) cur.parse(jobs[fi + k], R.ht, bits);
+        if ((int)fi + cnt == nf) cur.finish();
+        // pack the compact frame descriptions: measure, then write into pinned staging
+        Packer pk;
+        for (int k = 0; k < cnt; ++k) pack_frame(pk, jobs[fi + k], offs[k]);
+        const int b = L.stage_next++ % Lane::kStage;
+        if (L.staged[b]) CUDA_CHECK(cudaEventSynchronize(L.staged[b]));
+        L.reserve_stage(b, pk.off + 16);
+        pk.base = L.host_stage[b];
+        pk.off = 0;
+        pk.measure = false;
+        for (int k = 0; k < cnt; ++k) pack_frame(pk, jobs[fi + k], offs[k]);
+        CUDA_CHECK(cudaMemcpyAsync(L.dev_stage[b], L.host_stage[b], pk.off, cudaMemcpyHostToDevice, s));
+        R.h2d += (int64_t)pk.off;
+        if (!L.staged[b]) CUDA_CHECK(cudaEventCreateWithFlags(&L.staged[b], cudaEventDisableTiming));
+        CUDA_CHECK(cudaEventRecord(L.staged[b], s));
+        const uint8_t* dev = L.dev_stage[b];
+        for (int k = 0; k < cnt; ++k, ++fi) {
+            const FrameJob& J = jobs[fi];
+            const FrameOffsets& o = offs[k];
+            FrameArgs A;
+            A.h = h;
+            A.w = w;
+            A.channels = C;
+            uint8_t* fr = gop_dev + fi * frame_bytes;
+            uint8_t* frprev = fi ? gop_dev + (fi - 1) * frame_bytes : nullptr;
             for (int c = 0; c < C; ++c) {
-                int t = c == 0 ? 0 : 1;
-                const auto& pts = J.intra.pts[t];
-                CUDA_CHECK(cudaMemsetAsync(L.f[c], 0, N * sizeof(double), s));
-                if (c <= 1) CUDA_CHECK(cudaMemsetAsync(L.m[t], 0, N, s));
-                launch_scatter(at<int32_t>(dev, o.pts[t]), at<double>(dev, o.vals[c]), (int)pts.size(), L.f[c],
-                               c <= 1 ? L.m[t] : nullptr, s);
-                ++launches;
-                solve_homogeneous_async(L.ws, s, L.f[c], L.m[t], h, w, 1e-4, 160, L.u[c], &launches,
-                                        timed ? &L.probe : nullptr);
-                A.u[c] = L.u[c];
+                if (C == 1) {
+                    A.recon[c] = fr;  // gray: the reconstruction IS the output frame
+                    A.prev[c] = frprev;
+                } else {
+                    A.recon[c] = L.ring[fi & 1][c];
+                    A.prev[c] = L.ring[(fi + 1) & 1][c];
+                    A.rgb[c] = fr + c * N;
+                }
             }
-            ctx.launches += launches;
-            ev_end(ev_intra);
+            ResDev& RD = A.res;
+            RD.ngroups = J.res.zero ? 0 : J.res.ngroups;
+            RD.dz_step = 127.0 / (double)((hd.residual_levels - 1) / 2);  // quantize.py:43-47
+            RD.c_scale = J.res.c_scale;
+            RD.a_scale = J.res.a_scale;
+            for (int g = 0; g < RD.ngroups; ++g) {
+                const ResidualGroup& G = J.res.g[g];
+                ResGroupDev& D = RD.g[g];
+                D.nplanes = G.nplanes;
+                D.nblocks = G.nblocks;
+                D.npoints = G.npoints;
+                D.tile_words = at<uint64_t>(dev, o.g[g][0]);
+                D.word_prefix = at<int32_t>(dev, o.g[g][1]);
+                D.block_mask = at<uint64_t>(dev, o.g[g][2]);
+                D.block_off = at<int32_t>(dev, o.g[g][3]);
+                D.c_sym = at<int32_t>(dev, o.g[g][4]);
+                D.a_sym = at<int32_t>(dev, o.g[g][5]);
+            }
+            EvRec e;
+            e.stream = R.stream;
+            e.gop = gi;
+            e.frame = (int)fi;
+            auto ev_begin = [&]() {
+                if (!timed) return;
+                CUDA_CHECK(cudaEventCreate(&e.first));
+                CUDA_CHECK(cudaEventCreate(&e.second));
+                CUDA_CHECK(cudaEventRecord(e.first, s));
+            };
+            auto ev_end = [&](EvPairs& v) {
+                if (!timed) return;
+                CUDA_CHECK(cudaEventRecord(e.second, s));
+                v.push_back(e);
+            };
             ev_begin();
-            launch_frame(A, false, s);
-            ctx.launches += 1;
-            ev_end(ev_ifin);
-        } else {
-            for (int c = 0; c < 2; ++c) {
-                A.flow.nodes[c] = at<int32_t>(dev, o.nodes[c]);
-                A.flow.vals[c] = at<double>(dev, o.fvals[c]);
-                A.flow.tiles[c] = at<uint16_t>(dev, o.ftiles[c]);
+            (J.type == 0 ? R.intra_frames : R.inter_frames) += 1;
+            if (J.type == 0) {
+                // intra: f = 0 with the values scattered at the mask points, then solve (prediction.py:203-208)
+                int64_t launches = 0;
+                for (int c = 0; c < C; ++c) {
+                    int t = c == 0 ? 0 : 1;
+                    const auto& pts = J.intra.pts[t];
+                    CUDA_CHECK(cudaMemsetAsync(L.f[c], 0, N * sizeof(double), s));
+                    if (c <= 1) CUDA_CHECK(cudaMemsetAsync(L.m[t], 0, N, s));
+                    launch_scatter(at<int32_t>(dev, o.pts[t]), at<double>(dev, o.vals[c]), (int)pts.size(), L.f[c],
+                                   c <= 1 ? L.m[t] : nullptr, s);
+                    ++launches;
+                    solve_homogeneous_async(L.ws, s, L.f[c], L.m[t], h, w, 1e-4, 160, L.u[c], &launches,
+                                            timed ? &L.probe : nullptr);
+                    A.u[c] = L.u[c];
+                }
+                ctx.launches += launches;
+                ev_end(ev_intra);
+                ev_begin();
+                launch_frame(A, false, s);
+                ctx.launches += 1;
+                ev_end(ev_ifin);
+            } else {
+                for (int c = 0; c < 2; ++c) {
+                    A.flow.nodes[c] = at<int32_t>(dev, o.nodes[c]);
+                    A.flow.vals[c] = at<double>(dev, o.fvals[c]);
+                    A.flow.tiles[c] = at<uint16_t>(dev, o.ftiles[c]);
+                }
+                launch_frame(A, true, s);
+                ctx.launches += 1;
+                ev_end(ev_inter);
             }
-            launch_frame(A, true, s);
-            ctx.launches += 1;
-            ev_end(ev_inter);
-        }
-        if (!out_on_device) {  // frame fi is final: copy it out while fi+1 decodes
-            cudaEvent_t fe = L.frame_ev[L.frame_ev_next++ % Lane::kFrameEv];
-            CUDA_CHECK(cudaEventRecord(fe, s));
-            CUDA_CHECK(cudaStreamWaitEvent(L.copy, fe, 0));
-            CUDA_CHECK(cudaMemcpyAsync(gop_host + fi * frame_bytes, fr, frame_bytes, cudaMemcpyDeviceToHost, L.copy));
-            R.d2h += (int64_t)frame_bytes;
+            if (!out_on_device) {  // frame fi is final: copy it out while fi+1 decodes
+                cudaEvent_t fe = L.frame_ev[L.frame_ev_next++ % Lane::kFrameEv];
+                CUDA_CHECK(cudaEventRecord(fe, s));
+                CUDA_CHECK(cudaStreamWaitEvent(L.copy, fe, 0));
+                CUDA_CHECK(cudaMemcpyAsync(gop_host + fi * frame_bytes, fr, frame_bytes, cudaMemcpyDeviceToHost, L.copy));
+                R.d2h += (int64_t)frame_bytes;
+            }
         }
     }
     if (!out_on_device) CUDA_CHECK(cudaEventRecord(L.out_free[slot], L.copy));
@@ -431,7 +480,8 @@ void decode_gop(Context& ctx, Lane& L, const StreamJob& S, int gi, bool out_on_d
 }
 
 void run_lane(Context& ctx, Lane& L, const std::vector<StreamJob>& streams, const std::vector<WorkItem>& items,
-              bool out_on_device, bool timed, cudaEvent_t origin, cudaEvent_t done, LaneResult& R) {
+              std::atomic<size_t>& next_item, bool out_on_device, bool timed, cudaEvent_t origin, cudaEvent_t done,
+              LaneResult& R) {
     std::vector<FrameJob> jobs;
     std::vector<uint64_t> bits;
     EvPairs ev_intra, ev_inter, ev_ifin;
@@ -439,19 +489,23 @@ void run_lane(Context& ctx, Lane& L, const std::vector<StreamJob>& streams, cons
     try {
         CUDA_CHECK(cudaSetDevice(L.device));
         CUDA_CHECK(cudaStreamWaitEvent(L.stream, origin, 0));
-        for (const WorkItem& it : items) {
+        bool any = false;
+        for (size_t i; (i = next_item.fetch_add(1)) < items.size();) {  // largest planes first, first free lane
+            const WorkItem& it = items[i];
+            any = true;
             R.stream = it.stream;
             R.gop = it.gop;
             decode_gop(ctx, L, streams[it.stream], it.gop, out_on_device, timed, R, jobs, bits, slot, ev_intra,
                        ev_inter, ev_ifin);
         }
-        if (!out_on_device && !items.empty())  // the span ends with the last D2H copy
+        if (!out_on_device && any)  // the span ends with the last D2H copy
             CUDA_CHECK(cudaStreamWaitEvent(L.stream, L.out_free[slot ^ 1], 0));
         CUDA_CHECK(cudaEventRecord(done, L.stream));
         CUDA_CHECK(cudaStreamSynchronize(L.stream));
-        R.gpu_intra = drain(ev_intra);
-        R.gpu_inter = drain(ev_inter);
-        R.gpu_ifinal = drain(ev_ifin);
+        std::string* tl = std::getenv("HIVC_TIMELINE") ? &R.timeline : nullptr;
+        R.gpu_intra = drain(ev_intra, origin, 'I', tl);
+        R.gpu_inter = drain(ev_inter, origin, 'P', tl);
+        R.gpu_ifinal = drain(ev_ifin, origin, 'F', tl);
         L.probe.harvest(R.cg);
     } catch (const Error& e) {
         R.code = e.code;
@@ -521,11 +575,13 @@ void decode_streams(Context& ctx, int nstreams, const uint8_t* const* data, cons
         L.reserve_planes(max_h, max_w, max_c);
         L.ws.reserve(max_h, max_w, ctx.device);
         if (!out_on_device) L.reserve_gop_out(max_gop_bytes);
+        // staging sized up front (an I-frame of a typical mask fits), so a lane
+        // meeting its first large chunk does not reallocate (cudaFree syncs the device)
+        for (int b = 0; b < Lane::kStage; ++b) L.reserve_stage(b, (size_t)2 * max_h * max_w * max_c + 65536);
     }
-    std::vector<std::vector<WorkItem>> assign(nlanes);
-    for (size_t i = 0; i < items.size(); ++i) assign[i % nlanes].push_back(items[i]);
+    std::atomic<size_t> next_item{0};
     std::vector<LaneResult> res(nlanes);
-    const bool timed = stage_seconds != nullptr && ctx.stage_events;
+    const bool timed = (stage_seconds != nullptr && ctx.stage_events) || std::getenv("HIVC_TIMELINE");
     // device-side span: every lane waits on `origin`, records `done[l]` after its last copy
     cudaEvent_t origin;
     CUDA_CHECK(cudaEventCreate(&origin));
@@ -533,12 +589,12 @@ void decode_streams(Context& ctx, int nstreams, const uint8_t* const* data, cons
     for (auto& e : done) CUDA_CHECK(cudaEventCreate(&e));
     CUDA_CHECK(cudaEventRecord(origin, ctx.stream));
     if (nlanes == 1) {
-        run_lane(ctx, *ctx.lanes[0], streams, assign[0], out_on_device, timed, origin, done[0], res[0]);
+        run_lane(ctx, *ctx.lanes[0], streams, items, next_item, out_on_device, timed, origin, done[0], res[0]);
     } else {
         std::vector<std::thread> th;
         for (int l = 0; l < nlanes; ++l)
-            th.emplace_back(run_lane, std::ref(ctx), std::ref(*ctx.lanes[l]), std::cref(streams), std::cref(assign[l]),
-                            out_on_device, timed, origin, done[l], std::ref(res[l]));
+            th.emplace_back(run_lane, std::ref(ctx), std::ref(*ctx.lanes[l]), std::cref(streams), std::cref(items),
+                            std::ref(next_item), out_on_device, timed, origin, done[l], std::ref(res[l]));
         for (auto& t : th) t.join();
     }
     double span = 0;
@@ -566,6 +622,21 @@ void decode_streams(Context& ctx, int nstreams, const uint8_t* const* data, cons
             if (total != (size_t)S.hd.frame_count)
                 fail(HIVC_E_CODEC, "decoded " + std::to_string(total) + " frames, header promised " +
                                        std::to_string(S.hd.frame_count));
+        }
+    }
+    if (const char* tl = std::getenv("HIVC_TIMELINE")) {  // debug: append lane,kind,stream,gop,frame,t0,t1
+        if (FILE* f = std::fopen(tl, "a")) {
+            for (int l = 0; l < nlanes; ++l) {
+                size_t a = 0;
+                const std::string& t = res[l].timeline;
+                while (a < t.size()) {
+                    size_t b = t.find('\n', a);
+                    std::fprintf(f, "%d,%s\n", l, t.substr(a, b - a).c_str());
+                    a = b + 1;
+                }
+            }
+            std::fprintf(f, "-\n");
+            std::fclose(f);
         }
     }
     for (auto& r : res) {

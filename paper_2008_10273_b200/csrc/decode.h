@@ -27,10 +27,13 @@ struct Lane {
     uint8_t* m[2] = {nullptr, nullptr};
     double* u[3] = {nullptr, nullptr, nullptr};
     int16_t* ring[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
-    uint8_t* host_stage[2] = {nullptr, nullptr};
-    uint8_t* dev_stage[2] = {nullptr, nullptr};
-    size_t stage_cap[2] = {0, 0};
-    cudaEvent_t staged[2] = {nullptr, nullptr};
+    // ring of pinned staging buffers: one per shipped chunk of frame descriptions
+    static constexpr int kStage = 4;
+    uint8_t* host_stage[kStage] = {};
+    uint8_t* dev_stage[kStage] = {};
+    size_t stage_cap[kStage] = {};
+    cudaEvent_t staged[kStage] = {};
+    int stage_next = 0;
     uint8_t* gop_out[2] = {nullptr, nullptr};  // device frame buffers when output goes to the host
     size_t gop_out_cap = 0;
     // host output: each finished frame is copied D2H on `copy` while the lane
