@@ -24,6 +24,7 @@
 constexpr int kBandThreads = 512;
 constexpr int kBandCols = 4;  // column slots per thread: w <= 2048
 constexpr int kBandRows = 8;  // rows per band
+constexpr int kPackRows = 16; // rows per band in throughput mode (w <= 1024)
 constexpr int kBandPx = kBandCols * kBandRows;
 constexpr int kSetupCtas = 296;
 

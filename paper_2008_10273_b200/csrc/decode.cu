@@ -562,7 +562,11 @@ void decode_streams(Context& ctx, int nstreams, const uint8_t* const* data, cons
         const StreamHeader &ha = streams[a.stream].hd, &hb = streams[b.stream].hd;
         return (int64_t)ha.height * ha.width * ha.channels > (int64_t)hb.height * hb.width * hb.channels;
     });
-    int nlanes = std::max(1, std::min((int)items.size(), 8));
+    static const int kMaxLanes = [] {
+        const char* e = std::getenv("HIVC_LANES");
+        return e ? std::max(1, std::min(32, std::atoi(e))) : 8;
+    }();
+    int nlanes = std::max(1, std::min((int)items.size(), kMaxLanes));
     CUDA_CHECK(cudaSetDevice(ctx.device));
     while ((int)ctx.lanes.size() < nlanes) {
         auto L = std::make_unique<Lane>();
@@ -574,6 +578,7 @@ void decode_streams(Context& ctx, int nstreams, const uint8_t* const* data, cons
         Lane& L = *ctx.lanes[l];
         L.reserve_planes(max_h, max_w, max_c);
         L.ws.reserve(max_h, max_w, ctx.device);
+        L.ws.pack_bands = true;  // lanes solve side by side: throughput mode
         if (!out_on_device) L.reserve_gop_out(max_gop_bytes);
         // staging sized up front (an I-frame of a typical mask fits), so a lane
         // meeting its first large chunk does not reallocate (cudaFree syncs the device)

@@ -374,6 +374,10 @@ void InpaintWorkspace::reserve(int h, int w, int dev) {
     band_variant = (env && env[0] == '1') ? 1 : 2;
     CUDA_CHECK(cudaFuncSetAttribute(cg_band2_kernel<4, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     CUDA_CHECK(cudaFuncSetAttribute(cg_band2_kernel<8, 4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    CUDA_CHECK(cudaFuncSetAttribute(cg_band2_kernel<kPackRows, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    220 * 1024));
+    const char* env_pack = getenv("HIVC_CG_PACK");
+    pack_env_off = env_pack && env_pack[0] == '0';
     const char* env_small = getenv("HIVC_CG_SMALL");
     small_enabled = !(env_small && env_small[0] == '0');
     CUDA_CHECK(cudaFuncSetAttribute(cg_band_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
@@ -566,10 +570,13 @@ int solve_homogeneous_async(InpaintWorkspace& ws, cudaStream_t s, const double* 
             CUDA_CHECK(cudaEventRecord(rec.start, s));
         }
         // on-chip band kernel when a band fits registers + shared memory
-        const int band_rows = (P.h + ws.num_sms - 1) / std::max(ws.num_sms, 1);
+        const int kc = (P.w + kBandThreads - 1) / kBandThreads;
+        int band_rows = (P.h + ws.num_sms - 1) / std::max(ws.num_sms, 1);
+        const bool pack = ws.pack_bands && !ws.pack_env_off && ws.band_variant == 2 && kc <= 2 && band_rows <= kPackRows;
+        if (pack) band_rows = kPackRows;
         const int nbands = (P.h + band_rows - 1) / band_rows;
         const size_t band_smem = (size_t)(kBandRows + 2) * (P.w + 2) * sizeof(double) + (size_t)kBandRows * P.w;
-        const bool band = grid && ws.band_enabled && P.uc != nullptr && band_rows <= kBandRows &&
+        const bool band = grid && ws.band_enabled && P.uc != nullptr && (pack || band_rows <= kBandRows) &&
                           P.w <= kBandCols * kBandThreads && band_smem <= 220 * 1024 && nbands <= ws.num_sms;
         if (grid) CUDA_CHECK(cudaMemsetAsync(ws.bar, 0, sizeof(unsigned int), s));  // barrier epoch counter
         if (probe && grid) P.stamp = probe->stamp_slot((int)probe->launches.size());
@@ -589,10 +596,12 @@ int solve_homogeneous_async(InpaintWorkspace& ws, cudaStream_t s, const double* 
             cg_setup_kernel<<<kSetupCtas, 512, 0, s>>>(P, setup);
             *launches += 2;
             void* args[] = {&P, &setup};
-            const int kc = (P.w + kBandThreads - 1) / kBandThreads;
             const void* fn = (const void*)cg_band_kernel;
             size_t smem_b = band_smem;
-            if (ws.band_variant == 2) {
+            if (pack) {
+                smem_b = (size_t)(kPackRows + 2) * (P.w + 2) * sizeof(double);
+                fn = (const void*)cg_band2_kernel<kPackRows, 2, false>;
+            } else if (ws.band_variant == 2) {
                 smem_b = (size_t)(kBandRows + 2) * (P.w + 2) * sizeof(double);
                 fn = (band_rows <= 4 && kc <= 2) ? (const void*)cg_band2_kernel<4, 2, true>
                                                  : (const void*)cg_band2_kernel<8, 4, false>;
