@@ -27,19 +27,44 @@ constexpr int kBandRows = 8;  // rows per band
 constexpr int kPackRows = 16; // rows per band in throughput mode (w <= 1024)
 constexpr int kBandPx = kBandCols * kBandRows;
 constexpr int kSetupCtas = 296;
+constexpr int kBand2Smem = 224 * 1024;  // band2 dynamic smem cap (+ 2.1 KB static <= the 227 KB opt-in limit)
+
+// A batch of same-shape level solves (kernel parameter, __grid_constant__).
+// ticket != nullptr: CTAs take (solve, band) = divmod(ticket, nb) in the order
+// they start, so the CTAs of a solve are resident together as long as nb
+// CTAs fit the GPU (the first solves finish and free SMs for the rest); the
+// batch never runs concurrently with another spinning launch (one solver stream).
+struct BandBatch {
+    CgParams P[kMaxBatch];
+    const double* setup[kMaxBatch];
+    int nb;
+    unsigned int* ticket;
+};
+struct SetupBatch {
+    CgParams P[kMaxBatch];
+    double* partials[kMaxBatch];
+    unsigned int* ticket;  // reset with the solves' barrier counters (nullable)
+};
 
 // Setup for the band kernel: x = x0*interior, r = b - A x (global), and the
 // per-CTA partials of r.r, b.b, |f_mask|^2, #interior (homogeneous.py:64-77).
 // setup pass 1: x = x0 * interior, x0 prolonged from the coarser level (homogeneous.py:71)
-__global__ void __launch_bounds__(512) cg_setup_x_kernel(CgParams P) {
+__global__ void __launch_bounds__(512) cg_setup_x_kernel(const __grid_constant__ SetupBatch B) {
+    const CgParams& P = B.P[blockIdx.y];
     const int w = P.w, n = P.n;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {  // the band launch that follows starts a fresh barrier epoch
+        P.bar[0] = 0;
+        if (blockIdx.y == 0 && B.ticket) *B.ticket = 0;
+    }
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
         P.x[i] = prolong_at(P, i / w, i % w) * (P.m[i] ? 0.0 : 1.0);
 }
 
 // setup pass 2: b = L(u_D) * interior, r = b - A x and the level partials
-__global__ void __launch_bounds__(512) cg_setup_kernel(CgParams P, double* partials) {
+__global__ void __launch_bounds__(512) cg_setup_kernel(const __grid_constant__ SetupBatch B) {
     __shared__ double sh[4 * 32];
+    const CgParams& P = B.P[blockIdx.y];
+    double* partials = B.partials[blockIdx.y];
     const int h = P.h, w = P.w, n = P.n;
     const double* __restrict__ f = P.f;
     const uint8_t* __restrict__ m = P.m;

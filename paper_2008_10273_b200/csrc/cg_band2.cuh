@@ -12,13 +12,22 @@
 #pragma once
 
 template <int ROWS, int KC, bool STORE_AP>
-__global__ void __launch_bounds__(kBandThreads, 1) cg_band2_kernel(CgParams P, const double* __restrict__ setup) {
+__global__ void __launch_bounds__(kBandThreads, 1) cg_band2_kernel(const __grid_constant__ BandBatch B) {
     static_assert(ROWS * KC <= 32, "mask bits");
     extern __shared__ double sp[];  // (ROWS + 2) x (w + 2)
     __shared__ double sh[2 * 4 * 32 + 8];
+    __shared__ int s_ticket;
+    int t = blockIdx.x;
+    if (B.ticket) {
+        if (threadIdx.x == 0) s_ticket = (int)atomicAdd(B.ticket, 1u);
+        __syncthreads();
+        t = s_ticket;
+    }
+    const int nb = B.nb, band = t % nb;
+    const CgParams& P = B.P[t / nb];
+    const double* __restrict__ setup = B.setup[t / nb];
     RedState red;
     const int h = P.h, w = P.w, W2 = w + 2;
-    const int band = blockIdx.x, nb = gridDim.x;
     const int y0 = band * P.band_rows;
     const int rows = min(P.band_rows, h - y0);
     const int tid = threadIdx.x;
@@ -42,6 +51,10 @@ __global__ void __launch_bounds__(kBandThreads, 1) cg_band2_kernel(CgParams P, c
     const double bn = (P.finest && sh[64] != 0.0) ? sqrt(sh[64]) : sqrt(sh[32]);
     __syncthreads();
 
+    // resident x rows behind the padded p
+    double* sx = sp + (size_t)(ROWS + 2) * W2;
+    const int xr = min(P.x_rows, rows);
+    for (int i = tid; i < xr * w; i += kBandThreads) sx[i] = __ldcg(P.x + (size_t)y0 * w + i);
     // ---- r into registers (index row * KC + k), mask bits, p = 0
     double r[ROWS * KC];
     double ap[STORE_AP ? ROWS * KC : 1];
@@ -139,7 +152,7 @@ __global__ void __launch_bounds__(kBandThreads, 1) cg_band2_kernel(CgParams P, c
             }
             HIVC_TRACE(2);
             if (P.trace && tid == 0 && k < 256) P.trace[2048 + k * 160 + band] = globaltimer_ns();  // arrival spread
-            grid_reduce<1>(d, sh, P, red);
+            grid_reduce<1>(d, sh, P, red, band, nb);
             HIVC_TRACE(3);
             const double pap = d[0];
             if (pap <= 0.0 || rs < 1e-300) break;
@@ -165,9 +178,6 @@ __global__ void __launch_bounds__(kBandThreads, 1) cg_band2_kernel(CgParams P, c
                         const double lap = (((cur * -4.0 + up) + dn) + q[-1]) + q[1];
                         api = -lap * (((mbits >> (row * KC + k2)) & 1u) ? 0.0 : 1.0);
                     }
-                    const double pi = STORE_AP ? q[0] : cur;
-                    const size_t gi = (size_t)(y0 + row) * w + c;
-                    P.x[gi] = P.x[gi] + alpha * pi;
                     double& rr = r[row * KC + k2];
                     rr = rr - alpha * api;
                     e1[0] += rr * rr;
@@ -180,7 +190,26 @@ __global__ void __launch_bounds__(kBandThreads, 1) cg_band2_kernel(CgParams P, c
                 }
             }
             HIVC_TRACE(4);
-            grid_reduce<1>(e1, sh, P, red);
+            grid_reduce_arrive<1>(e1, sh, P, red, band);
+            // x += alpha p while the other CTAs arrive (x is not read until the level ends)
+#pragma unroll
+            for (int k2 = 0; k2 < KC; ++k2) {
+                const int c = tid + kBandThreads * k2;
+                if (c >= w) continue;
+#pragma unroll
+                for (int row = 0; row < ROWS; ++row) {
+                    if (row >= rows) break;
+                    const double pi = sp[(row + 1) * W2 + c + 1];
+                    if (row < xr) {
+                        double& xs = sx[row * w + c];
+                        xs = xs + alpha * pi;
+                    } else {
+                        const size_t gi = (size_t)(y0 + row) * w + c;
+                        P.x[gi] = P.x[gi] + alpha * pi;
+                    }
+                }
+            }
+            grid_reduce_finish<1>(e1, sh, P, red, nb);
             HIVC_TRACE(5);
             const double rs1 = e1[0];
             const double lhs = sqrt(rs1), rhs = P.tol * bn;
@@ -195,7 +224,8 @@ __global__ void __launch_bounds__(kBandThreads, 1) cg_band2_kernel(CgParams P, c
         for (int c = tid; c < w; c += kBandThreads) {
             const size_t gi = (size_t)(y0 + row) * w + c;
             const bool mi = m[gi] != 0;
-            P.u[gi] = all_mask ? __ldg(f + gi) : (mi ? __ldg(f + gi) : 0.0) + P.x[gi];
+            const double xv = row < xr ? sx[row * w + c] : P.x[gi];
+            P.u[gi] = all_mask ? __ldg(f + gi) : (mi ? __ldg(f + gi) : 0.0) + xv;
         }
     if (band == 0 && tid == 0) {
         *P.iters = it;

@@ -35,9 +35,14 @@ struct ClusterLevels {
     unsigned long long* trace;  // HIVC_CG_TRACE diagnostics (finest cluster level, rank 0)
 };
 
+struct ClusterBatch {  // one cluster per solve (blockIdx.x / kClusterSize)
+    ClusterLevels S[kMaxBatch];
+};
+
 namespace cgc = cooperative_groups;
 
-__global__ void __launch_bounds__(kClThreads, 1) cg_cluster_kernel(ClusterLevels S) {
+__global__ void __launch_bounds__(kClThreads, 1) cg_cluster_kernel(const __grid_constant__ ClusterBatch CB) {
+    const ClusterLevels& S = CB.S[blockIdx.x / kClusterSize];
     extern __shared__ double smem_cl[];
     __shared__ double sh[2 * 4 * 32];
     __shared__ double red[2][4];     // this CTA's partials (double-buffered)

@@ -11,11 +11,17 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <condition_variable>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <deque>
 #include <mutex>
 #include <thread>
+
+#include <sys/resource.h>
+#include <sys/syscall.h>
+#include <unistd.h>
 
 #include "decode.h"
 
@@ -33,12 +39,6 @@ inline uint32_t rd_u32(const uint8_t* p) {
     return v;
 }
 
-struct FrameJob {
-    int type = 0;  // 0 intra, 1 inter
-    IntraJob intra;
-    FlowJob flow;
-    ResidualJob res;
-};
 
 struct HostTimes {
     double intra_parse = 0, flow_parse = 0, residual_parse = 0;
@@ -155,11 +155,24 @@ const T* at(const uint8_t* base, size_t off) {
 
 }  // namespace
 
-// ---------------------------------------------------------------- lanes
+// ---------------------------------------------------------------- slots
 
-void Lane::reserve_planes(int h, int w, int channels) {
+void Slot::init(int dev) {
+    if (stream) return;
+    device = dev;
+    CUDA_CHECK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    CUDA_CHECK(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking));
+    for (auto& e : frame_ev) CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CUDA_CHECK(cudaEventCreateWithFlags(&out_free, cudaEventDisableTiming));
+    CUDA_CHECK(cudaEventCreateWithFlags(&intra_ready, cudaEventDisableTiming));
+    CUDA_CHECK(cudaEventCreateWithFlags(&intra_done, cudaEventDisableTiming));
+    ws.pack_bands = true;  // batched solves run side by side: throughput mode
+}
+
+void Slot::reserve_planes(int h, int w, int channels) {
     size_t n = (size_t)h * w;
     if (n <= plane_px && channels <= chans) return;
+    CUDA_CHECK(cudaStreamSynchronize(stream));
     for (int c = 0; c < 3; ++c) {
         if (f[c]) cudaFree(f[c]);
         if (u[c]) cudaFree(u[c]);
@@ -184,32 +197,50 @@ void Lane::reserve_planes(int h, int w, int channels) {
     chans = channels;
 }
 
-void Lane::reserve_stage(int slot, size_t bytes) {
-    if (bytes <= stage_cap[slot]) return;
-    if (host_stage[slot]) cudaFreeHost(host_stage[slot]);
-    if (dev_stage[slot]) cudaFree(dev_stage[slot]);
-    size_t cap = bytes + bytes / 4 + 4096;
-    CUDA_CHECK(cudaHostAlloc(&host_stage[slot], cap, cudaHostAllocDefault));
-    CUDA_CHECK(cudaMalloc(&dev_stage[slot], cap));
-    stage_cap[slot] = cap;
+void Slot::stage_begin_call(size_t min_bytes) {
+    // the previous call has synchronised: consolidate into one block
+    size_t want = std::max(min_bytes, stage_used + stage_used / 4);
+    if (stage.size() != 1 || stage[0].cap < want) {
+        for (auto& b : stage) {
+            if (b.host) cudaFreeHost(b.host);
+            if (b.dev) cudaFree(b.dev);
+        }
+        stage.clear();
+        StageBlock b;
+        b.cap = std::max(want, (size_t)1 << 20);
+        CUDA_CHECK(cudaHostAlloc(&b.host, b.cap, cudaHostAllocDefault));
+        CUDA_CHECK(cudaMalloc(&b.dev, b.cap));
+        stage.push_back(b);
+    }
+    stage_off = 0;
+    stage_used = 0;
 }
 
-void Lane::reserve_gop_out(size_t bytes) {
-    if (!copy) {
-        CUDA_CHECK(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking));
-        for (auto& e : frame_ev) CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        for (auto& e : out_free) CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+void Slot::stage_alloc(size_t bytes, uint8_t*& host, uint8_t*& dev) {
+    bytes = (bytes + 255) & ~size_t(255);
+    if (stage.empty() || stage_off + bytes > stage.back().cap) {  // chain a block (no wait, no free mid-call)
+        StageBlock b;
+        b.cap = std::max(bytes, stage.empty() ? (size_t)1 << 20 : 2 * stage.back().cap);
+        CUDA_CHECK(cudaHostAlloc(&b.host, b.cap, cudaHostAllocDefault));
+        CUDA_CHECK(cudaMalloc(&b.dev, b.cap));
+        stage.push_back(b);
+        stage_off = 0;
     }
+    host = stage.back().host + stage_off;
+    dev = stage.back().dev + stage_off;
+    stage_off += bytes;
+    stage_used += bytes;
+}
+
+void Slot::reserve_gop_out(size_t bytes) {
     if (bytes <= gop_out_cap) return;
     CUDA_CHECK(cudaStreamSynchronize(copy));
-    for (int k = 0; k < 2; ++k) {
-        if (gop_out[k]) cudaFree(gop_out[k]);
-        CUDA_CHECK(cudaMalloc(&gop_out[k], bytes));
-    }
+    if (gop_out) cudaFree(gop_out);
+    CUDA_CHECK(cudaMalloc(&gop_out, bytes));
     gop_out_cap = bytes;
 }
 
-Lane::~Lane() {
+Slot::~Slot() {
     if (stream) cudaStreamSynchronize(stream);
     if (copy) cudaStreamSynchronize(copy);
     for (int c = 0; c < 3; ++c) {
@@ -218,28 +249,29 @@ Lane::~Lane() {
         for (int k = 0; k < 2; ++k)
             if (ring[k][c]) cudaFree(ring[k][c]);
     }
-    for (int t = 0; t < 2; ++t) {
+    for (int t = 0; t < 2; ++t)
         if (m[t]) cudaFree(m[t]);
-        if (gop_out[t]) cudaFree(gop_out[t]);
+    if (gop_out) cudaFree(gop_out);
+    for (auto& b : stage) {
+        if (b.host) cudaFreeHost(b.host);
+        if (b.dev) cudaFree(b.dev);
     }
-    for (int t = 0; t < kStage; ++t) {
-        if (host_stage[t]) cudaFreeHost(host_stage[t]);
-        if (dev_stage[t]) cudaFree(dev_stage[t]);
-        if (staged[t]) cudaEventDestroy(staged[t]);
-    }
-    if (copy) cudaStreamSynchronize(copy);
     for (auto& e : frame_ev)
         if (e) cudaEventDestroy(e);
-    for (auto& e : out_free)
+    for (cudaEvent_t e : {out_free, intra_ready, intra_done})
         if (e) cudaEventDestroy(e);
     if (copy) cudaStreamDestroy(copy);
     if (stream) cudaStreamDestroy(stream);
 }
 
 Context::~Context() {
-    lanes.clear();
+    slots.clear();
+    probe.reset();
     if (d_status) cudaFree(d_status);
     if (op_hi) cudaFree(op_hi);
+    if (solver) cudaStreamDestroy(solver);
+    for (cudaStream_t p : pre)
+        if (p) cudaStreamDestroy(p);
     if (stream) cudaStreamDestroy(stream);
 }
 
@@ -300,29 +332,13 @@ struct StreamJob {
     int gop_begin = 0, gop_end = 0;
 };
 
-struct WorkItem {
-    int stream, gop;
-};
-
-struct LaneResult {
-    int code = HIVC_OK;
-    int stream = -1, gop = -1;
-    std::string msg;
-    HostTimes ht;
-    double gpu_intra = 0, gpu_inter = 0, gpu_ifinal = 0;
-    int64_t h2d = 0, d2h = 0;
-    int64_t inter_frames = 0, intra_frames = 0;
-    CgTotals cg;
-    std::string timeline;  // HIVC_TIMELINE rows: kind,stream,gop,frame,t0_us,t1_us (from the decode origin)
-};
-
 struct EvRec {
     cudaEvent_t first = nullptr, second = nullptr;
     int stream = 0, gop = 0, frame = 0;
 };
 using EvPairs = std::vector<EvRec>;
 
-double drain(EvPairs& v, cudaEvent_t origin, char kind, std::string* timeline) {
+double drain(EvPairs& v, cudaEvent_t origin, char kind, int lane, std::string* timeline) {
     double t = 0;
     for (auto& e : v) {
         float ms = 0;
@@ -332,8 +348,9 @@ double drain(EvPairs& v, cudaEvent_t origin, char kind, std::string* timeline) {
             float a = 0, b = 0;
             cudaEventElapsedTime(&a, origin, e.first);
             cudaEventElapsedTime(&b, origin, e.second);
-            char line[128];
-            std::snprintf(line, sizeof line, "%c,%d,%d,%d,%.1f,%.1f\n", kind, e.stream, e.gop, e.frame, a * 1e3, b * 1e3);
+            char line[160];
+            std::snprintf(line, sizeof line, "%d,%c,%d,%d,%d,%.1f,%.1f\n", lane, kind, e.stream, e.gop, e.frame,
+                          a * 1e3, b * 1e3);
             *timeline += line;
         }
         cudaEventDestroy(e.first);
@@ -343,183 +360,340 @@ double drain(EvPairs& v, cudaEvent_t origin, char kind, std::string* timeline) {
     return t;
 }
 
-void decode_gop(Context& ctx, Lane& L, const StreamJob& S, int gi, bool out_on_device, bool timed, LaneResult& R,
-                std::vector<FrameJob>& jobs, std::vector<uint64_t>& bits, int& slot, EvPairs& ev_intra,
-                EvPairs& ev_inter, EvPairs& ev_ifin) {
-    const StreamHeader& hd = S.hd;
-    const int h = hd.height, w = hd.width, C = hd.channels;
-    const size_t N = (size_t)h * w;
-    const size_t frame_bytes = N * C;
-    GopCursor cur(S.data + S.gops[gi].first, S.gops[gi].second, hd, gi);
-    const int nf = cur.nframes;
-    if ((int)jobs.size() < nf) jobs.resize(nf);
-    cudaStream_t s = L.stream;
-    uint8_t* gop_dev = out_on_device ? S.out + S.frame_base[gi] * frame_bytes : L.gop_out[slot];
-    uint8_t* gop_host = out_on_device ? nullptr : S.out + S.frame_base[gi] * frame_bytes;
-    if (!out_on_device) CUDA_CHECK(cudaStreamWaitEvent(s, L.out_free[slot], 0));  // copies out of this slot done
-    // Parse and ship in chunks: the I-frame alone, so its solve runs while the
-    // host parses the P frames, then kChunk P frames at a time.
-    constexpr int kChunk = 2;
-    FrameOffsets offs[kChunk];
-    size_t fi = 0;
-    while ((int)fi < nf) {
-        const int cnt = fi == 0 ? 1 : std::min(kChunk, nf - (int)fi);
-        for (int k = 0; k < cnt; ++k) cur.parse(jobs[fi + k], R.ht, bits);
-        if ((int)fi + cnt == nf) cur.finish();
-        // pack the compact frame descriptions: measure, then write into pinned staging
-        Packer pk;
-        for (int k = 0; k < cnt; ++k) pack_frame(pk, jobs[fi + k], offs[k]);
-        const int b = L.stage_next++ % Lane::kStage;
-        if (L.staged[b]) CUDA_CHECK(cudaEventSynchronize(L.staged[b]));
-        L.reserve_stage(b, pk.off + 16);
-        pk.base = L.host_stage[b];
-        pk.off = 0;
-        pk.measure = false;
-        for (int k = 0; k < cnt; ++k) pack_frame(pk, jobs[fi + k], offs[k]);
-        CUDA_CHECK(cudaMemcpyAsync(L.dev_stage[b], L.host_stage[b], pk.off, cudaMemcpyHostToDevice, s));
-        R.h2d += (int64_t)pk.off;
-        if (!L.staged[b]) CUDA_CHECK(cudaEventCreateWithFlags(&L.staged[b], cudaEventDisableTiming));
-        CUDA_CHECK(cudaEventRecord(L.staged[b], s));
-        const uint8_t* dev = L.dev_stage[b];
-        for (int k = 0; k < cnt; ++k, ++fi) {
-            const FrameJob& J = jobs[fi];
-            const FrameOffsets& o = offs[k];
-            FrameArgs A;
-            A.h = h;
-            A.w = w;
-            A.channels = C;
-            uint8_t* fr = gop_dev + fi * frame_bytes;
-            uint8_t* frprev = fi ? gop_dev + (fi - 1) * frame_bytes : nullptr;
-            for (int c = 0; c < C; ++c) {
-                if (C == 1) {
-                    A.recon[c] = fr;  // gray: the reconstruction IS the output frame
-                    A.prev[c] = frprev;
-                } else {
-                    A.recon[c] = L.ring[fi & 1][c];
-                    A.prev[c] = L.ring[(fi + 1) & 1][c];
-                    A.rgb[c] = fr + c * N;
-                }
-            }
-            ResDev& RD = A.res;
-            RD.ngroups = J.res.zero ? 0 : J.res.ngroups;
-            RD.dz_step = 127.0 / (double)((hd.residual_levels - 1) / 2);  // quantize.py:43-47
-            RD.c_scale = J.res.c_scale;
-            RD.a_scale = J.res.a_scale;
-            for (int g = 0; g < RD.ngroups; ++g) {
-                const ResidualGroup& G = J.res.g[g];
-                ResGroupDev& D = RD.g[g];
-                D.nplanes = G.nplanes;
-                D.nblocks = G.nblocks;
-                D.npoints = G.npoints;
-                D.tile_words = at<uint64_t>(dev, o.g[g][0]);
-                D.word_prefix = at<int32_t>(dev, o.g[g][1]);
-                D.block_mask = at<uint64_t>(dev, o.g[g][2]);
-                D.block_off = at<int32_t>(dev, o.g[g][3]);
-                D.c_sym = at<int32_t>(dev, o.g[g][4]);
-                D.a_sym = at<int32_t>(dev, o.g[g][5]);
-            }
-            EvRec e;
-            e.stream = R.stream;
-            e.gop = gi;
-            e.frame = (int)fi;
-            auto ev_begin = [&]() {
-                if (!timed) return;
-                CUDA_CHECK(cudaEventCreate(&e.first));
-                CUDA_CHECK(cudaEventCreate(&e.second));
-                CUDA_CHECK(cudaEventRecord(e.first, s));
-            };
-            auto ev_end = [&](EvPairs& v) {
-                if (!timed) return;
-                CUDA_CHECK(cudaEventRecord(e.second, s));
-                v.push_back(e);
-            };
-            ev_begin();
-            (J.type == 0 ? R.intra_frames : R.inter_frames) += 1;
-            if (J.type == 0) {
-                // intra: f = 0 with the values scattered at the mask points, then solve (prediction.py:203-208)
-                int64_t launches = 0;
-                for (int c = 0; c < C; ++c) {
-                    int t = c == 0 ? 0 : 1;
-                    const auto& pts = J.intra.pts[t];
-                    CUDA_CHECK(cudaMemsetAsync(L.f[c], 0, N * sizeof(double), s));
-                    if (c <= 1) CUDA_CHECK(cudaMemsetAsync(L.m[t], 0, N, s));
-                    launch_scatter(at<int32_t>(dev, o.pts[t]), at<double>(dev, o.vals[c]), (int)pts.size(), L.f[c],
-                                   c <= 1 ? L.m[t] : nullptr, s);
-                    ++launches;
-                    solve_homogeneous_async(L.ws, s, L.f[c], L.m[t], h, w, 1e-4, 160, L.u[c], &launches,
-                                            timed ? &L.probe : nullptr);
-                    A.u[c] = L.u[c];
-                }
-                ctx.launches += launches;
-                ev_end(ev_intra);
-                ev_begin();
-                launch_frame(A, false, s);
-                ctx.launches += 1;
-                ev_end(ev_ifin);
-            } else {
-                for (int c = 0; c < 2; ++c) {
-                    A.flow.nodes[c] = at<int32_t>(dev, o.nodes[c]);
-                    A.flow.vals[c] = at<double>(dev, o.fvals[c]);
-                    A.flow.tiles[c] = at<uint16_t>(dev, o.ftiles[c]);
-                }
-                launch_frame(A, true, s);
-                ctx.launches += 1;
-                ev_end(ev_inter);
-            }
-            if (!out_on_device) {  // frame fi is final: copy it out while fi+1 decodes
-                cudaEvent_t fe = L.frame_ev[L.frame_ev_next++ % Lane::kFrameEv];
-                CUDA_CHECK(cudaEventRecord(fe, s));
-                CUDA_CHECK(cudaStreamWaitEvent(L.copy, fe, 0));
-                CUDA_CHECK(cudaMemcpyAsync(gop_host + fi * frame_bytes, fr, frame_bytes, cudaMemcpyDeviceToHost, L.copy));
-                R.d2h += (int64_t)frame_bytes;
-            }
-        }
+// One (stream, GOP) of a decode call.
+struct Item {
+    int stream = 0, gop = 0, group = 0;
+    Slot* slot = nullptr;
+    std::unique_ptr<GopCursor> cur;
+    int nf = 0;
+    FrameArgs a0;  // I-frame finalize (frame 0)
+    uint8_t* gop_dev = nullptr;
+    uint8_t* gop_host = nullptr;
+    bool solve0 = false;  // frame 0 staged and waiting for the batched solve
+    int code = HIVC_OK;
+    std::string msg;
+    HostTimes ht;
+    int64_t h2d = 0, d2h = 0, inter_frames = 0, intra_frames = 0;
+    EvPairs ev_inter, ev_intra, ev_ifin;
+    cudaEvent_t done = nullptr;
+    double h_i0 = 0, h_i1 = 0, h_issue = 0, h_p0 = 0, h_p1 = 0;  // host timeline (HIVC_TIMELINE)
+};
+
+// Same-shape items whose I-frame solves are issued as batches.
+struct Group {
+    int h = 0, w = 0, c = 0;
+    std::vector<int> items;
+    std::atomic<int> pending{0};
+    bool issued = false;  // under Shared::mu
+};
+
+struct Shared {
+    std::mutex mu;
+    std::condition_variable cv;
+};
+
+void fail_item(Item& it, int code, const std::string& msg) {
+    if (it.code == HIVC_OK) {
+        it.code = code;
+        it.msg = msg;
     }
-    if (!out_on_device) CUDA_CHECK(cudaEventRecord(L.out_free[slot], L.copy));
-    slot ^= 1;
 }
 
-void run_lane(Context& ctx, Lane& L, const std::vector<StreamJob>& streams, const std::vector<WorkItem>& items,
-              std::atomic<size_t>& next_item, bool out_on_device, bool timed, cudaEvent_t origin, cudaEvent_t done,
-              LaneResult& R) {
-    std::vector<FrameJob> jobs;
-    std::vector<uint64_t> bits;
-    EvPairs ev_intra, ev_inter, ev_ifin;
-    int slot = 0;
+// Pack frames [fi, fi + cnt) of the item into the next staging buffer and ship them.
+const uint8_t* stage_chunk(Slot& L, Item& it, size_t fi, int cnt, FrameOffsets* offs) {
+    Packer pk;
+    for (int k = 0; k < cnt; ++k) pack_frame(pk, it.slot->jobs[fi + k], offs[k]);
+    uint8_t *host, *dev;
+    L.stage_alloc(pk.off + 16, host, dev);
+    pk.base = host;
+    pk.off = 0;
+    pk.measure = false;
+    for (int k = 0; k < cnt; ++k) pack_frame(pk, it.slot->jobs[fi + k], offs[k]);
+    CUDA_CHECK(cudaMemcpyAsync(dev, host, pk.off, cudaMemcpyHostToDevice, L.stream));
+    it.h2d += (int64_t)pk.off;
+    return dev;
+}
+
+// Frame arguments of frame fi (prediction source, residual, outputs).
+FrameArgs frame_args(Slot& L, const StreamHeader& hd, Item& it, size_t fi, const FrameOffsets& o, const uint8_t* dev) {
+    const int h = hd.height, w = hd.width, C = hd.channels;
+    const size_t N = (size_t)h * w, frame_bytes = N * C;
+    const FrameJob& J = it.slot->jobs[fi];
+    FrameArgs A;
+    A.h = h;
+    A.w = w;
+    A.channels = C;
+    uint8_t* fr = it.gop_dev + fi * frame_bytes;
+    uint8_t* frprev = fi ? it.gop_dev + (fi - 1) * frame_bytes : nullptr;
+    for (int c = 0; c < C; ++c) {
+        if (C == 1) {
+            A.recon[c] = fr;  // gray: the reconstruction IS the output frame
+            A.prev[c] = frprev;
+        } else {
+            A.recon[c] = L.ring[fi & 1][c];
+            A.prev[c] = L.ring[(fi + 1) & 1][c];
+            A.rgb[c] = fr + c * N;
+        }
+        A.u[c] = L.u[c];
+    }
+    ResDev& RD = A.res;
+    RD.ngroups = J.res.zero ? 0 : J.res.ngroups;
+    RD.dz_step = 127.0 / (double)((hd.residual_levels - 1) / 2);  // quantize.py:43-47
+    RD.c_scale = J.res.c_scale;
+    RD.a_scale = J.res.a_scale;
+    for (int g = 0; g < RD.ngroups; ++g) {
+        const ResidualGroup& G = J.res.g[g];
+        ResGroupDev& D = RD.g[g];
+        D.nplanes = G.nplanes;
+        D.nblocks = G.nblocks;
+        D.npoints = G.npoints;
+        D.tile_words = at<uint64_t>(dev, o.g[g][0]);
+        D.word_prefix = at<int32_t>(dev, o.g[g][1]);
+        D.block_mask = at<uint64_t>(dev, o.g[g][2]);
+        D.block_off = at<int32_t>(dev, o.g[g][3]);
+        D.c_sym = at<int32_t>(dev, o.g[g][4]);
+        D.a_sym = at<int32_t>(dev, o.g[g][5]);
+    }
+    if (J.type == 1)
+        for (int c = 0; c < 2; ++c) {
+            A.flow.nodes[c] = at<int32_t>(dev, o.nodes[c]);
+            A.flow.vals[c] = at<double>(dev, o.fvals[c]);
+            A.flow.tiles[c] = at<uint16_t>(dev, o.ftiles[c]);
+        }
+    return A;
+}
+
+// f = 0 with the intra values scattered at the mask points (prediction.py:203-208), on the slot stream.
+void scatter_intra(Context& ctx, Slot& L, const StreamHeader& hd, const FrameJob& J, const FrameOffsets& o,
+                   const uint8_t* dev) {
+    const size_t N = (size_t)hd.height * hd.width;
+    for (int c = 0; c < hd.channels; ++c) {
+        const int t = c == 0 ? 0 : 1;
+        CUDA_CHECK(cudaMemsetAsync(L.f[c], 0, N * sizeof(double), L.stream));
+        if (c <= 1) CUDA_CHECK(cudaMemsetAsync(L.m[t], 0, N, L.stream));
+        launch_scatter(at<int32_t>(dev, o.pts[t]), at<double>(dev, o.vals[c]), (int)J.intra.pts[t].size(), L.f[c],
+                       c <= 1 ? L.m[t] : nullptr, L.stream);
+        ctx.launches += 1;
+    }
+}
+
+struct CallState {
+    Context& ctx;
+    std::vector<StreamJob>& streams;
+    std::vector<Item>& items;
+    std::deque<Group>& groups;
+    Shared& sh;
+    bool out_on_device, timed;
+    cudaEvent_t origin;
+    double t0;  // host clock at the origin event
+};
+
+void copy_out(CallState& cs, Slot& L, Item& it, size_t fi, size_t frame_bytes) {
+    if (cs.out_on_device) return;
+    cudaEvent_t fe = L.frame_ev[L.frame_ev_next++ % Slot::kFrameEv];
+    CUDA_CHECK(cudaEventRecord(fe, L.stream));
+    CUDA_CHECK(cudaStreamWaitEvent(L.copy, fe, 0));
+    CUDA_CHECK(cudaMemcpyAsync(it.gop_host + fi * frame_bytes, it.gop_dev + fi * frame_bytes, frame_bytes,
+                               cudaMemcpyDeviceToHost, L.copy));
+    it.d2h += (int64_t)frame_bytes;
+}
+
+// Solve the staged I-frames of items idx (same shape): pyramid + cluster
+// levels on a side stream, grid levels on the solver stream; each item's
+// intra_done is recorded as soon as its own solve is complete (the finest
+// levels run one solve after another), so its finalize and P frames start
+// while the batch's later solves still run.  Callers hold ctx.solver_mu.
+void issue_solves(CallState& cs, const std::vector<int>& idx, const StreamHeader& hd) {
+    Context& ctx = cs.ctx;
+    const int h = hd.height, w = hd.width, C = hd.channels;
+    const cudaStream_t pre = idx.empty() ? nullptr : ctx.pre[cs.items[idx[0]].group & 1];
+    for (size_t b0 = 0; b0 < idx.size(); b0 += kMaxBatch) {
+        const int K = (int)std::min<size_t>(kMaxBatch, idx.size() - b0);
+        for (int j = 0; j < K; ++j) CUDA_CHECK(cudaStreamWaitEvent(pre, cs.items[idx[b0 + j]].slot->intra_ready, 0));
+        EvRec r;
+        if (cs.timed) {
+            const Item& i0 = cs.items[idx[b0]];
+            r.stream = i0.stream;
+            r.gop = i0.gop;
+            CUDA_CHECK(cudaEventCreate(&r.first));
+            CUDA_CHECK(cudaEventCreate(&r.second));
+            CUDA_CHECK(cudaEventRecord(r.first, pre));
+        }
+        int64_t launches = 0;
+        for (int c = 0; c < C; ++c) {
+            SolveJob sj[kMaxBatch];
+            for (int j = 0; j < K; ++j) {
+                Slot& L = *cs.items[idx[b0 + j]].slot;
+                sj[j] = {&L.ws, L.f[c], L.m[c == 0 ? 0 : 1], L.u[c], c == C - 1 ? L.intra_done : nullptr};
+            }
+            solve_batch_async(sj, K, h, w, 1e-4, 160, ctx.solver, &launches, cs.timed ? &ctx.probe : nullptr, pre);
+        }
+        ctx.launches += launches;
+        if (cs.timed) {  // the batch interval (stage sums stay per batch), kept with its first item
+            CUDA_CHECK(cudaEventRecord(r.second, ctx.solver));
+            cs.items[idx[b0]].ev_intra.push_back(r);
+        }
+        for (int j = 0; j < K; ++j) cs.items[idx[b0 + j]].solve0 = false;
+    }
+}
+
+// I-frame finalize (rint / clip / RCT of the inpainted planes + residual) on the slot stream.
+void finalize_intra(CallState& cs, Item& it, const FrameArgs& A, int frame) {
+    Slot& L = *it.slot;
+    CUDA_CHECK(cudaStreamWaitEvent(L.stream, L.intra_done, 0));
+    EvRec r;
+    r.stream = it.stream;
+    r.gop = it.gop;
+    r.frame = frame;
+    if (cs.timed) {
+        CUDA_CHECK(cudaEventCreate(&r.first));
+        CUDA_CHECK(cudaEventCreate(&r.second));
+        CUDA_CHECK(cudaEventRecord(r.first, L.stream));
+    }
+    launch_frame(A, false, L.stream);
+    cs.ctx.launches += 1;
+    if (cs.timed) {
+        CUDA_CHECK(cudaEventRecord(r.second, L.stream));
+        it.ev_ifin.push_back(r);
+    }
+}
+
+// Phase 1 of an item: parse + ship its I-frame, scatter the mask values; the
+// last item of a shape group issues the group's batched solves.
+void intra_phase(CallState& cs, Item& it) {
+    std::vector<uint64_t>& bits = it.slot->bits;
+    const StreamJob& S = cs.streams[it.stream];
+    const StreamHeader& hd = S.hd;
+    Slot& L = *it.slot;
+    const size_t frame_bytes = (size_t)hd.height * hd.width * hd.channels;
+    it.h_i0 = now_s() - cs.t0;
     try {
         CUDA_CHECK(cudaSetDevice(L.device));
-        CUDA_CHECK(cudaStreamWaitEvent(L.stream, origin, 0));
-        bool any = false;
-        for (size_t i; (i = next_item.fetch_add(1)) < items.size();) {  // largest planes first, first free lane
-            const WorkItem& it = items[i];
-            any = true;
-            R.stream = it.stream;
-            R.gop = it.gop;
-            decode_gop(ctx, L, streams[it.stream], it.gop, out_on_device, timed, R, jobs, bits, slot, ev_intra,
-                       ev_inter, ev_ifin);
+        CUDA_CHECK(cudaStreamWaitEvent(L.stream, cs.origin, 0));
+        CUDA_CHECK(cudaStreamWaitEvent(L.copy, cs.origin, 0));
+        it.gop_dev = cs.out_on_device ? S.out + S.frame_base[it.gop] * frame_bytes : L.gop_out;
+        it.gop_host = cs.out_on_device ? nullptr : S.out + S.frame_base[it.gop] * frame_bytes;
+        if (!cs.out_on_device) CUDA_CHECK(cudaStreamWaitEvent(L.stream, L.out_free, 0));  // last call's copies
+        it.cur = std::make_unique<GopCursor>(S.data + S.gops[it.gop].first, S.gops[it.gop].second, hd, it.gop);
+        it.nf = it.cur->nframes;
+        if ((int)it.slot->jobs.size() < it.nf) it.slot->jobs.resize(it.nf);
+        if (it.nf > 0) {
+            it.cur->parse(it.slot->jobs[0], it.ht, bits);  // frame 0 must be intra (codec.py:503)
+            if (it.nf == 1) it.cur->finish();
+            FrameOffsets o[1];
+            const uint8_t* dev = stage_chunk(L, it, 0, 1, o);
+            scatter_intra(cs.ctx, L, hd, it.slot->jobs[0], o[0], dev);
+            CUDA_CHECK(cudaEventRecord(L.intra_ready, L.stream));
+            it.a0 = frame_args(L, hd, it, 0, o[0], dev);
+            it.intra_frames += 1;
+            it.solve0 = true;
+        } else {
+            it.cur->finish();
         }
-        if (!out_on_device && any)  // the span ends with the last D2H copy
-            CUDA_CHECK(cudaStreamWaitEvent(L.stream, L.out_free[slot ^ 1], 0));
-        CUDA_CHECK(cudaEventRecord(done, L.stream));
-        CUDA_CHECK(cudaStreamSynchronize(L.stream));
-        std::string* tl = std::getenv("HIVC_TIMELINE") ? &R.timeline : nullptr;
-        R.gpu_intra = drain(ev_intra, origin, 'I', tl);
-        R.gpu_inter = drain(ev_inter, origin, 'P', tl);
-        R.gpu_ifinal = drain(ev_ifin, origin, 'F', tl);
-        L.probe.harvest(R.cg);
     } catch (const Error& e) {
-        R.code = e.code;
-        R.msg = e.what();
-        cudaEventRecord(done, L.stream);
-        cudaStreamSynchronize(L.stream);
-        if (L.copy) cudaStreamSynchronize(L.copy);
+        fail_item(it, e.code, e.what());
     } catch (const std::exception& e) {
-        R.code = HIVC_E_ARGUMENT;
-        R.msg = e.what();
-        cudaEventRecord(done, L.stream);
-        cudaStreamSynchronize(L.stream);
-        if (L.copy) cudaStreamSynchronize(L.copy);
+        fail_item(it, HIVC_E_ARGUMENT, e.what());
     }
+    it.h_i1 = now_s() - cs.t0;
+    Group& g = cs.groups[it.group];
+    if (g.pending.fetch_sub(1) == 1) {
+        for (int i : g.items) cs.items[i].h_issue = now_s() - cs.t0;
+        std::vector<int> ready;
+        for (int i : g.items)
+            if (cs.items[i].code == HIVC_OK && cs.items[i].solve0) ready.push_back(i);
+        try {
+            std::lock_guard<std::mutex> lk(cs.ctx.solver_mu);
+            CUDA_CHECK(cudaSetDevice(cs.ctx.device));
+            issue_solves(cs, ready, hd);
+        } catch (const Error& e) {
+            for (int i : ready) fail_item(cs.items[i], e.code, e.what());
+        } catch (const std::exception& e) {
+            for (int i : ready) fail_item(cs.items[i], HIVC_E_ARGUMENT, e.what());
+        }
+        {
+            std::lock_guard<std::mutex> lk(cs.sh.mu);
+            g.issued = true;
+        }
+        cs.sh.cv.notify_all();
+    }
+}
+
+// Phase 2 of an item: after its group's solves are queued, parse and run the
+// P frames (chunks of kChunk) on the slot stream; host output copies each
+// finished frame out on the copy stream.
+void inter_phase(CallState& cs, Item& it) {
+    std::vector<uint64_t>& bits = it.slot->bits;
+    const StreamJob& S = cs.streams[it.stream];
+    const StreamHeader& hd = S.hd;
+    Slot& L = *it.slot;
+    const size_t frame_bytes = (size_t)hd.height * hd.width * hd.channels;
+    {
+        std::unique_lock<std::mutex> lk(cs.sh.mu);
+        cs.sh.cv.wait(lk, [&] { return cs.groups[it.group].issued; });
+    }
+    it.h_p0 = now_s() - cs.t0;
+    try {
+        CUDA_CHECK(cudaSetDevice(L.device));
+        if (it.code != HIVC_OK) throw Error(it.code, it.msg);
+        if (it.nf > 0) {
+            finalize_intra(cs, it, it.a0, 0);
+            copy_out(cs, L, it, 0, frame_bytes);
+        }
+        constexpr int kChunk = 2;
+        FrameOffsets offs[kChunk];
+        size_t fi = 1;
+        while ((int)fi < it.nf) {
+            const int cnt = std::min(kChunk, it.nf - (int)fi);
+            for (int k = 0; k < cnt; ++k) it.cur->parse(it.slot->jobs[fi + k], it.ht, bits);
+            if ((int)fi + cnt == it.nf) it.cur->finish();
+            const uint8_t* dev = stage_chunk(L, it, fi, cnt, offs);
+            for (int k = 0; k < cnt; ++k, ++fi) {
+                const FrameJob& J = it.slot->jobs[fi];
+                FrameArgs A = frame_args(L, hd, it, fi, offs[k], dev);
+                EvRec e;
+                e.stream = it.stream;
+                e.gop = it.gop;
+                e.frame = (int)fi;
+                if (cs.timed) {
+                    CUDA_CHECK(cudaEventCreate(&e.first));
+                    CUDA_CHECK(cudaEventCreate(&e.second));
+                    CUDA_CHECK(cudaEventRecord(e.first, L.stream));
+                }
+                if (J.type == 0) {
+                    // an intra frame inside the GOP: solve it alone on the solver stream
+                    scatter_intra(cs.ctx, L, hd, J, offs[k], dev);
+                    CUDA_CHECK(cudaEventRecord(L.intra_ready, L.stream));
+                    {
+                        std::lock_guard<std::mutex> lk(cs.ctx.solver_mu);
+                        issue_solves(cs, std::vector<int>{(int)(&it - cs.items.data())}, hd);
+                    }
+                    finalize_intra(cs, it, A, (int)fi);
+                    it.intra_frames += 1;
+                } else {
+                    launch_frame(A, true, L.stream);
+                    cs.ctx.launches += 1;
+                    it.inter_frames += 1;
+                }
+                if (cs.timed) {
+                    CUDA_CHECK(cudaEventRecord(e.second, L.stream));
+                    it.ev_inter.push_back(e);
+                }
+                copy_out(cs, L, it, fi, frame_bytes);
+            }
+        }
+    } catch (const Error& e) {
+        fail_item(it, e.code, e.what());
+    } catch (const std::exception& e) {
+        fail_item(it, HIVC_E_ARGUMENT, e.what());
+    }
+    // the item's device span ends with its last frame (and its last D2H copy)
+    if (!cs.out_on_device) {
+        cudaEventRecord(L.out_free, L.copy);
+        cudaStreamWaitEvent(L.stream, L.out_free, 0);
+    }
+    cudaEventRecord(it.done, L.stream);
+    it.h_p1 = now_s() - cs.t0;
 }
 
 }  // namespace
@@ -528,7 +702,7 @@ void decode_streams(Context& ctx, int nstreams, const uint8_t* const* data, cons
                     const int* gop_end, uint8_t* const* out, bool out_on_device, double* stage_seconds) {
     double t_all = now_s();
     std::vector<StreamJob> streams(nstreams);
-    std::vector<WorkItem> items;
+    std::vector<Item> items;
     int max_h = 1, max_w = 1, max_c = 1;
     size_t max_gop_bytes = 1;
     for (int k = 0; k < nstreams; ++k) {
@@ -551,71 +725,139 @@ void decode_streams(Context& ctx, int nstreams, const uint8_t* const* data, cons
             if (S.gops[g].second >= 2) std::memcpy(&nf, S.data + S.gops[g].first, 2);
             acc += nf;
             max_gop_bytes = std::max(max_gop_bytes, nf * frame_bytes);
-            items.push_back({k, g});
+            Item it;
+            it.stream = k;
+            it.gop = g;
+            items.push_back(std::move(it));
         }
         max_h = std::max(max_h, S.hd.height);
         max_w = std::max(max_w, S.hd.width);
         max_c = std::max(max_c, S.hd.channels);
     }
-    // largest planes first so lanes finish together
-    std::stable_sort(items.begin(), items.end(), [&](const WorkItem& a, const WorkItem& b) {
+    const int n = (int)items.size();
+    // smallest planes first: their I-frames parse fastest, so their batch is
+    // issued (and on the GPU) first while the large planes are still parsing
+    std::stable_sort(items.begin(), items.end(), [&](const Item& a, const Item& b) {
         const StreamHeader &ha = streams[a.stream].hd, &hb = streams[b.stream].hd;
-        return (int64_t)ha.height * ha.width * ha.channels > (int64_t)hb.height * hb.width * hb.channels;
+        return (int64_t)ha.height * ha.width * ha.channels < (int64_t)hb.height * hb.width * hb.channels;
     });
-    static const int kMaxLanes = [] {
-        const char* e = std::getenv("HIVC_LANES");
-        return e ? std::max(1, std::min(32, std::atoi(e))) : 8;
-    }();
-    int nlanes = std::max(1, std::min((int)items.size(), kMaxLanes));
-    CUDA_CHECK(cudaSetDevice(ctx.device));
-    while ((int)ctx.lanes.size() < nlanes) {
-        auto L = std::make_unique<Lane>();
-        L->device = ctx.device;
-        CUDA_CHECK(cudaStreamCreateWithFlags(&L->stream, cudaStreamNonBlocking));
-        ctx.lanes.push_back(std::move(L));
+    // shape groups: their I-frame solves are batched
+    std::deque<Group> groups;
+    for (int i = 0; i < n; ++i) {
+        const StreamHeader& hd = streams[items[i].stream].hd;
+        int gi = -1;
+        for (size_t g = 0; g < groups.size(); ++g)
+            if (groups[g].h == hd.height && groups[g].w == hd.width && groups[g].c == hd.channels) gi = (int)g;
+        if (gi < 0) {
+            groups.emplace_back();
+            gi = (int)groups.size() - 1;
+            groups[gi].h = hd.height;
+            groups[gi].w = hd.width;
+            groups[gi].c = hd.channels;
+        }
+        items[i].group = gi;
+        groups[gi].items.push_back(i);
     }
-    for (int l = 0; l < nlanes; ++l) {
-        Lane& L = *ctx.lanes[l];
+    for (auto& g : groups) g.pending = (int)g.items.size();
+    CUDA_CHECK(cudaSetDevice(ctx.device));
+    if (!ctx.solver) CUDA_CHECK(cudaStreamCreateWithFlags(&ctx.solver, cudaStreamNonBlocking));
+    for (cudaStream_t& p : ctx.pre)
+        if (!p) CUDA_CHECK(cudaStreamCreateWithFlags(&p, cudaStreamNonBlocking));
+    while ((int)ctx.slots.size() < n) ctx.slots.push_back(std::make_unique<Slot>());
+    for (int i = 0; i < n; ++i) {
+        Slot& L = *ctx.slots[i];
+        L.init(ctx.device);
         L.reserve_planes(max_h, max_w, max_c);
         L.ws.reserve(max_h, max_w, ctx.device);
-        L.ws.pack_bands = true;  // lanes solve side by side: throughput mode
         if (!out_on_device) L.reserve_gop_out(max_gop_bytes);
-        // staging sized up front (an I-frame of a typical mask fits), so a lane
-        // meeting its first large chunk does not reallocate (cudaFree syncs the device)
-        for (int b = 0; b < Lane::kStage; ++b) L.reserve_stage(b, (size_t)2 * max_h * max_w * max_c + 65536);
+        L.stage_begin_call((size_t)4 * max_h * max_w * max_c + 65536);
+        items[i].slot = &L;
+        CUDA_CHECK(cudaEventCreate(&items[i].done));
     }
-    std::atomic<size_t> next_item{0};
-    std::vector<LaneResult> res(nlanes);
     const bool timed = (stage_seconds != nullptr && ctx.stage_events) || std::getenv("HIVC_TIMELINE");
-    // device-side span: every lane waits on `origin`, records `done[l]` after its last copy
     cudaEvent_t origin;
     CUDA_CHECK(cudaEventCreate(&origin));
-    std::vector<cudaEvent_t> done(nlanes);
-    for (auto& e : done) CUDA_CHECK(cudaEventCreate(&e));
     CUDA_CHECK(cudaEventRecord(origin, ctx.stream));
-    if (nlanes == 1) {
-        run_lane(ctx, *ctx.lanes[0], streams, items, next_item, out_on_device, timed, origin, done[0], res[0]);
+    CUDA_CHECK(cudaStreamWaitEvent(ctx.solver, origin, 0));
+    for (cudaStream_t p : ctx.pre) CUDA_CHECK(cudaStreamWaitEvent(p, origin, 0));
+    Shared sh;
+    CallState cs{ctx, streams, items, groups, sh, out_on_device, timed, origin, now_s()};
+    // task queue: every item's intra phase, then the inter phases, both in
+    // batch-issue order.  A pool thread that reaches the inter phases drops
+    // its scheduling priority: P-frame parsing has slack (its GPU work queues
+    // behind the batched solves) while the large I-frames being parsed on the
+    // other threads gate the next batch.
+    std::atomic<int> next_task{0};
+    auto worker = [&](bool pool) {
+        bool low = false;
+        for (int t; (t = next_task.fetch_add(1)) < 2 * n;) {
+            if (t < n) {
+                intra_phase(cs, items[t]);
+            } else {
+                if (pool && !low) {
+                    setpriority(PRIO_PROCESS, (id_t)syscall(SYS_gettid), 10);
+                    low = true;
+                }
+                inter_phase(cs, items[t - n]);
+            }
+        }
+    };
+    static const int kMaxWorkers = [] {
+        const char* e = std::getenv("HIVC_WORKERS");
+        const int hw = (int)std::max(2u, std::thread::hardware_concurrency());
+        return e ? std::max(1, std::min(64, std::atoi(e))) : std::min(hw, 32);
+    }();
+    const int nworkers = std::max(1, std::min(n, kMaxWorkers));
+    if (nworkers == 1 || n == 0) {
+        worker(false);
     } else {
         std::vector<std::thread> th;
-        for (int l = 0; l < nlanes; ++l)
-            th.emplace_back(run_lane, std::ref(ctx), std::ref(*ctx.lanes[l]), std::cref(streams), std::cref(items),
-                            std::ref(next_item), out_on_device, timed, origin, done[l], std::ref(res[l]));
+        for (int l = 0; l < nworkers; ++l) th.emplace_back(worker, true);
         for (auto& t : th) t.join();
     }
     double span = 0;
-    for (auto& e : done) {
+    for (auto& it : items) {
+        cudaStreamSynchronize(it.slot->stream);
+        cudaStreamSynchronize(it.slot->copy);
         float ms = 0;
-        if (cudaEventElapsedTime(&ms, origin, e) == cudaSuccess) span = std::max(span, (double)ms * 1e-3);
-        cudaEventDestroy(e);
+        if (cudaEventElapsedTime(&ms, origin, it.done) == cudaSuccess) span = std::max(span, (double)ms * 1e-3);
+    }
+    cudaStreamSynchronize(ctx.solver);
+    std::string timeline;
+    std::string* tl = std::getenv("HIVC_TIMELINE") ? &timeline : nullptr;
+    double gpu_intra = 0, gpu_inter = 0, gpu_ifin = 0;
+    for (int i = 0; i < n; ++i) {
+        Item& it = items[i];
+        gpu_intra += drain(it.ev_intra, origin, 'I', i, tl);
+        gpu_inter += drain(it.ev_inter, origin, 'P', i, tl);
+        gpu_ifin += drain(it.ev_ifin, origin, 'F', i, tl);
+        cudaEventDestroy(it.done);
+        if (tl) {
+            char line[200];
+            std::snprintf(line, sizeof line, "%d,H,%d,%d,0,%.1f,%.1f\n%d,Q,%d,%d,0,%.1f,%.1f\n", i, it.stream, it.gop,
+                          it.h_i0 * 1e6, it.h_i1 * 1e6, i, it.stream, it.gop, it.h_p0 * 1e6, it.h_p1 * 1e6);
+            *tl += line;
+        }
     }
     cudaEventDestroy(origin);
+    if (tl) {
+        if (FILE* f = std::fopen(std::getenv("HIVC_TIMELINE"), "a")) {
+            std::fputs(timeline.c_str(), f);
+            std::fprintf(f, "-\n");
+            std::fclose(f);
+        }
+    }
+    CgTotals cg;
+    if (timed) ctx.probe.harvest(cg);
     // the first failing (stream, GOP) in stream order wins (the reference decodes sequentially)
     int worst = -1;
-    for (int l = 0; l < nlanes; ++l)
-        if (res[l].code != HIVC_OK &&
-            (worst < 0 || std::make_pair(res[l].stream, res[l].gop) < std::make_pair(res[worst].stream, res[worst].gop)))
-            worst = l;
-    if (worst >= 0) fail(res[worst].code, res[worst].msg);
+    for (int i = 0; i < n; ++i)
+        if (items[i].code != HIVC_OK &&
+            (worst < 0 ||
+             std::make_pair(items[i].stream, items[i].gop) < std::make_pair(items[worst].stream, items[worst].gop)))
+            worst = i;
+    if (worst >= 0) fail(items[worst].code, items[worst].msg);
+    CUDA_CHECK(cudaGetLastError());
     for (const StreamJob& S : streams) {
         if (S.gop_begin == 0 && S.gop_end == (int)S.gops.size()) {  // codec.py:558-561
             size_t total = 0;
@@ -629,46 +871,30 @@ void decode_streams(Context& ctx, int nstreams, const uint8_t* const* data, cons
                                        std::to_string(S.hd.frame_count));
         }
     }
-    if (const char* tl = std::getenv("HIVC_TIMELINE")) {  // debug: append lane,kind,stream,gop,frame,t0,t1
-        if (FILE* f = std::fopen(tl, "a")) {
-            for (int l = 0; l < nlanes; ++l) {
-                size_t a = 0;
-                const std::string& t = res[l].timeline;
-                while (a < t.size()) {
-                    size_t b = t.find('\n', a);
-                    std::fprintf(f, "%d,%s\n", l, t.substr(a, b - a).c_str());
-                    a = b + 1;
-                }
-            }
-            std::fprintf(f, "-\n");
-            std::fclose(f);
-        }
-    }
-    for (auto& r : res) {
-        ctx.h2d_bytes += r.h2d;
-        ctx.d2h_bytes += r.d2h;
+    HostTimes ht;
+    {
         std::lock_guard<std::mutex> g(ctx.stats_mu);
         CgTotals& T = ctx.cg;
-        T.solves += r.cg.solves;
-        T.pixel_iters += r.cg.pixel_iters;
-        T.pixel_levels += r.cg.pixel_levels;
-        T.grid_launches += r.cg.grid_launches;
-        T.grid_seconds += r.cg.grid_seconds;
-        T.grid_pixel_iters += r.cg.grid_pixel_iters;
-        T.grid_pixels += r.cg.grid_pixels;
-        ctx.inter_frames += r.inter_frames;
-        ctx.inter_seconds += r.gpu_inter;
-        ctx.intra_frames += r.intra_frames;
+        T.solves += cg.solves;
+        T.pixel_iters += cg.pixel_iters;
+        T.pixel_levels += cg.pixel_levels;
+        T.grid_launches += cg.grid_launches;
+        T.grid_seconds += cg.grid_seconds;
+        T.grid_pixel_iters += cg.grid_pixel_iters;
+        T.grid_pixels += cg.grid_pixels;
+        for (auto& it : items) {
+            ctx.h2d_bytes += it.h2d;
+            ctx.d2h_bytes += it.d2h;
+            ctx.inter_frames += it.inter_frames;
+            ctx.intra_frames += it.intra_frames;
+            ht.intra_parse += it.ht.intra_parse;
+            ht.flow_parse += it.ht.flow_parse;
+            ht.residual_parse += it.ht.residual_parse;
+        }
+        ctx.inter_seconds += gpu_inter;
     }
     if (stage_seconds) {
-        double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        for (auto& r : res) {
-            s[0] += r.ht.intra_parse + r.gpu_intra;
-            s[1] += r.ht.flow_parse;
-            s[2] += r.gpu_inter;
-            s[3] += r.ht.residual_parse;
-            s[4] += r.gpu_ifinal;
-        }
+        double s[8] = {ht.intra_parse + gpu_intra, ht.flow_parse, gpu_inter, ht.residual_parse, gpu_ifin, 0, 0, 0};
         s[6] = now_s() - t_all;
         s[7] = span;
         std::memcpy(stage_seconds, s, sizeof(s));

@@ -1,4 +1,4 @@
-// Stream decoder: GOP-parallel host parsing feeding per-lane CUDA streams.
+// Stream decoder: GOP-parallel host parsing, batched I-frame solves, per-GOP P-frame streams.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -15,11 +15,22 @@
 
 namespace hivc {
 
-// One decode lane: a CUDA stream, a solver workspace and double-buffered
-// staging (pinned host + device) for the compact frame descriptions.
-struct Lane {
+// Parsed description of one frame record (host side).
+struct FrameJob {
+    int type = 0;  // 0 intra, 1 inter
+    IntraJob intra;
+    FlowJob flow;
+    ResidualJob res;
+};
+
+// Device state of one work item (one GOP of one stream) of a decode call;
+// a call uses slots [0, items).  The slot's stream carries the item's
+// uploads, the I-frame scatter and the P-frame chain; its I-frame solve runs
+// batched with the other items' on the context's solver stream.
+struct Slot {
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t copy = nullptr;  // host output: D2H of finished frames
     InpaintWorkspace ws;
     size_t plane_px = 0;
     int chans = 0;
@@ -27,27 +38,34 @@ struct Lane {
     uint8_t* m[2] = {nullptr, nullptr};
     double* u[3] = {nullptr, nullptr, nullptr};
     int16_t* ring[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
-    // ring of pinned staging buffers: one per shipped chunk of frame descriptions
-    static constexpr int kStage = 4;
-    uint8_t* host_stage[kStage] = {};
-    uint8_t* dev_stage[kStage] = {};
-    size_t stage_cap[kStage] = {};
-    cudaEvent_t staged[kStage] = {};
-    int stage_next = 0;
-    uint8_t* gop_out[2] = {nullptr, nullptr};  // device frame buffers when output goes to the host
+    // staging arena (pinned host block + device block): every chunk of frame
+    // descriptions of a call gets its own range, so a worker never waits for
+    // the GPU to free a buffer; a call that outgrows the block chains a new
+    // one and the next call starts with one block of the combined size
+    struct StageBlock {
+        uint8_t* host = nullptr;
+        uint8_t* dev = nullptr;
+        size_t cap = 0;
+    };
+    std::vector<StageBlock> stage;
+    size_t stage_off = 0, stage_used = 0;
+    void stage_begin_call(size_t min_bytes);
+    void stage_alloc(size_t bytes, uint8_t*& host, uint8_t*& dev);
+    uint8_t* gop_out = nullptr;  // host-output mode: the GOP's frames on the device
     size_t gop_out_cap = 0;
-    // host output: each finished frame is copied D2H on `copy` while the lane
-    // stream decodes the next one; out_free[slot] = last copy out of gop_out[slot]
-    cudaStream_t copy = nullptr;
     static constexpr int kFrameEv = 8;
     cudaEvent_t frame_ev[kFrameEv] = {};
-    cudaEvent_t out_free[2] = {nullptr, nullptr};
     int frame_ev_next = 0;
-    CgProbe probe;
+    cudaEvent_t out_free = nullptr;     // last D2H out of gop_out
+    cudaEvent_t intra_ready = nullptr;  // I-frame f / mask planes in place (slot stream)
+    cudaEvent_t intra_done = nullptr;   // I-frame solved and finalised (solver stream)
+    // host scratch kept across calls (capacity reuse: no page faults per call)
+    std::vector<FrameJob> jobs;
+    std::vector<uint64_t> bits;
+    void init(int dev);
     void reserve_planes(int h, int w, int channels);
-    void reserve_stage(int slot, size_t bytes);
     void reserve_gop_out(size_t bytes);
-    ~Lane();
+    ~Slot();
 };
 
 struct Context {
@@ -55,7 +73,11 @@ struct Context {
     cudaStream_t stream = nullptr;  // function-level API stream
     InpaintWorkspace ws;            // function-level solver scratch
     BroxWorkspace brox;             // flow_brox scratch
-    std::vector<std::unique_ptr<Lane>> lanes;
+    std::vector<std::unique_ptr<Slot>> slots;
+    cudaStream_t solver = nullptr;  // every batched (grid-barrier) solve of a decode call, in order
+    cudaStream_t pre[2] = {nullptr, nullptr};  // pyramid + cluster levels of a batch (side streams)
+    std::mutex solver_mu;           // one batch's launches stay contiguous on the solver stream
+    CgProbe probe;                  // solver-stream launches (stage timing on)
     std::atomic<int64_t> launches{0};
     std::atomic<int64_t> h2d_bytes{0}, d2h_bytes{0};
     bool stage_events = true;  // per-frame CUDA events for the stage breakdown
@@ -69,8 +91,8 @@ struct Context {
     ~Context();
 };
 
-// Decode GOP ranges of several streams in one pass (one lane per host thread,
-// work items = (stream, GOP)).  stage_seconds (nullable, 8 doubles): the 7
+// Decode GOP ranges of several streams in one pass (work items = (stream,
+// GOP), parsed by a pool of host threads; I-frame solves batched per shape).  stage_seconds (nullable, 8 doubles): the 7
 // reference timing keys + the device-side span (first lane start -> last lane end).
 void decode_streams(Context& ctx, int nstreams, const uint8_t* const* data, const size_t* len, const int* gop_begin,
                     const int* gop_end, uint8_t* const* out, bool out_on_device, double* stage_seconds);

@@ -102,6 +102,24 @@ __device__ __forceinline__ void grid_arrive_wait(unsigned int* bar, unsigned int
     __syncthreads();
 }
 
+// Split form: arrive (after a CTA barrier that ordered the CTA's global
+// writes), independent work, then wait.
+__device__ __forceinline__ void grid_arrive(unsigned int* bar, unsigned int& epoch) {
+    ++epoch;
+    if (threadIdx.x == 0) {
+        unsigned int old;
+        asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(bar) : "memory");
+    }
+}
+__device__ __forceinline__ void grid_wait(const unsigned int* bar, unsigned int nblocks, unsigned int epoch) {
+    if (threadIdx.x == 0) {
+        const unsigned int target = epoch * nblocks;
+        while (ld_acquire_gpu(bar) < target) {
+        }
+    }
+    __syncthreads();
+}
+
 __device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int nblocks, unsigned int& epoch) {
     __syncthreads();
     ++epoch;

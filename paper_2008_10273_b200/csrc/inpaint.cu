@@ -16,6 +16,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "device.cuh"
@@ -30,8 +32,18 @@ constexpr int kSingleCtaMaxPx = 16384;
 
 // ---------------------------------------------------------------- pyramid
 
-__global__ void restrict_kernel(const double* __restrict__ f, const uint8_t* __restrict__ m, int h, int w,
-                                double* __restrict__ fc, uint8_t* __restrict__ mc, int hc, int wc) {
+struct RestrictBatch {  // blockIdx.y = solve
+    const double* f[16];
+    const uint8_t* m[16];
+    double* fc[16];
+    uint8_t* mc[16];
+};
+
+__global__ void restrict_kernel(const __grid_constant__ RestrictBatch B, int h, int w, int hc, int wc) {
+    const double* __restrict__ f = B.f[blockIdx.y];
+    const uint8_t* __restrict__ m = B.m[blockIdx.y];
+    double* __restrict__ fc = B.fc[blockIdx.y];
+    uint8_t* __restrict__ mc = B.mc[blockIdx.y];
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= hc * wc) return;
     int cy = i / wc, cx = i % wc;
@@ -90,6 +102,7 @@ struct CgParams {
     int band_rows;
     double* ex_r;  // [nbands][2][w]: first/last owned row of r
     double* ex_p;  // [2 parity][nbands][2][w]: first/last owned row of p
+    int x_rows = 0;  // band2: leading band rows whose x lives in shared memory (the rest streams)
     unsigned long long* trace = nullptr;  // diagnostics: per-iteration phase timestamps of CTA 0
     unsigned long long* stamp = nullptr;  // probe: globaltimer at kernel entry / exit (CTA 0)
 };
@@ -150,13 +163,15 @@ struct RedState {
     unsigned int epoch = 0;
     int par = 0, bpar = 0;
 };
+// idx / n: this CTA's slot and the number of CTAs taking part (one solve of a batch)
 template <int NV>
-__device__ __forceinline__ void grid_reduce(double (&v)[NV], double* sh, const CgParams& P, RedState& st) {
+__device__ __forceinline__ void grid_reduce(double (&v)[NV], double* sh, const CgParams& P, RedState& st, int idx,
+                                            int n) {
     block_sum1<NV>(v, sh, st.par);
     if (threadIdx.x == 0)
 #pragma unroll
-        for (int k = 0; k < NV; ++k) P.partials[blockIdx.x * 4 + k] = v[k];
-    grid_arrive_wait(P.bar, gridDim.x, st.epoch);
+        for (int k = 0; k < NV; ++k) P.partials[idx * 4 + k] = v[k];
+    grid_arrive_wait(P.bar, n, st.epoch);
     double* bc = sh + 2 * 4 * 32 + st.bpar * 4;
     st.bpar ^= 1;
     if (threadIdx.x < 32) {
@@ -164,7 +179,7 @@ __device__ __forceinline__ void grid_reduce(double (&v)[NV], double* sh, const C
 #pragma unroll
         for (int k = 0; k < NV; ++k) {
             double s = 0.0;
-            for (int g = lane; g < (int)gridDim.x; g += 32) s += __ldcg(P.partials + g * 4 + k);
+            for (int g = lane; g < n; g += 32) s += __ldcg(P.partials + g * 4 + k);
             s = warp_sum(s);
             if (lane == 0) bc[k] = s;
         }
@@ -172,6 +187,40 @@ __device__ __forceinline__ void grid_reduce(double (&v)[NV], double* sh, const C
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < NV; ++k) v[k] = bc[k];
+}
+// grid_reduce in two halves: publish this CTA's partial and arrive; ...; wait and sum.
+template <int NV>
+__device__ __forceinline__ void grid_reduce_arrive(double (&v)[NV], double* sh, const CgParams& P, RedState& st,
+                                                   int idx) {
+    block_sum1<NV>(v, sh, st.par);
+    if (threadIdx.x == 0)
+#pragma unroll
+        for (int k = 0; k < NV; ++k) P.partials[idx * 4 + k] = v[k];
+    grid_arrive(P.bar, st.epoch);
+}
+template <int NV>
+__device__ __forceinline__ void grid_reduce_finish(double (&v)[NV], double* sh, const CgParams& P, RedState& st,
+                                                   int n) {
+    grid_wait(P.bar, n, st.epoch);
+    double* bc = sh + 2 * 4 * 32 + st.bpar * 4;
+    st.bpar ^= 1;
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+#pragma unroll
+        for (int k = 0; k < NV; ++k) {
+            double s = 0.0;
+            for (int g = lane; g < n; g += 32) s += __ldcg(P.partials + g * 4 + k);
+            s = warp_sum(s);
+            if (lane == 0) bc[k] = s;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < NV; ++k) v[k] = bc[k];
+}
+template <int NV>
+__device__ __forceinline__ void grid_reduce(double (&v)[NV], double* sh, const CgParams& P, RedState& st) {
+    grid_reduce<NV>(v, sh, P, st, (int)blockIdx.x, (int)gridDim.x);
 }
 
 template <bool kGrid>
@@ -372,10 +421,10 @@ void InpaintWorkspace::reserve(int h, int w, int dev) {
     const char* env = getenv("HIVC_CG_BAND");
     band_enabled = !(env && env[0] == '0');
     band_variant = (env && env[0] == '1') ? 1 : 2;
-    CUDA_CHECK(cudaFuncSetAttribute(cg_band2_kernel<4, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    CUDA_CHECK(cudaFuncSetAttribute(cg_band2_kernel<8, 4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    CUDA_CHECK(cudaFuncSetAttribute(cg_band2_kernel<4, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBand2Smem));
+    CUDA_CHECK(cudaFuncSetAttribute(cg_band2_kernel<8, 4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBand2Smem));
     CUDA_CHECK(cudaFuncSetAttribute(cg_band2_kernel<kPackRows, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    220 * 1024));
+                                    kBand2Smem));
     const char* env_pack = getenv("HIVC_CG_PACK");
     pack_env_off = env_pack && env_pack[0] == '0';
     const char* env_small = getenv("HIVC_CG_SMALL");
@@ -430,76 +479,178 @@ void InpaintWorkspace::release() {
 
 int solve_homogeneous_async(InpaintWorkspace& ws, cudaStream_t s, const double* f, const uint8_t* m, int h, int w,
                             double tol, int max_iter, double* u_out, int64_t* launches, CgProbe* probe) {
+    SolveJob job{&ws, f, m, u_out};
+    return solve_batch_async(&job, 1, h, w, tol, max_iter, s, launches, probe);
+}
+
+namespace {
+
+// band2 dynamic shared memory: padded p for a ROWS-row band, then as many x
+// rows as fit (CgParams::x_rows, set here) — those never touch global memory.
+size_t band2_smem(int rows_tpl, int band_rows, int w, CgParams* P, int K) {
+    const size_t p_bytes = (size_t)(rows_tpl + 2) * (w + 2) * sizeof(double);
+    const char* e = getenv("HIVC_CG_XRES");
+    int xr = 0;
+    if (!(e && e[0] == '0') && p_bytes < (size_t)kBand2Smem)
+        xr = (int)std::min<size_t>((size_t)band_rows, ((size_t)kBand2Smem - p_bytes) / ((size_t)w * sizeof(double)));
+    for (int j = 0; j < K; ++j) P[j].x_rows = xr;
+    return p_bytes + (size_t)xr * w * sizeof(double);
+}
+
+// Per-job views of its workspace: finest CG vectors + every level's f, m, u.
+struct JobLevels {
+    double* x;
+    double* r;
+    double* pa;
+    double* pb;
+    double* ap;
+    std::vector<const double*> f;
+    std::vector<const uint8_t*> m;
+    std::vector<double*> u;
+};
+
+CgParams level_params(const JobLevels& J, InpaintWorkspace& ws, const std::vector<std::pair<int, int>>& shapes, int l,
+                      double tol, int max_iter) {
+    const int L = (int)shapes.size();
+    CgParams P{};
+    P.h = shapes[l].first;
+    P.w = shapes[l].second;
+    P.n = P.h * P.w;
+    P.f = J.f[l];
+    P.m = J.m[l];
+    P.uc = l == L - 1 ? nullptr : J.u[l + 1];
+    P.hc = l == L - 1 ? 0 : shapes[l + 1].first;
+    P.wc = l == L - 1 ? 0 : shapes[l + 1].second;
+    P.x = J.x;
+    P.r = J.r;
+    P.pa = J.pa;
+    P.pb = J.pb;
+    P.ap = J.ap;
+    P.u = J.u[l];
+    P.tol = l == 0 ? tol : std::max(kLevelTol, tol);
+    P.max_iter = max_iter;
+    P.finest = l == 0;
+    P.partials = ws.partials;
+    P.bar = ws.bar;
+    P.iters = ws.iters + (L - 1 - l);
+    P.margin = ws.margins + (L - 1 - l);
+    return P;
+}
+
+}  // namespace
+
+int solve_batch_async(const SolveJob* jobs, int K, int h, int w, double tol, int max_iter, cudaStream_t s,
+                      int64_t* launches, CgProbe* probe, cudaStream_t s_pre) {
+    if (K < 1 || K > kMaxBatch) fail(HIVC_E_ARGUMENT, "solve batch size out of range");
+    InpaintWorkspace& ws0 = *jobs[0].ws;
+    // pyramid + cluster/single-CTA levels never wait on other CTAs' progress
+    // across launches, so they may run on a side stream next to another
+    // batch's grid-barrier levels; the grid levels stay on s
+    const cudaStream_t sp = s_pre ? s_pre : s;
+    std::vector<bool> recorded(K, false);
     std::vector<std::pair<int, int>> shapes;
     pyramid_shapes(h, w, shapes);
     const int L = (int)shapes.size();
-    size_t n0 = (size_t)h * w;
-    double* x = ws.dbl;
-    double* r = x + n0;
-    double* pa = r + n0;
-    double* pb = pa + n0;
-    double* ap = pb + n0;
-    double* cur = ap + n0;  // coarse f / u storage
-    uint8_t* cm = ws.bytes;
-    std::vector<const double*> lf(L);
-    std::vector<const uint8_t*> lm(L);
-    std::vector<double*> lu(L);
-    lf[0] = f;
-    lm[0] = m;
-    lu[0] = u_out;
+    const size_t n0 = (size_t)h * w;
+    std::vector<JobLevels> J(K);
+    for (int j = 0; j < K; ++j) {
+        InpaintWorkspace& ws = *jobs[j].ws;
+        JobLevels& V = J[j];
+        V.x = ws.dbl;
+        V.r = V.x + n0;
+        V.pa = V.r + n0;
+        V.pb = V.pa + n0;
+        V.ap = V.pb + n0;
+        double* cur = V.ap + n0;  // coarse f / u storage
+        uint8_t* cm = ws.bytes;
+        V.f.assign(L, nullptr);
+        V.m.assign(L, nullptr);
+        V.u.assign(L, nullptr);
+        V.f[0] = jobs[j].f;
+        V.m[0] = jobs[j].m;
+        V.u[0] = jobs[j].u;
+        for (int l = 1; l < L; ++l) {
+            const size_t nl = (size_t)shapes[l].first * shapes[l].second;
+            V.f[l] = cur;
+            cur += nl;
+            V.u[l] = cur;
+            cur += nl;
+            V.m[l] = cm;
+            cm += nl;
+        }
+    }
+    const bool bt = probe && getenv("HIVC_BATCH_TRACE");
+    auto mb = [&](const std::string& label, cudaStream_t st) {
+        if (bt) probe->mark_begin(st, label + " K=" + std::to_string(K) + " " + std::to_string(h) + "x" + std::to_string(w));
+    };
+    auto me = [&](cudaStream_t st) {
+        if (bt) probe->mark_end(st);
+    };
+    // ---- pyramid (homogeneous.py:96-130): one launch per level for the whole batch
+    mb("restrict", sp);
     for (int l = 1; l < L; ++l) {
-        size_t nl = (size_t)shapes[l].first * shapes[l].second;
-        double* fl = cur;
-        cur += nl;
-        lu[l] = cur;
-        cur += nl;
-        lf[l] = fl;
-        lm[l] = cm;
-        cm += nl;
-        int nb = (int)((nl + 255) / 256);
-        restrict_kernel<<<nb, 256, 0, s>>>(lf[l - 1], lm[l - 1], shapes[l - 1].first, shapes[l - 1].second, fl,
-                                           const_cast<uint8_t*>(lm[l]), shapes[l].first, shapes[l].second);
+        RestrictBatch RB{};
+        for (int j = 0; j < K; ++j) {
+            RB.f[j] = J[j].f[l - 1];
+            RB.m[j] = J[j].m[l - 1];
+            RB.fc[j] = const_cast<double*>(J[j].f[l]);
+            RB.mc[j] = const_cast<uint8_t*>(J[j].m[l]);
+        }
+        const size_t nl = (size_t)shapes[l].first * shapes[l].second;
+        restrict_kernel<<<dim3((unsigned)((nl + 255) / 256), K), 256, 0, sp>>>(
+            RB, shapes[l - 1].first, shapes[l - 1].second, shapes[l].first, shapes[l].second);
         ++*launches;
     }
+    me(sp);
     CUDA_CHECK(cudaGetLastError());
-    // coarse and mid levels: one thread-block-cluster launch (levels whose
-    // 16 row bands fit on chip), else one single-CTA launch for the tiny ones
+    const int first_solve = probe ? (int)probe->solves.size() : 0;
+    // ---- coarse and mid levels: one cluster per solve (levels whose 16 row
+    // bands fit on chip), else one single-CTA launch per solve for the tiny ones
     int l_start = L - 1;
-    if (ws.cluster_ok) {
-        ClusterLevels S{};
+    if (ws0.cluster_ok) {
+        ClusterBatch CB{};
         size_t smem = 0;
+        int nlev = 0;
         int l = L - 1;
-        while (l >= 0 && S.nlev < kClMaxLevels) {
-            const int h = shapes[l].first, w = shapes[l].second;
-            const int br = (h + kClusterSize - 1) / kClusterSize;
+        while (l >= 0 && nlev < kClMaxLevels) {
+            const int hh = shapes[l].first, ww = shapes[l].second;
+            const int br = (hh + kClusterSize - 1) / kClusterSize;
             const size_t need =
-                ((size_t)(br + 2) * (w + 2) + (size_t)br * w + 6 * (size_t)w) * sizeof(double) + (size_t)br * w;
-            if ((size_t)br * w > (size_t)kClPx * kClThreads || w > kClMaxW || need > 200 * 1024) break;
-            const int i = S.nlev++;
-            S.h[i] = h;
-            S.w[i] = w;
-            S.f[i] = lf[l];
-            S.m[i] = lm[l];
-            S.u[i] = lu[l];
-            S.iters[i] = ws.iters + (L - 1 - l);
+                ((size_t)(br + 2) * (ww + 2) + (size_t)br * ww + 6 * (size_t)ww) * sizeof(double) + (size_t)br * ww;
+            if ((size_t)br * ww > (size_t)kClPx * kClThreads || ww > kClMaxW || need > 200 * 1024) break;
+            for (int j = 0; j < K; ++j) {
+                ClusterLevels& S = CB.S[j];
+                S.h[nlev] = hh;
+                S.w[nlev] = ww;
+                S.f[nlev] = J[j].f[l];
+                S.m[nlev] = J[j].m[l];
+                S.u[nlev] = J[j].u[l];
+                S.iters[nlev] = jobs[j].ws->iters + (L - 1 - l);
+            }
+            ++nlev;
             smem = std::max(smem, need);
             --l;
         }
-        if (S.nlev > 0) {
-            S.uc0 = nullptr;
-            S.last_is_finest = l < 0;
-            if (getenv("HIVC_CG_TRACE_CLUSTER")) {
-                if (!ws.trace) CUDA_CHECK(cudaMalloc(&ws.trace, kTraceLen * sizeof(unsigned long long)));
-                CUDA_CHECK(cudaMemsetAsync(ws.trace, 0, kTraceLen * sizeof(unsigned long long), s));
-                S.trace = ws.trace;
+        if (nlev > 0) {
+            for (int j = 0; j < K; ++j) {
+                ClusterLevels& S = CB.S[j];
+                S.nlev = nlev;
+                S.uc0 = nullptr;
+                S.last_is_finest = l < 0;
+                S.tol = tol;
+                S.max_iter = max_iter;
+                S.trace = nullptr;
             }
-            S.tol = tol;
-            S.max_iter = max_iter;
+            if (getenv("HIVC_CG_TRACE_CLUSTER") && K == 1) {
+                if (!ws0.trace) CUDA_CHECK(cudaMalloc(&ws0.trace, kTraceLen * sizeof(unsigned long long)));
+                CUDA_CHECK(cudaMemsetAsync(ws0.trace, 0, kTraceLen * sizeof(unsigned long long), sp));
+                CB.S[0].trace = ws0.trace;
+            }
             cudaLaunchConfig_t cfg = {};
-            cfg.gridDim = dim3(kClusterSize);
+            cfg.gridDim = dim3(kClusterSize * K);
             cfg.blockDim = dim3(kClThreads);
             cfg.dynamicSmemBytes = smem;
-            cfg.stream = s;
+            cfg.stream = sp;
             cudaLaunchAttribute attr[1];
             attr[0].id = cudaLaunchAttributeClusterDimension;
             attr[0].val.clusterDim.x = kClusterSize;
@@ -507,129 +658,187 @@ int solve_homogeneous_async(InpaintWorkspace& ws, cudaStream_t s, const double* 
             attr[0].val.clusterDim.z = 1;
             cfg.attrs = attr;
             cfg.numAttrs = 1;
-            CUDA_CHECK(cudaLaunchKernelEx(&cfg, cg_cluster_kernel, S));
+            mb("cluster nlev=" + std::to_string(nlev), sp);
+            CUDA_CHECK(cudaLaunchKernelEx(&cfg, cg_cluster_kernel, CB));
+            me(sp);
             ++*launches;
             l_start = l;
         }
     }
-    if (ws.small_enabled && l_start == L - 1) {
-        SmallLevels S{};
-        size_t smem = 0;
-        int l = L - 1;
-        while (l >= 0 && (size_t)shapes[l].first * shapes[l].second <= (size_t)kSmallMaxPx &&
-               S.nlev < kSmallMaxLevels) {
-            const int i = S.nlev++;
-            S.h[i] = shapes[l].first;
-            S.w[i] = shapes[l].second;
-            S.f[i] = lf[l];
-            S.m[i] = lm[l];
-            S.u[i] = lu[l];
-            S.iters[i] = ws.iters + (L - 1 - l);
-            const size_t n = (size_t)S.h[i] * S.w[i];
-            smem = std::max(smem, ((size_t)(S.h[i] + 2) * (S.w[i] + 2) + n) * sizeof(double) + n);
-            --l;
+    if (ws0.small_enabled && l_start == L - 1) {
+        int l_end = l_start;
+        for (int j = 0; j < K; ++j) {
+            SmallLevels S{};
+            size_t smem = 0;
+            int l = L - 1;
+            while (l >= 0 && (size_t)shapes[l].first * shapes[l].second <= (size_t)kSmallMaxPx &&
+                   S.nlev < kSmallMaxLevels) {
+                const int i = S.nlev++;
+                S.h[i] = shapes[l].first;
+                S.w[i] = shapes[l].second;
+                S.f[i] = J[j].f[l];
+                S.m[i] = J[j].m[l];
+                S.u[i] = J[j].u[l];
+                S.iters[i] = jobs[j].ws->iters + (L - 1 - l);
+                const size_t n = (size_t)S.h[i] * S.w[i];
+                smem = std::max(smem, ((size_t)(S.h[i] + 2) * (S.w[i] + 2) + n) * sizeof(double) + n);
+                --l;
+            }
+            if (S.nlev > 0) {
+                S.last_is_finest = l < 0;
+                S.tol = tol;
+                S.max_iter = max_iter;
+                cg_small_kernel<<<1, kSmallThreads, smem, sp>>>(S);
+                ++*launches;
+                CUDA_CHECK(cudaGetLastError());
+            }
+            l_end = l;
         }
-        if (S.nlev > 0) {
-            S.last_is_finest = l < 0;
-            S.tol = tol;
-            S.max_iter = max_iter;
-            cg_small_kernel<<<1, kSmallThreads, smem, s>>>(S);
-            ++*launches;
-            CUDA_CHECK(cudaGetLastError());
-            l_start = l;
-        }
+        l_start = l_end;
     }
+    if (sp != s) {  // the grid levels (and the caller's next work on s) follow the side-stream levels
+        if (!ws0.pre_done) CUDA_CHECK(cudaEventCreateWithFlags(&ws0.pre_done, cudaEventDisableTiming));
+        CUDA_CHECK(cudaEventRecord(ws0.pre_done, sp));
+        CUDA_CHECK(cudaStreamWaitEvent(s, ws0.pre_done, 0));
+    }
+    // ---- remaining (large) levels
     for (int l = l_start; l >= 0; --l) {
-        CgParams P;
-        P.h = shapes[l].first;
-        P.w = shapes[l].second;
-        P.n = P.h * P.w;
-        P.f = lf[l];
-        P.m = lm[l];
-        P.uc = l == L - 1 ? nullptr : lu[l + 1];
-        P.hc = l == L - 1 ? 0 : shapes[l + 1].first;
-        P.wc = l == L - 1 ? 0 : shapes[l + 1].second;
-        P.x = x;
-        P.r = r;
-        P.pa = pa;
-        P.pb = pb;
-        P.ap = ap;
-        P.u = lu[l];
-        P.tol = l == 0 ? tol : std::max(kLevelTol, tol);
-        P.max_iter = max_iter;
-        P.finest = l == 0;
-        P.partials = ws.partials;
-        P.bar = ws.bar;
-        P.iters = ws.iters + (L - 1 - l);
-        P.margin = ws.margins + (L - 1 - l);
-        const bool grid = !(P.n <= kSingleCtaMaxPx || ws.grid_ctas == 0);
+        std::vector<CgParams> P(K);
+        for (int j = 0; j < K; ++j) P[j] = level_params(J[j], *jobs[j].ws, shapes, l, tol, max_iter);
+        const int hh = P[0].h, ww = P[0].w;
+        const bool grid = !(P[0].n <= kSingleCtaMaxPx || ws0.grid_ctas == 0);
+        // on-chip band kernel when a band fits registers + shared memory
+        const int kc = (ww + kBandThreads - 1) / kBandThreads;
+        int band_rows = (hh + ws0.num_sms - 1) / std::max(ws0.num_sms, 1);
+        const bool pack = ws0.pack_bands && !ws0.pack_env_off && ws0.band_variant == 2 && kc <= 2 &&
+                          band_rows <= kPackRows;
+        if (pack) band_rows = kPackRows;
+        const int nbands = (hh + band_rows - 1) / band_rows;
+        const size_t band_smem = (size_t)(kBandRows + 2) * (ww + 2) * sizeof(double) + (size_t)kBandRows * ww;
+        const bool band = grid && ws0.band_enabled && P[0].uc != nullptr && (pack || band_rows <= kBandRows) &&
+                          ww <= kBandCols * kBandThreads && band_smem <= 220 * 1024 && nbands <= ws0.num_sms;
         CgProbe::Launch rec{};
         if (probe && grid) {
+            rec.stamp_base = probe->next_stamp;
+            probe->next_stamp += K;
+            for (int j = 0; j < K; ++j) P[j].stamp = probe->stamp_slot(rec.stamp_base + j);
+        }
+        auto rec_begin = [&]() {
+            if (!(probe && grid)) return;
             CUDA_CHECK(cudaEventCreate(&rec.start));
             CUDA_CHECK(cudaEventCreate(&rec.stop));
             CUDA_CHECK(cudaEventRecord(rec.start, s));
-        }
-        // on-chip band kernel when a band fits registers + shared memory
-        const int kc = (P.w + kBandThreads - 1) / kBandThreads;
-        int band_rows = (P.h + ws.num_sms - 1) / std::max(ws.num_sms, 1);
-        const bool pack = ws.pack_bands && !ws.pack_env_off && ws.band_variant == 2 && kc <= 2 && band_rows <= kPackRows;
-        if (pack) band_rows = kPackRows;
-        const int nbands = (P.h + band_rows - 1) / band_rows;
-        const size_t band_smem = (size_t)(kBandRows + 2) * (P.w + 2) * sizeof(double) + (size_t)kBandRows * P.w;
-        const bool band = grid && ws.band_enabled && P.uc != nullptr && (pack || band_rows <= kBandRows) &&
-                          P.w <= kBandCols * kBandThreads && band_smem <= 220 * 1024 && nbands <= ws.num_sms;
-        if (grid) CUDA_CHECK(cudaMemsetAsync(ws.bar, 0, sizeof(unsigned int), s));  // barrier epoch counter
-        if (probe && grid) P.stamp = probe->stamp_slot((int)probe->launches.size());
+        };
         if (!grid) {
-            cg_level_kernel<false><<<1, kThreads, 0, s>>>(P);
+            rec_begin();
+            for (int j = 0; j < K; ++j) {
+                cg_level_kernel<false><<<1, kThreads, 0, s>>>(P[j]);
+                ++*launches;
+            }
         } else if (band) {
-            P.band_rows = band_rows;
-            P.ex_r = ws.ex;
-            P.ex_p = ws.ex + (size_t)2 * nbands * P.w;
-            double* setup = ws.partials + 4096;
-            if (getenv("HIVC_CG_TRACE") && l == 0) {
-                if (!ws.trace) CUDA_CHECK(cudaMalloc(&ws.trace, kTraceLen * sizeof(unsigned long long)));
-                CUDA_CHECK(cudaMemsetAsync(ws.trace, 0, kTraceLen * sizeof(unsigned long long), s));
-                P.trace = ws.trace;
+            SetupBatch SB{};
+            BandBatch BB{};
+            for (int j = 0; j < K; ++j) {
+                InpaintWorkspace& ws = *jobs[j].ws;
+                P[j].band_rows = band_rows;
+                P[j].ex_r = ws.ex;
+                P[j].ex_p = ws.ex + (size_t)2 * nbands * ww;
+                SB.P[j] = P[j];
+                SB.partials[j] = ws.partials + 4096;
+                BB.P[j] = P[j];
+                BB.setup[j] = ws.partials + 4096;
             }
-            cg_setup_x_kernel<<<kSetupCtas, 512, 0, s>>>(P);
-            cg_setup_kernel<<<kSetupCtas, 512, 0, s>>>(P, setup);
+            if (getenv("HIVC_CG_TRACE") && l == 0 && K == 1) {
+                if (!ws0.trace) CUDA_CHECK(cudaMalloc(&ws0.trace, kTraceLen * sizeof(unsigned long long)));
+                CUDA_CHECK(cudaMemsetAsync(ws0.trace, 0, kTraceLen * sizeof(unsigned long long), s));
+                SB.P[0].trace = BB.P[0].trace = ws0.trace;
+            }
+            unsigned int* ticket = ws0.bar + 32;
+            SB.ticket = pack && K > 1 ? ticket : nullptr;  // setup resets the barrier counters + ticket
+            mb("setup l=" + std::to_string(l), s);
+            cg_setup_x_kernel<<<dim3(kSetupCtas, K), 512, 0, s>>>(SB);
+            cg_setup_kernel<<<dim3(kSetupCtas, K), 512, 0, s>>>(SB);
+            me(s);
             *launches += 2;
-            void* args[] = {&P, &setup};
-            const void* fn = (const void*)cg_band_kernel;
-            size_t smem_b = band_smem;
-            if (pack) {
-                smem_b = (size_t)(kPackRows + 2) * (P.w + 2) * sizeof(double);
-                fn = (const void*)cg_band2_kernel<kPackRows, 2, false>;
-            } else if (ws.band_variant == 2) {
-                smem_b = (size_t)(kBandRows + 2) * (P.w + 2) * sizeof(double);
-                fn = (band_rows <= 4 && kc <= 2) ? (const void*)cg_band2_kernel<4, 2, true>
-                                                 : (const void*)cg_band2_kernel<8, 4, false>;
+            mb(std::string(pack && K > 1 ? "band-ticket" : "band-coop") + " l=" + std::to_string(l) + " nb=" +
+                   std::to_string(nbands),
+               s);
+            rec_begin();
+            if (pack && K > 1) {
+                // several solves side by side: ticketed plain launch (see BandBatch)
+                BB.nb = nbands;
+                BB.ticket = ticket;
+                const size_t smem_b = band2_smem(kPackRows, band_rows, ww, BB.P, K);
+                cg_band2_kernel<kPackRows, 2, false><<<nbands * K, kBandThreads, smem_b, s>>>(BB);
+                ++*launches;
+            } else {
+                for (int j = 0; j < K; ++j) {
+                    if (ws0.band_variant == 2) {
+                        BandBatch one{};
+                        one.P[0] = BB.P[j];
+                        one.setup[0] = BB.setup[j];
+                        one.nb = nbands;
+                        one.ticket = nullptr;
+                        const void* fn;
+                        size_t smem_b;
+                        if (pack) {
+                            smem_b = band2_smem(kPackRows, band_rows, ww, one.P, 1);
+                            fn = (const void*)cg_band2_kernel<kPackRows, 2, false>;
+                        } else {
+                            const bool small = band_rows <= 4 && kc <= 2;
+                            smem_b = band2_smem(small ? 4 : kBandRows, band_rows, ww, one.P, 1);
+                            fn = small ? (const void*)cg_band2_kernel<4, 2, true>
+                                       : (const void*)cg_band2_kernel<8, 4, false>;
+                        }
+                        void* args[] = {&one};
+                        CUDA_CHECK(cudaLaunchCooperativeKernel(fn, dim3(nbands), dim3(kBandThreads), args, smem_b, s));
+                    } else {
+                        const double* setup = BB.setup[j];
+                        void* args[] = {&BB.P[j], &setup};
+                        CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)cg_band_kernel, dim3(nbands),
+                                                               dim3(kBandThreads), args, band_smem, s));
+                    }
+                    ++*launches;
+                    if (l == 0 && jobs[j].done) {  // this solve is complete: its consumer may start now
+                        CUDA_CHECK(cudaEventRecord(jobs[j].done, s));
+                        recorded[j] = true;
+                    }
+                }
             }
-            CUDA_CHECK(cudaLaunchCooperativeKernel(fn, dim3(nbands), dim3(kBandThreads), args, smem_b, s));
         } else {
-            void* args[] = {&P};
-            CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)cg_level_kernel<true>, dim3(ws.grid_ctas),
-                                                   dim3(kThreads), args, 0, s));
+            rec_begin();
+            for (int j = 0; j < K; ++j) {
+                CUDA_CHECK(cudaMemsetAsync(jobs[j].ws->bar, 0, sizeof(unsigned int), s));  // barrier epoch counter
+                void* args[] = {&P[j]};
+                CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)cg_level_kernel<true>, dim3(ws0.grid_ctas),
+                                                       dim3(kThreads), args, 0, s));
+                ++*launches;
+            }
         }
-        ++*launches;
         CUDA_CHECK(cudaGetLastError());
+        if (band) me(s);
         if (probe && grid) {
             CUDA_CHECK(cudaEventRecord(rec.stop, s));
-            rec.pixels = P.n;
-            rec.solve = (int)probe->solves.size();
+            rec.pixels = P[0].n;
+            rec.first_solve = first_solve;
+            rec.nsolves = K;
             rec.level = L - 1 - l;
             probe->launches.push_back(rec);
         }
     }
+    for (int j = 0; j < K; ++j)
+        if (jobs[j].done && !recorded[j]) CUDA_CHECK(cudaEventRecord(jobs[j].done, s));
     if (probe) {
-        // per-level iteration counts of this solve, read back after the stream syncs
-        CgProbe::Solve sv;
-        sv.nlevels = L;
-        for (int l = 0; l < L; ++l) sv.pixels[l] = (int64_t)shapes[L - 1 - l].first * shapes[L - 1 - l].second;
-        sv.host_iters = probe->alloc_iters();
-        if (sv.host_iters) CUDA_CHECK(cudaMemcpyAsync(sv.host_iters, ws.iters, L * sizeof(int), cudaMemcpyDeviceToHost, s));
-        probe->solves.push_back(sv);
+        // per-level iteration counts of each solve, read back after the stream syncs
+        for (int j = 0; j < K; ++j) {
+            CgProbe::Solve sv;
+            sv.nlevels = L;
+            for (int l = 0; l < L; ++l) sv.pixels[l] = (int64_t)shapes[L - 1 - l].first * shapes[L - 1 - l].second;
+            sv.host_iters = probe->alloc_iters();
+            if (sv.host_iters)
+                CUDA_CHECK(cudaMemcpyAsync(sv.host_iters, jobs[j].ws->iters, L * sizeof(int), cudaMemcpyDeviceToHost, s));
+            probe->solves.push_back(sv);
+        }
     }
     return L;
 }
@@ -651,7 +860,22 @@ unsigned long long* CgProbe::stamp_slot(int i) {
     return stamps_dev + 2 * i;
 }
 
+void CgProbe::mark_begin(cudaStream_t s, const std::string& label) {
+    Mark m{label, nullptr, nullptr};
+    CUDA_CHECK(cudaEventCreate(&m.a));
+    CUDA_CHECK(cudaEventCreate(&m.b));
+    CUDA_CHECK(cudaEventRecord(m.a, s));
+    marks.push_back(m);
+}
+
+void CgProbe::mark_end(cudaStream_t s) { CUDA_CHECK(cudaEventRecord(marks.back().b, s)); }
+
 void CgProbe::reset() {
+    for (auto& m : marks) {
+        cudaEventDestroy(m.a);
+        cudaEventDestroy(m.b);
+    }
+    marks.clear();
     for (auto& l : launches) {
         if (l.start) cudaEventDestroy(l.start);
         if (l.stop) cudaEventDestroy(l.stop);
@@ -659,6 +883,7 @@ void CgProbe::reset() {
     launches.clear();
     solves.clear();
     used = 0;
+    next_stamp = 0;
 }
 
 CgProbe::~CgProbe() {
@@ -668,6 +893,17 @@ CgProbe::~CgProbe() {
 }
 
 void CgProbe::harvest(CgTotals& t) {
+    if (!marks.empty()) {
+        float t0 = 0;
+        for (auto& m : marks) {
+            float a = 0, d = 0;
+            cudaEventElapsedTime(&a, marks[0].a, m.a);
+            cudaEventElapsedTime(&d, m.a, m.b);
+            std::fprintf(stderr, "[batch] %-28s start %9.1f us  dur %8.1f us\n", m.label.c_str(), a * 1e3, d * 1e3);
+            t0 = a;
+        }
+        (void)t0;
+    }
     // after the stream synchronised: accumulate iteration-weighted pixel counts
     // and the grid-mode launches' device time
     std::vector<int> it_of_solve_level;
@@ -684,23 +920,37 @@ void CgProbe::harvest(CgTotals& t) {
     // behind other lanes' kernels, so they are only the fallback
     std::vector<unsigned long long> st;
     if (stamps_dev && !launches.empty()) {
-        st.resize(2 * std::min<size_t>(launches.size(), kStampCap));
+        st.resize(2 * std::min<size_t>(next_stamp, kStampCap));
         cudaMemcpy(st.data(), stamps_dev, st.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
         cudaMemset(stamps_dev, 0, st.size() * sizeof(unsigned long long));
     }
     for (size_t i = 0; i < launches.size(); ++i) {
         const Launch& l = launches[i];
+        // span of the launch: first solve's entry to last solve's exit
+        unsigned long long t0 = ~0ull, t1 = 0;
+        bool ok = true;
+        for (int j = 0; j < l.nsolves; ++j) {
+            const size_t k = 2 * (size_t)(l.stamp_base + j);
+            if (k + 1 >= st.size() || !st[k] || st[k + 1] <= st[k]) {
+                ok = false;
+                break;
+            }
+            t0 = std::min(t0, st[k]);
+            t1 = std::max(t1, st[k + 1]);
+        }
         float ms = 0;
-        if (2 * i + 1 < st.size() && st[2 * i] && st[2 * i + 1] > st[2 * i])
-            ms = (float)((st[2 * i + 1] - st[2 * i]) * 1e-6);
+        if (ok && l.nsolves > 0)
+            ms = (float)((t1 - t0) * 1e-6);
         else
             cudaEventElapsedTime(&ms, l.start, l.stop);
-        const Solve& sv = solves[l.solve];
-        int it = sv.host_iters ? sv.host_iters[l.level] : 0;
         t.grid_launches += 1;
         t.grid_seconds += ms * 1e-3;
-        t.grid_pixel_iters += l.pixels * it;
-        t.grid_pixels += l.pixels;
+        for (int j = 0; j < l.nsolves; ++j) {
+            const Solve& sv = solves[l.first_solve + j];
+            const int it = sv.host_iters ? sv.host_iters[l.level] : 0;
+            t.grid_pixel_iters += l.pixels * it;
+            t.grid_pixels += l.pixels;
+        }
     }
     reset();
 }

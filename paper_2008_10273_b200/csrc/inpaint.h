@@ -19,6 +19,7 @@
 
 namespace hivc {
 
+constexpr int kMaxBatch = 16;  // solves per batched launch
 constexpr int kTraceLen = 2048 + 256 * 160;  // HIVC_CG_TRACE: phase stamps + per-CTA arrival stamps
 
 // Device scratch for one solve at a time (per stream): finest-level CG
@@ -45,9 +46,13 @@ struct InpaintWorkspace {
     unsigned int* bar = nullptr;
     int* iters = nullptr;      // device: per level (coarse -> fine) CG iterations
     double* margins = nullptr; // device: per level min relative stop-test margin
+    cudaEvent_t pre_done = nullptr;  // solve_batch_async: side-stream levels done
     void reserve(int h, int w, int dev);
     void release();
-    ~InpaintWorkspace() { release(); }
+    ~InpaintWorkspace() {
+        release();
+        if (pre_done) cudaEventDestroy(pre_done);
+    }
 };
 
 void pyramid_shapes(int h, int w, std::vector<std::pair<int, int>>& shapes);
@@ -66,10 +71,11 @@ struct CgTotals {
 // Optional per-solve probe: CUDA events around every cooperative level
 // kernel and an async copy of the per-level iteration counts to pinned memory.
 struct CgProbe {
-    struct Launch {
+    struct Launch {  // one level launch covering solves [first_solve, first_solve + nsolves)
         cudaEvent_t start = nullptr, stop = nullptr;
-        int64_t pixels = 0;
-        int solve = 0, level = 0;
+        int64_t pixels = 0;  // per solve
+        int first_solve = 0, nsolves = 1, level = 0;
+        int stamp_base = 0;  // stamp slots stamp_base + j (entry/exit of solve j's band 0)
     };
     struct Solve {
         int nlevels = 0;
@@ -82,6 +88,16 @@ struct CgProbe {
     std::vector<Solve> solves;
     int* host = nullptr;
     int used = 0;
+    int next_stamp = 0;
+    // HIVC_BATCH_TRACE: labelled event pairs around each phase of a batched
+    // solve, printed (stderr) by harvest
+    struct Mark {
+        std::string label;
+        cudaEvent_t a, b;
+    };
+    std::vector<Mark> marks;
+    void mark_begin(cudaStream_t s, const std::string& label);
+    void mark_end(cudaStream_t s);
     unsigned long long* stamps_dev = nullptr;  // [kStampCap][2] globaltimer entry/exit per launch
     int* alloc_iters();
     unsigned long long* stamp_slot(int i);
@@ -95,6 +111,25 @@ struct CgProbe {
 // iteration counts land in ws.iters (coarse -> fine) on the device.
 int solve_homogeneous_async(InpaintWorkspace& ws, cudaStream_t s, const double* f, const uint8_t* m, int h, int w,
                             double tol, int max_iter, double* u_out, int64_t* launches, CgProbe* probe = nullptr);
+
+// K (<= 16) same-shape solves in one set of launches on stream s: batched
+// pyramid, one thread-block cluster per solve for the coarse levels, and for
+// the large levels either one ticketed launch running the solves side by side
+// (throughput mode, w <= 1024) or one cooperative launch per solve.  Every
+// job needs its own workspace.  Spinning (grid-barrier) launches must not run
+// concurrently with another batch's: issue all batches on one stream.
+struct SolveJob {
+    InpaintWorkspace* ws;
+    const double* f;
+    const uint8_t* m;
+    double* u;
+    cudaEvent_t done = nullptr;  // optional: recorded on s as soon as this job's solution is complete
+};
+// s_pre (optional): stream for the pyramid and the cluster/single-CTA levels;
+// the finest levels (grid barriers) follow on s.  Either way the solution is
+// complete in stream order on s.
+int solve_batch_async(const SolveJob* jobs, int K, int h, int w, double tol, int max_iter, cudaStream_t s,
+                      int64_t* launches, CgProbe* probe = nullptr, cudaStream_t s_pre = nullptr);
 
 // Relative residual of the inpainting equation (homogeneous.py:206-211);
 // synchronises the stream.  Returns -1 when ||f|mask|| == 0.

@@ -3,7 +3,14 @@
 
 #include <algorithm>
 #include <cmath>
+#include <atomic>
 #include <cstring>
+#include <exception>
+#include <thread>
+
+#include <sys/resource.h>
+#include <sys/syscall.h>
+#include <unistd.h>
 
 namespace hivc {
 
@@ -255,49 +262,306 @@ void split_gops(const uint8_t* d, size_t len, const StreamHeader& h, std::vector
 
 // ---------------------------------------------------------------- intra payload
 
-static size_t intra_tree(const uint8_t* d, size_t len, size_t pos, int32_t h, int32_t w, std::vector<int32_t>& pts,
-                         std::vector<uint64_t>& bits) {
-    // prediction._read_tree (prediction.py:149-159) + mask points in raster
-    // order (_mask_points, prediction.py:117-119)
-    if (pos + 4 > len) fail(HIVC_E_TRUNCATED_STREAM, "intra payload truncated");
-    uint32_t nbits = rd_u32(d + pos);
-    pos += 4;
-    size_t nbytes = ((size_t)nbits + 7) / 8;
-    if (pos + nbytes > len) fail(HIVC_E_TRUNCATED_STREAM, "intra payload truncated");
-    BitReader rd(d + pos, nbytes, nbits);
-    const size_t npx = (size_t)h * w;
-    bits.assign((npx + 63) / 64, 0);
-    size_t nleaves = 0;
-    walk_tree(rd, w, h, [&](int32_t x, int32_t y, int32_t rw, int32_t rh) {
-        const size_t i = (size_t)(y + rh / 2) * w + (x + rw / 2);
-        bits[i >> 6] |= 1ull << (i & 63);
-        ++nleaves;
-    });
-    pts.clear();
-    pts.reserve(nleaves);
-    for (size_t wi = 0; wi < bits.size(); ++wi) {
-        uint64_t b = bits[wi];
-        while (b) {
-            int t = __builtin_ctzll(b);
-            pts.push_back((int32_t)(wi * 64 + t));
-            b &= b - 1;
+// Preorder walk of an intra mask tree (subdivision.py:198-222) with the
+// current rectangle in registers: a split bit continues into the first child
+// and pushes the second, a leaf bit ORs the leaf centre into the mask bitmap
+// (prediction.py:117-119) and pops — selected without branches, since split
+// and leaf bits alternate unpredictably.  Rectangles are packed 4 x 16 bits.
+// Bits come from a look-ahead buffer without per-bit limit checks: reads past
+// the tree's bit length see zeros (leaves, so the walk winds down) and the
+// length is checked once at the end — and before reporting a bad split, so
+// the error is the one a bit-by-bit reader raises first.  The bitmap has
+// `stride` bits per row and its origin at plane pixel (x0, y0).
+static uint64_t intra_tree_walk(const uint8_t* d, size_t nbytes, uint64_t nbits, uint64_t start, int32_t x, int32_t y,
+                                int32_t w, int32_t h, int32_t x0, int32_t y0, size_t stride, uint64_t* bits,
+                                size_t& nleaves) {
+    constexpr int kCap = 128;  // >= log2(area) + 1 pending rectangles: unreachable (areas halve)
+    uint64_t st[kCap + 2];
+    size_t next = (size_t)(start >> 3);
+    uint64_t buf = 0;
+    int avail = 0;
+    auto refill = [&]() {
+        while (avail <= 56) {
+            const uint64_t v = next < nbytes ? d[next] : 0;
+            ++next;
+            buf |= v << (56 - avail);
+            avail += 8;
+        }
+    };
+    refill();
+    {
+        const int drop = (int)(start & 7);
+        buf <<= drop;
+        avail -= drop;
+    }
+    uint64_t used = 0;
+    uint64_t cur = (uint64_t)(uint16_t)x | (uint64_t)(uint16_t)y << 16 | (uint64_t)(uint16_t)w << 32 |
+                   (uint64_t)(uint16_t)h << 48;
+    int sp = 1;  // st[0] is a sentinel (never popped: the walk ends first)
+    st[0] = 0;
+    size_t nl = 0;
+    for (;;) {
+        if (avail == 0) refill();
+        const uint32_t b = (uint32_t)(buf >> 63);
+        buf <<= 1;
+        --avail;
+        ++used;
+        const int32_t cx = (int32_t)(cur & 0xFFFF), cy = (int32_t)((cur >> 16) & 0xFFFF);
+        const int32_t cw = (int32_t)((cur >> 32) & 0xFFFF), ch = (int32_t)(cur >> 48);
+        if (b & (uint32_t)(cw == 1) & (uint32_t)(ch == 1)) {
+            if (start + used > nbits) fail(HIVC_E_TRUNCATED_STREAM, "bit stream exhausted");
+            fail(HIVC_E_SUBDIVISION, "split of a single pixel");
+        }
+        const size_t i = (size_t)(cy + (ch >> 1) - y0) * stride + (size_t)(cx + (cw >> 1) - x0);
+        bits[i >> 6] |= (uint64_t)(b ^ 1u) << (i & 63);
+        nl += b ^ 1u;
+        if (!b && sp == 1) break;
+        const bool sh = ch > cw;  // halve the longer side, ties halve the width; first half rounded up
+        const int32_t t = ((sh ? ch : cw) + 1) >> 1;
+        const uint64_t first = sh ? (cur & 0x0000FFFFFFFFFFFFull) | (uint64_t)t << 48
+                                  : (cur & 0xFFFF0000FFFFFFFFull) | (uint64_t)t << 32;
+        const uint64_t second = sh ? (cur + ((uint64_t)t << 16)) - ((uint64_t)t << 48)
+                                   : (cur + (uint64_t)t) - ((uint64_t)t << 32);
+        const uint64_t popped = st[sp - 1];
+        st[sp] = second;
+        cur = b ? first : popped;
+        sp += (int)(2 * b) - 1;
+        if (sp > kCap) fail(HIVC_E_SUBDIVISION, "subdivision tree too deep");
+    }
+    if (start + used > nbits) fail(HIVC_E_TRUNCATED_STREAM, "bit stream exhausted");
+    nleaves = nl;
+    return start + used;
+}
+
+// Excess tables over MSB-first bytes: a leaf bit (0) counts +1, a split (1)
+// -1; a preorder subtree ends at the first bit where its excess reaches +1.
+static const struct ExcessTables {
+    int8_t net[256], maxp[256];
+    ExcessTables() {
+        for (int v = 0; v < 256; ++v) {
+            int c = 0, m = -100;
+            for (int k = 7; k >= 0; --k) {
+                c += ((v >> k) & 1) ? -1 : 1;
+                m = std::max(m, c);
+            }
+            net[v] = (int8_t)c;
+            maxp[v] = (int8_t)m;
         }
     }
+} kExcess;
+
+// First bit after the preorder subtree that starts at bit s.
+static uint64_t subtree_skip(const uint8_t* d, uint64_t nbits, uint64_t s) {
+    uint64_t pos = s;
+    int c = 0;
+    while (pos < nbits) {
+        if ((pos & 7) == 0 && pos + 8 <= nbits) {
+            const uint8_t v = d[pos >> 3];
+            if (c + kExcess.maxp[v] < 1) {
+                c += kExcess.net[v];
+                pos += 8;
+                continue;
+            }
+        }
+        c += ((d[pos >> 3] >> (7 - (pos & 7))) & 1) ? -1 : 1;
+        ++pos;
+        if (c == 1) return pos;
+    }
+    fail(HIVC_E_TRUNCATED_STREAM, "bit stream exhausted");
+}
+
+struct TreeTask {
+    uint64_t start;
+    int32_t x, y, w, h;
+    size_t off = 0, stride = 0, nleaves = 0;  // local bitmap (words) and its row stride (bits)
+    uint64_t end = 0;                         // first bit after the walked subtree
+};
+
+// Cut the tree at depth `depth` into independent subtrees (preorder).
+static void tree_tasks(const uint8_t* d, uint64_t nbits, uint64_t s, int32_t x, int32_t y, int32_t w, int32_t h,
+                       int depth, std::vector<TreeTask>& out) {
+    if (depth == 0 || s >= nbits || !((d[s >> 3] >> (7 - (s & 7))) & 1) || (w == 1 && h == 1)) {
+        out.push_back({s, x, y, w, h});
+        return;
+    }
+    int32_t ax, ay, aw, ah, bx, by, bw, bh;
+    if (h > w) {
+        const int32_t t = (h + 1) / 2;
+        ax = x, ay = y, aw = w, ah = t, bx = x, by = y + t, bw = w, bh = h - t;
+    } else {
+        const int32_t t = (w + 1) / 2;
+        ax = x, ay = y, aw = t, ah = h, bx = x + t, by = y, bw = w - t, bh = h;
+    }
+    tree_tasks(d, nbits, s + 1, ax, ay, aw, ah, depth - 1, out);
+    tree_tasks(d, nbits, subtree_skip(d, nbits, s + 1), bx, by, bw, bh, depth - 1, out);
+}
+
+// OR a (w x h) bitmap with a row stride of `stride` bits into the plane bitmap at (x0, y0).
+static void merge_rect_bits(const uint64_t* src, size_t stride, int32_t x0, int32_t y0, int32_t w, int32_t h,
+                            int32_t W, uint64_t* dst, size_t dst_words) {
+    const size_t nw = ((size_t)w + 63) / 64;
+    for (int32_t r = 0; r < h; ++r) {
+        const uint64_t* row = src + (size_t)r * (stride / 64);
+        const size_t g = (size_t)(y0 + r) * W + x0;
+        for (size_t k = 0; k < nw; ++k) {
+            uint64_t v = row[k];
+            if (!v) continue;
+            const size_t rem = (size_t)w - 64 * k;
+            if (rem < 64) v &= (1ull << rem) - 1;
+            const size_t gb = g + 64 * k, gw = gb >> 6, sh = gb & 63;
+            dst[gw] |= v << sh;
+            if (sh && gw + 1 < dst_words) dst[gw + 1] |= v >> (64 - sh);
+        }
+    }
+}
+
+// Run fn(i) for i in [0, n) on up to nthreads threads (the caller included).
+// Helper threads run at a lower priority (nice +3) than the decode's parse
+// workers: they soak up idle cores without delaying the smaller planes'
+// parses that gate the first solve batch.
+static void helper_priority() { setpriority(PRIO_PROCESS, (id_t)syscall(SYS_gettid), 3); }
+
+template <class F>
+static void parallel_for(int n, int nthreads, F&& fn) {
+    std::atomic<int> next{0};
+    auto body = [&]() {
+        for (int i; (i = next.fetch_add(1)) < n;) fn(i);
+    };
+    std::vector<std::thread> th;
+    for (int t = 1; t < std::min(n, nthreads); ++t)
+        th.emplace_back([&]() {
+            helper_priority();
+            body();
+        });
+    body();
+    for (auto& t : th) t.join();
+}
+
+// prediction._read_tree (prediction.py:149-159): returns the end of the tree payload
+static size_t intra_tree_span(const uint8_t* d, size_t len, size_t pos, uint32_t& nbits) {
+    if (pos + 4 > len) fail(HIVC_E_TRUNCATED_STREAM, "intra payload truncated");
+    nbits = rd_u32(d + pos);
+    const size_t nbytes = ((size_t)nbits + 7) / 8;
+    if (pos + 4 + nbytes > len) fail(HIVC_E_TRUNCATED_STREAM, "intra payload truncated");
+    return pos + 4 + nbytes;
+}
+
+// Sequential: mask bitmap of one tree (the exact reference error on a bad stream).
+static size_t intra_tree_seq(const uint8_t* d, size_t pos, uint32_t nbits, int32_t h, int32_t w,
+                             std::vector<uint64_t>& bits) {
+    bits.assign(((size_t)h * w + 63) / 64, 0);
+    size_t nleaves = 0;
+    intra_tree_walk(d + pos + 4, ((size_t)nbits + 7) / 8, nbits, 0, 0, 0, w, h, 0, 0, (size_t)w, bits.data(), nleaves);
+    return nleaves;
+}
+
+// Parallel: cut at depth 5 (32 subtrees), walk them into local bitmaps on
+// `threads` threads, merge; any failure reruns the sequential walk so the
+// error is the one a preorder walk meets first.
+static size_t intra_tree_par(const uint8_t* d, size_t pos, uint32_t nbits, int32_t h, int32_t w, int threads,
+                             std::vector<uint64_t>& bits, std::vector<uint64_t>& local) {
+    const uint8_t* tb = d + pos + 4;
+    const size_t nbytes = ((size_t)nbits + 7) / 8;
+    std::vector<TreeTask> tasks;
+    try {
+        tree_tasks(tb, nbits, 0, 0, 0, w, h, 5, tasks);
+    } catch (const Error&) {
+        return intra_tree_seq(d, pos, nbits, h, w, bits);
+    }
+    size_t words = 0;
+    for (TreeTask& t : tasks) {
+        t.stride = ((size_t)t.w + 63) / 64 * 64;
+        t.off = words;
+        words += (size_t)t.h * (t.stride / 64);
+    }
+    local.assign(words, 0);
+    std::atomic<bool> bad{false};
+    parallel_for((int)tasks.size(), threads, [&](int i) {
+        TreeTask& t = tasks[i];
+        try {
+            t.end = intra_tree_walk(tb, nbytes, nbits, t.start, t.x, t.y, t.w, t.h, t.x, t.y, t.stride,
+                                    local.data() + t.off, t.nleaves);
+        } catch (const Error&) {
+            bad = true;
+        }
+    });
+    if (bad) return intra_tree_seq(d, pos, nbits, h, w, bits);
+    bits.assign(((size_t)h * w + 63) / 64, 0);
+    size_t nleaves = 0;
+    for (const TreeTask& t : tasks) {
+        merge_rect_bits(local.data() + t.off, t.stride, t.x, t.y, t.w, t.h, w, bits.data(), bits.size());
+        nleaves += t.nleaves;
+    }
+    return nleaves;
+}
+
+// Raster-ordered mask points (flat indices) of a bitmap; `threads` ranges in parallel.
+static void intra_points(const std::vector<uint64_t>& bits, size_t nleaves, std::vector<int32_t>& pts, int threads) {
+    const size_t nw = bits.size();
+    const int nr = threads > 1 ? threads * 4 : 1;
+    std::vector<size_t> base(nr + 1, 0);
+    auto range = [&](int r, size_t& a, size_t& b) {
+        a = nw * r / nr;
+        b = nw * (r + 1) / nr;
+    };
+    parallel_for(nr, threads, [&](int r) {
+        size_t a, b, c = 0;
+        range(r, a, b);
+        for (size_t i = a; i < b; ++i) c += (size_t)__builtin_popcountll(bits[i]);
+        base[r + 1] = c;
+    });
+    for (int r = 0; r < nr; ++r) base[r + 1] += base[r];
+    if (base[nr] != nleaves) fail(HIVC_E_SUBDIVISION, "mask leaf count mismatch");
+    pts.resize(nleaves);
+    parallel_for(nr, threads, [&](int r) {
+        size_t a, b;
+        range(r, a, b);
+        int32_t* o = pts.data() + base[r];
+        for (size_t wi = a; wi < b; ++wi) {
+            uint64_t v = bits[wi];
+            while (v) {
+                *o++ = (int32_t)(wi * 64 + __builtin_ctzll(v));
+                v &= v - 1;
+            }
+        }
+    });
+}
+
+// End of an entropy.decode_symbols payload without decoding it (entropy.py:227-240, 276-291).
+static size_t symbols_span(const uint8_t* d, size_t len, size_t pos) {
+    if (pos >= len) fail(HIVC_E_TRUNCATED_STREAM, "entropy payload truncated");
+    const int tl = d[pos++];
+    if (tl < 5 || tl > 12) fail(HIVC_E_ENTROPY, "bad table_log " + std::to_string(tl));
+    const uint64_t nsym = read_uvarint(d, len, pos);
+    if (nsym == 0 || nsym > (1ull << tl)) fail(HIVC_E_ENTROPY, "bad alphabet size");
+    for (uint64_t i = 0; i < nsym; ++i) read_uvarint(d, len, pos);
+    if (pos + 10 > len) fail(HIVC_E_TRUNCATED_STREAM, "entropy payload truncated");
+    const uint32_t bit_len = rd_u32(d + pos + 6);
+    pos += 10;
+    const size_t nbytes = ((size_t)bit_len + 7) / 8;
+    if (pos + nbytes > len) fail(HIVC_E_TRUNCATED_STREAM, "entropy payload truncated");
     return pos + nbytes;
 }
 
-static size_t intra_values(const uint8_t* d, size_t len, size_t pos, int levels, size_t npts, std::vector<double>& out) {
-    // prediction._decode_plane_values (prediction.py:133-139) + uniform_dequantize (quantize.py:78-82)
+// prediction._decode_plane_values (prediction.py:133-139): lo/hi, then the symbols.
+static size_t intra_values_span(const uint8_t* d, size_t len, size_t pos) {
     if (pos + 4 > len) fail(HIVC_E_TRUNCATED_STREAM, "intra payload truncated");
+    return symbols_span(d, len, pos + 4);
+}
+
+static void intra_symbols(const uint8_t* d, size_t len, size_t pos, std::vector<int32_t>& idx) {
+    decode_symbols(d, len, pos + 4, idx);
+}
+
+static void intra_dequantize(const uint8_t* d, size_t pos, int levels, const std::vector<int32_t>& idx, size_t npts,
+                             std::vector<double>& out) {
+    // uniform_dequantize (quantize.py:78-82)
     int16_t lo, hi;
     std::memcpy(&lo, d + pos, 2);
     std::memcpy(&hi, d + pos + 2, 2);
-    pos += 4;
-    std::vector<int32_t> idx;
-    pos = decode_symbols(d, len, pos, idx);
-    double flo = lo, fhi = hi;
+    const double flo = lo, fhi = hi;
     if (!(flo < fhi)) fail(HIVC_E_QUANTIZE, "need lo < hi");
-    double step = (fhi - flo) / (double)(levels - 1);
+    const double step = (fhi - flo) / (double)(levels - 1);
     // f.ravel()[points] = values (prediction.py:205): numpy broadcasts a
     // single value, any other length mismatch is a ValueError.
     if (idx.size() != npts && idx.size() != 1)
@@ -305,21 +569,82 @@ static size_t intra_values(const uint8_t* d, size_t len, size_t pos, int levels,
                                   std::to_string(npts) + " mask points");
     out.resize(npts);
     for (size_t i = 0; i < npts; ++i) out[i] = flo + (double)idx[idx.size() == 1 ? 0 : i] * step;
-    return pos;
 }
 
 size_t parse_intra(const uint8_t* d, size_t len, size_t pos, int32_t h, int32_t w, int channels, int levels,
                    IntraJob& job, std::vector<uint64_t>& bits) {
-    // prediction.decode_intra (prediction.py:185-200)
-    pos = intra_tree(d, len, pos, h, w, job.pts[0], bits);
-    pos = intra_values(d, len, pos, levels, job.pts[0].size(), job.vals[0]);
+    // prediction.decode_intra (prediction.py:185-200).  The payload is
+    // [tree Y][values Y] (+ [tree chroma][values Cb][values Cr]); the section
+    // bounds come from the length fields, so the entropy-coded value planes
+    // decode on a helper thread while the trees are walked (large planes:
+    // each tree cut into 16 subtrees walked on several threads).
+    const int ntrees = channels == 3 ? 2 : 1;
+    uint32_t tbits[2] = {0, 0};
+    size_t tpos[2] = {0, 0}, vpos[3] = {0, 0, 0};
+    size_t p = pos;
+    tpos[0] = p;
+    p = intra_tree_span(d, len, p, tbits[0]);
+    vpos[0] = p;
+    p = intra_values_span(d, len, p);
+    if (ntrees == 2) {
+        tpos[1] = p;
+        p = intra_tree_span(d, len, p, tbits[1]);
+        for (int c = 1; c < 3; ++c) {
+            vpos[c] = p;
+            p = intra_values_span(d, len, p);
+        }
+    }
+    const size_t end = p;
+    const size_t npx = (size_t)h * w;
+    static const int kHw = (int)std::max(1u, std::thread::hardware_concurrency());
+    // (the decoder already runs one parse per GOP on its own thread: only the
+    // largest planes, whose I-frame parse is on the critical path, fan out)
+    const int tree_threads = npx >= (1u << 20) ? std::min(4, kHw) : 1;
+    std::vector<int32_t>* idx = job.idx;
+    std::exception_ptr verr[3], terr[2];
+    auto decode_vals = [&]() {
+        for (int c = 0; c < channels; ++c) {
+            try {
+                intra_symbols(d, len, vpos[c], idx[c]);
+            } catch (...) {
+                verr[c] = std::current_exception();
+            }
+        }
+    };
+    std::thread helper;
+    const bool par = npx >= (1u << 18) && kHw > 1;
+    if (par)
+        helper = std::thread([&]() {
+            helper_priority();
+            decode_vals();
+        });
+    for (int t = 0; t < ntrees; ++t) {
+        try {
+            const size_t nl = tree_threads > 1 ? intra_tree_par(d, tpos[t], tbits[t], h, w, tree_threads, bits, job.local)
+                                               : intra_tree_seq(d, tpos[t], tbits[t], h, w, bits);
+            intra_points(bits, nl, job.pts[t], tree_threads);
+        } catch (...) {
+            terr[t] = std::current_exception();
+        }
+    }
+    if (par)
+        helper.join();
+    else
+        decode_vals();
+    // errors in stream order: tree Y, values Y, tree chroma, values Cb, values Cr
+    if (terr[0]) std::rethrow_exception(terr[0]);
+    if (verr[0]) std::rethrow_exception(verr[0]);
+    intra_dequantize(d, vpos[0], levels, idx[0], job.pts[0].size(), job.vals[0]);
     job.nchan = 1;
-    if (channels == 3) {
-        pos = intra_tree(d, len, pos, h, w, job.pts[1], bits);
-        for (int c = 1; c < 3; ++c) pos = intra_values(d, len, pos, 2 * levels - 1, job.pts[1].size(), job.vals[c]);
+    if (ntrees == 2) {
+        if (terr[1]) std::rethrow_exception(terr[1]);
+        for (int c = 1; c < 3; ++c) {
+            if (verr[c]) std::rethrow_exception(verr[c]);
+            intra_dequantize(d, vpos[c], 2 * levels - 1, idx[c], job.pts[1].size(), job.vals[c]);
+        }
         job.nchan = 3;
     }
-    return pos;
+    return end;
 }
 
 // ---------------------------------------------------------------- flow payload

@@ -148,6 +148,8 @@ struct IntraJob {
     std::vector<int32_t> pts[2];    // raster-sorted flat indices of mask points
     std::vector<double> vals[3];    // per channel, raster order of its mask's points
     int nchan = 1;
+    std::vector<int32_t> idx[3];    // scratch: quantised values
+    std::vector<uint64_t> local;    // scratch: per-subtree bitmaps
 };
 // prediction.decode_intra (prediction.py:185-208), parse half; returns next pos.
 size_t parse_intra(const uint8_t* d, size_t len, size_t pos, int32_t h, int32_t w, int channels, int levels,
