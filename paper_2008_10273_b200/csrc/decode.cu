@@ -366,6 +366,7 @@ struct Item {
     Slot* slot = nullptr;
     std::unique_ptr<GopCursor> cur;
     int nf = 0;
+    const double* qtab = nullptr;  // device dequantisation table (ResDev::qtab), shipped with frame 0
     FrameArgs a0;  // I-frame finalize (frame 0)
     uint8_t* gop_dev = nullptr;
     uint8_t* gop_host = nullptr;
@@ -400,15 +401,18 @@ void fail_item(Item& it, int code, const std::string& msg) {
 }
 
 // Pack frames [fi, fi + cnt) of the item into the next staging buffer and ship them.
-const uint8_t* stage_chunk(Slot& L, Item& it, size_t fi, int cnt, FrameOffsets* offs) {
+const uint8_t* stage_chunk(Slot& L, Item& it, size_t fi, int cnt, FrameOffsets* offs,
+                           const std::vector<double>* table = nullptr, size_t* table_off = nullptr) {
     Packer pk;
     for (int k = 0; k < cnt; ++k) pack_frame(pk, it.slot->jobs[fi + k], offs[k]);
+    if (table) *table_off = pk.put(*table);
     uint8_t *host, *dev;
     L.stage_alloc(pk.off + 16, host, dev);
     pk.base = host;
     pk.off = 0;
     pk.measure = false;
     for (int k = 0; k < cnt; ++k) pack_frame(pk, it.slot->jobs[fi + k], offs[k]);
+    if (table) pk.put(*table);
     CUDA_CHECK(cudaMemcpyAsync(dev, host, pk.off, cudaMemcpyHostToDevice, L.stream));
     it.h2d += (int64_t)pk.off;
     return dev;
@@ -441,6 +445,7 @@ FrameArgs frame_args(Slot& L, const StreamHeader& hd, Item& it, size_t fi, const
     RD.dz_step = 127.0 / (double)((hd.residual_levels - 1) / 2);  // quantize.py:43-47
     RD.c_scale = J.res.c_scale;
     RD.a_scale = J.res.a_scale;
+    RD.qtab = it.qtab;
     for (int g = 0; g < RD.ngroups; ++g) {
         const ResidualGroup& G = J.res.g[g];
         ResGroupDev& D = RD.g[g];
@@ -459,6 +464,7 @@ FrameArgs frame_args(Slot& L, const StreamHeader& hd, Item& it, size_t fi, const
             A.flow.nodes[c] = at<int32_t>(dev, o.nodes[c]);
             A.flow.vals[c] = at<double>(dev, o.fvals[c]);
             A.flow.tiles[c] = at<uint16_t>(dev, o.ftiles[c]);
+            A.flow.nleaves[c] = (int)J.flow.vals[c].size();
         }
     return A;
 }
@@ -581,7 +587,12 @@ void intra_phase(CallState& cs, Item& it) {
             it.cur->parse(it.slot->jobs[0], it.ht, bits);  // frame 0 must be intra (codec.py:503)
             if (it.nf == 1) it.cur->finish();
             FrameOffsets o[1];
-            const uint8_t* dev = stage_chunk(L, it, 0, 1, o);
+            std::vector<double> qt(255);  // s * dz_step / 127 for |s| <= 127 (quantize.py:43-47, codec.py:316-321)
+            const double dz = 127.0 / (double)((hd.residual_levels - 1) / 2);
+            for (int k = 0; k < 255; ++k) qt[k] = (double)(k - 127) * dz / 127.0;
+            size_t qoff = 0;
+            const uint8_t* dev = stage_chunk(L, it, 0, 1, o, &qt, &qoff);
+            it.qtab = reinterpret_cast<const double*>(dev + qoff);
             scatter_intra(cs.ctx, L, hd, it.slot->jobs[0], o[0], dev);
             CUDA_CHECK(cudaEventRecord(L.intra_ready, L.stream));
             it.a0 = frame_args(L, hd, it, 0, o[0], dev);

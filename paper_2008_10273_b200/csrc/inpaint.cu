@@ -427,6 +427,7 @@ void InpaintWorkspace::reserve(int h, int w, int dev) {
                                     kBand2Smem));
     const char* env_pack = getenv("HIVC_CG_PACK");
     pack_env_off = env_pack && env_pack[0] == '0';
+    if (env_pack && env_pack[0] == '2') pack_bands = true;  // experiments: throughput mode for single solves too
     const char* env_small = getenv("HIVC_CG_SMALL");
     small_enabled = !(env_small && env_small[0] == '0');
     CUDA_CHECK(cudaFuncSetAttribute(cg_band_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));

@@ -193,12 +193,15 @@ void parse_flow_tree(BitReader& rd, int32_t w, int32_t h, std::vector<int32_t>& 
     }
 }
 
-// Tile -> covering leaf map (0xFFFF: tile straddles leaves).  Leaves tile the
-// plane, so a tile is either inside one leaf or mixed.
-static void flow_tile_map(const std::vector<Rect>& leaves, int32_t w, int32_t h, std::vector<uint16_t>& tiles) {
+// Tile -> covering leaf map.  A tile inside one leaf gets the leaf's value
+// index (< 0x8000); a tile straddling leaves gets 0x8000 + the deepest node
+// whose rectangle contains the whole tile (the device walks from there), or
+// 0xFFFF (walk from the root) when the indices do not fit 15 bits.
+static void flow_tile_map(const std::vector<Rect>& leaves, const std::vector<int32_t>& nodes, int32_t w, int32_t h,
+                          std::vector<uint16_t>& tiles) {
     const int nbx = (w + 7) / 8, nby = (h + 7) / 8;
     tiles.assign((size_t)nbx * nby, 0xFFFF);
-    if (leaves.size() >= 0xFFFF) return;  // all mixed: per-pixel walk
+    if (leaves.size() >= 0x8000) return;  // all: per-pixel walk from the root
     for (size_t li = 0; li < leaves.size(); ++li) {
         const Rect& r = leaves[li];
         // tiles entirely inside the leaf (edge tiles are clipped to the plane)
@@ -213,6 +216,27 @@ static void flow_tile_map(const std::vector<Rect>& leaves, int32_t w, int32_t h,
             }
         }
     }
+    if (nodes.size() / 2 >= 0x7FFF) return;
+    for (int ty = 0; ty < nby; ++ty)
+        for (int tx = 0; tx < nbx; ++tx) {
+            uint16_t& t = tiles[(size_t)ty * nbx + tx];
+            if (t != 0xFFFF) continue;
+            const int x0 = tx * 8, x1 = std::min(w, x0 + 8), y0 = ty * 8, y1 = std::min(h, y0 + 8);
+            int i = 0;
+            for (;;) {  // descend while one child holds the whole tile (parse.h node layout)
+                const int32_t a = nodes[2 * (size_t)i];
+                const int code = a & 3, c = a >> 2;
+                if (code == 0) break;  // (a leaf would have been mapped above)
+                const int lo = code == 1 ? x0 : y0, hi = code == 1 ? x1 : y1;
+                if (hi <= c)
+                    i = i + 1;
+                else if (lo >= c)
+                    i = nodes[2 * (size_t)i + 1];
+                else
+                    break;
+            }
+            t = (uint16_t)(0x8000 + i);
+        }
 }
 
 StreamHeader parse_header(const uint8_t* d, size_t len) {  // bitstream.py:102-121, 80-91
@@ -663,7 +687,7 @@ size_t parse_flow(const uint8_t* d, size_t len, size_t pos, int32_t h, int32_t w
         int32_t nleaves = 0;
         std::vector<Rect> leaves;
         parse_flow_tree(rd, w, h, job.nodes[c], nleaves, &leaves);
-        flow_tile_map(leaves, w, h, job.tiles[c]);
+        flow_tile_map(leaves, job.nodes[c], w, h, job.tiles[c]);
         pos += nbytes;
         std::vector<int32_t> idx;
         pos = decode_symbols(d, len, pos, idx);

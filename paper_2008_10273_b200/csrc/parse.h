@@ -158,8 +158,9 @@ size_t parse_intra(const uint8_t* d, size_t len, size_t pos, int32_t h, int32_t 
 struct FlowJob {
     std::vector<int32_t> nodes[2];   // u, v trees
     std::vector<double> vals[2];
-    // per 8x8 tile: index of the leaf covering the whole tile, 0xFFFF when the
-    // tile straddles a leaf boundary (then the device walks the tree per pixel)
+    // per 8x8 tile: index of the leaf covering the whole tile (< 0x8000), else
+    // 0x8000 + the deepest node containing the tile (the device walks the tree
+    // per pixel from there), or 0xFFFF (walk from the root)
     std::vector<uint16_t> tiles[2];
 };
 // flow.decompress_flow (flow.py:343-372); returns next pos.

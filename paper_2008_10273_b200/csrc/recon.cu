@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "device.cuh"
 #include "inpaint.h"
@@ -20,10 +21,11 @@
 
 namespace hivc {
 
-// Leaf node of the flow tree containing pixel (x, y).
-__device__ __forceinline__ int flow_leaf(const int32_t* __restrict__ nodes, int x, int y) {
-    int i = 0;
-    int a = __ldg(nodes);
+// Leaf node of the flow tree containing pixel (x, y); the tree may sit in
+// shared or global memory (parse.h: parse_flow_tree layout).
+__device__ __forceinline__ int flow_leaf(const int32_t* __restrict__ nodes, int x, int y, int start = 0) {
+    int i = start;
+    int a = __ldg(nodes + 2 * i);
     while (a & 3) {
         int coord = a >> 2;
         bool right = ((a & 3) == 1 ? x : y) >= coord;
@@ -33,150 +35,288 @@ __device__ __forceinline__ int flow_leaf(const int32_t* __restrict__ nodes, int 
     return i;
 }
 
-__device__ __forceinline__ double flow_lookup(const int32_t* __restrict__ nodes, const double* __restrict__ vals, int x,
-                                              int y) {
-    return __ldg(vals + __ldg(nodes + 2 * flow_leaf(nodes, x, y) + 1));
+// Exact int <-> double without the quarter-rate conversion pipe (B200: DADD
+// runs at 64/clk/SM, I2F/F2I/FRND.F64 at ~16): place the integer in the
+// mantissa of 2^52 (or 1.5 * 2^52) and subtract.
+__device__ __forceinline__ double u32_to_d(unsigned n) {  // exact, any n
+    return __hiloint2double(0x43300000, (int)n) - 4503599627370496.0;
 }
+__device__ __forceinline__ double s32_to_d(int n) {  // exact, any n: biased by 2^31
+    return __hiloint2double(0x43380000, n ^ (int)0x80000000) - 6755401588539392.0;
+}
+// rint (round half to even) for |v| < 2^51: adding 1.5 * 2^52 rounds to an
+// integer.  Used only where the result is then clipped to [-255, 255]: a
+// larger |v| (a corrupt residual) saturates the clip either way.
+__device__ __forceinline__ double rint_clip(double v) { return (v + 6755399441055744.0) - 6755399441055744.0; }
+// (int)v for an integral v with |v| < 2^31: its value sits in the low mantissa word of v + 1.5 * 2^52
+__device__ __forceinline__ int d_to_int_exact(double v) { return __double2loint(v + 6755399441055744.0); }
+
+__device__ __forceinline__ double to_d(uint8_t v) { return u32_to_d((unsigned)v); }
+__device__ __forceinline__ double to_d(int16_t v) { return s32_to_d((int)v); }
 
 template <typename RT>
-__device__ __forceinline__ double ld_plane(const void* p, size_t k) {
-    return (double)__ldg(reinterpret_cast<const RT*>(p) + k);
+__device__ __forceinline__ double ld_plane(const void* p, int k) {
+    const RT v = __ldg(reinterpret_cast<const RT*>(p) + k);
+    if (sizeof(RT) == 1) return u32_to_d((unsigned)v);
+    return s32_to_d((int)v);
+}
+
+// sym * dz_step / 127 * scale (codec.py:316-321), the first two factors from the table
+__device__ __forceinline__ double dequant(const ResDev& R, int sym, double scale) {
+    if (R.qtab && sym >= -127 && sym <= 127) return __ldg(R.qtab + sym + 127) * scale;
+    return (double)sym * R.dz_step / 127.0 * scale;
 }
 
 // Residual block of coded block b, plane ci of group G, built by lanes 0..7.
 __device__ __forceinline__ void residual_block(const ResDev& R, const ResGroupDev& G, int b, int ci, double* t,
-                                               int lane) {
+                                               int lane, unsigned mask8) {
     const uint64_t mask = __ldg(G.block_mask + b);
     const int off = __ldg(G.block_off + b);
     // scatter dequantised coefficients onto the mask (codec.py:316-321)
+    const uint64_t below = mask & ((1ull << (lane * 8)) - 1ull);
+    int rank = __popcll(below);
+#pragma unroll
     for (int x = 0; x < 8; ++x) {
-        int bit = lane * 8 + x;
         double v = 0.0;
-        if ((mask >> bit) & 1ull) {
-            int rank = __popcll(mask & ((1ull << bit) - 1ull));
-            int sym = __ldg(G.c_sym + (size_t)ci * G.npoints + off + rank);
-            v = (double)sym * R.dz_step / 127.0 * R.c_scale;
+        if ((mask >> (lane * 8 + x)) & 1ull) {
+            const int sym = __ldg(G.c_sym + ci * G.npoints + off + rank);
+            ++rank;
+            v = dequant(R, sym, R.c_scale);
         }
         t[lane * 8 + x] = v;
     }
-    double a = (double)__ldg(G.a_sym + (size_t)ci * G.nblocks + b) * R.dz_step / 127.0 * R.a_scale;
-    __syncwarp(0xffu);
-    block_reconstruct_8lanes(t, lane, kGreensEig, a, 0xffu);
+    double a = dequant(R, __ldg(G.a_sym + ci * G.nblocks + b), R.a_scale);
+    __syncwarp(mask8);
+    block_reconstruct_8lanes(t, lane, kGreensEig, a, mask8);
 }
 
+// min(max(v, lo), hi) for finite v (np.clip; the flow values are checked finite)
+__device__ __forceinline__ double clampd(double v, double lo, double hi) {
+    v = v < lo ? lo : v;
+    return v > hi ? hi : v;
+}
+
+// Layout: a warp covers 4 horizontally adjacent 8x8 tiles (32 x 8 pixels);
+// lane l owns column l of that strip for all 8 rows, so every load/store row
+// is 32 consecutive pixels, each lane has 8 independent prediction chains in
+// flight (the warp is latency-bound: tile map -> flow value -> 4 gathers),
+// and the coded residual blocks of the 4 tiles are rebuilt side by side by
+// the 4 groups of 8 lanes (lanes 8g..8g+7 for tile g).  2 warps per CTA.
+constexpr int kFrameWarps = 2;
+constexpr int kWarpTiles = 4;
+#ifndef HIVC_FRAME_MIN_BLOCKS
+#define HIVC_FRAME_MIN_BLOCKS 12  // 2-warp CTAs: <= 80 registers
+#endif
+constexpr int kFrameMinBlocks = HIVC_FRAME_MIN_BLOCKS;
+
 template <bool kInter, int C, typename RT>
-__global__ void __launch_bounds__(256) frame_kernel(FrameArgs A) {
-    __shared__ double s_res[C][8][64];
+__global__ void __launch_bounds__(32 * kFrameWarps, kFrameMinBlocks) frame_kernel(FrameArgs A) {
+    __shared__ double s_res[kFrameWarps][C][kWarpTiles][64];
     const int h = A.h, w = A.w;
     const int nbx = (w + 7) >> 3;
     const int ty = blockIdx.y;
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int tx = blockIdx.x * 8 + wid;
-
-    // One warp per 8x8 tile: lane l owns column l % 8 of rows l / 8 and l / 8 + 4.
-    // The prediction loads are issued first; the tile's residual block is
-    // rebuilt (lanes 0..7) while they are in flight; no CTA-wide barrier.
-    const int lx = lane & 7, ly = lane >> 3;
-    const int x = tx * 8 + lx;
+    const int grp = lane >> 3, gl = lane & 7;          // tile within the warp, column within the tile
+    const int tx = (blockIdx.x * kFrameWarps + wid) * kWarpTiles + grp;
     const bool tile_ok = tx < nbx;
-    double pred[2][C];
-    bool live[2];
+    const int x = tx * 8 + gl;
+    const bool col_ok = tile_ok && x < w;
+    const int y_base = ty * 8;
+    const int rows = min(8, h - y_base);
+    double pred[8][C];
     // ---- prediction
     if (kInter) {
         // the host rasterised each flow tree to tiles: most tiles lie inside one
         // leaf (one (u, v) for the tile); tiles on a leaf boundary walk the tree
-        const size_t tt = (size_t)ty * nbx + (tile_ok ? tx : 0);
-        const int lu = __ldg(A.flow.tiles[0] + tt), lv = __ldg(A.flow.tiles[1] + tt);
+        const int tt = ty * nbx + (tile_ok ? tx : 0);
+        const int lu = A.flow.tiles[0] ? __ldg(A.flow.tiles[0] + tt) : 0xFFFF;
+        const int lv = A.flow.tiles[1] ? __ldg(A.flow.tiles[1] + tt) : 0xFFFF;
+        const double* __restrict__ vals0 = A.flow.vals[0];
+        const double* __restrict__ vals1 = A.flow.vals[1];
+        const double wm1 = (double)(w - 1), hm1 = (double)(h - 1);
+        const double xd = u32_to_d((unsigned)x), yd0 = u32_to_d((unsigned)y_base);
+        // tile map: < 0x8000 leaf (value) index; else walk per pixel from node (t - 0x8000), 0xFFFF: root
+        const bool mu = lu >= 0x8000 && !A.exp_uniform, mv = lv >= 0x8000 && !A.exp_uniform;
+        const int su = lu == 0xFFFF ? 0 : lu - 0x8000, sv = lv == 0xFFFF ? 0 : lv - 0x8000;
+        const double u_tile = mu ? 0.0 : __ldg(vals0 + (lu & 0x7FFF) % max(1, A.flow.nleaves[0]));
+        const double v_tile = mv ? 0.0 : __ldg(vals1 + (lv & 0x7FFF) % max(1, A.flow.nleaves[1]));
 #pragma unroll
-        for (int rr = 0; rr < 2; ++rr) {
-            const int y = ty * 8 + ly + 4 * rr;
-            live[rr] = tile_ok && x < w && y < h;
-            if (!live[rr]) continue;
-            // flow.py:94-127 — coordinates clamped before flooring, taps summed w00..w11
-            double u = lu != 0xFFFF ? __ldg(A.flow.vals[0] + lu) : flow_lookup(A.flow.nodes[0], A.flow.vals[0], x, y);
-            double v = lv != 0xFFFF ? __ldg(A.flow.vals[1] + lv) : flow_lookup(A.flow.nodes[1], A.flow.vals[1], x, y);
-            double sx = fmin(fmax((double)x + u, 0.0), (double)(w - 1));
-            double sy = fmin(fmax((double)y + v, 0.0), (double)(h - 1));
-            int x0 = (int)floor(sx), y0 = (int)floor(sy);
-            int x1 = min(x0 + 1, w - 1), y1 = min(y0 + 1, h - 1);
-            double fx = sx - (double)x0, fy = sy - (double)y0;
-            double w00 = (1 - fy) * (1 - fx), w01 = (1 - fy) * fx, w10 = fy * (1 - fx), w11 = fy * fx;
-            size_t i00 = (size_t)y0 * w + x0, i01 = (size_t)y0 * w + x1, i10 = (size_t)y1 * w + x0,
-                   i11 = (size_t)y1 * w + x1;
+        for (int r = 0; r < 8; ++r)
+#pragma unroll
+            for (int c = 0; c < C; ++c) pred[r][c] = 0.0;
+        if (col_ok && !mu && !mv) {
+            // uniform flow over the tile: one source column pair for all 8 rows;
+            // the 8 rows' 32 taps are issued before any is used
+            const double sx = clampd(xd + u_tile, 0.0, wm1);
+            const int x0 = __double2int_rd(sx);  // floor; sx >= 0
+            const int x1 = min(x0 + 1, w - 1);
+            const double fx = sx - u32_to_d((unsigned)x0);
+            int ra[8], rb[8];
+            double fy[8];
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                const double sy = clampd((yd0 + (double)r) + v_tile, 0.0, hm1);
+                const int y0 = __double2int_rd(sy);
+                ra[r] = y0 * w;
+                rb[r] = min(y0 + 1, h - 1) * w;
+                fy[r] = sy - u32_to_d((unsigned)y0);
+            }
 #pragma unroll
             for (int c = 0; c < C; ++c) {
-                const void* p = A.prev[c];
-                pred[rr][c] = ((w00 * ld_plane<RT>(p, i00) + w01 * ld_plane<RT>(p, i01)) + w10 * ld_plane<RT>(p, i10)) +
-                              w11 * ld_plane<RT>(p, i11);
+                const RT* __restrict__ p = reinterpret_cast<const RT*>(A.prev[c]);
+                RT t00[8], t01[8], t10[8], t11[8];
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    if (r < rows) {
+                        t00[r] = __ldg(p + ra[r] + x0);
+                        t01[r] = __ldg(p + ra[r] + x1);
+                        t10[r] = __ldg(p + rb[r] + x0);
+                        t11[r] = __ldg(p + rb[r] + x1);
+                    }
+                }
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    if (r >= rows) break;
+                    const double w00 = (1 - fy[r]) * (1 - fx), w01 = (1 - fy[r]) * fx, w10 = fy[r] * (1 - fx),
+                                 w11 = fy[r] * fx;
+                    pred[r][c] = ((w00 * to_d(t00[r]) + w01 * to_d(t01[r])) + w10 * to_d(t10[r])) + w11 * to_d(t11[r]);
+                }
+            }
+        } else if (col_ok) {
+            // a tile on a leaf boundary: descend both trees for the 8 rows in
+            // lockstep (one 8-byte node load per row and tree per level), then
+            // the 8 rows' flow values and taps
+            int iu[8], iv[8];  // node -> (at the end) value index per row
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                iu[r] = mu ? su : -1;
+                iv[r] = mv ? sv : -1;
+            }
+            const int2* __restrict__ n0 = reinterpret_cast<const int2*>(A.flow.nodes[0]);
+            const int2* __restrict__ n1 = reinterpret_cast<const int2*>(A.flow.nodes[1]);
+            bool more = true;
+            while (more) {
+                more = false;
+                int2 e0[8], e1[8];
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    e0[r] = iu[r] >= 0 ? __ldg(n0 + iu[r]) : make_int2(0, 0);
+                    e1[r] = iv[r] >= 0 ? __ldg(n1 + iv[r]) : make_int2(0, 0);
+                }
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    const int y = y_base + r;
+                    if (iu[r] >= 0 && (e0[r].x & 3)) {  // split: x-split code 1, y-split code 2
+                        const bool right = ((e0[r].x & 3) == 1 ? x : y) >= (e0[r].x >> 2);
+                        iu[r] = right ? e0[r].y : iu[r] + 1;
+                        more = true;
+                    }
+                    if (iv[r] >= 0 && (e1[r].x & 3)) {
+                        const bool right = ((e1[r].x & 3) == 1 ? x : y) >= (e1[r].x >> 2);
+                        iv[r] = right ? e1[r].y : iv[r] + 1;
+                        more = true;
+                    }
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {  // leaf node -> its value index
+                iu[r] = iu[r] >= 0 ? __ldg(n0 + iu[r]).y : -1;
+                iv[r] = iv[r] >= 0 ? __ldg(n1 + iv[r]).y : -1;
+            }
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                if (r >= rows) break;
+                // flow.py:94-127 — coordinates clamped before flooring, taps summed w00..w11
+                const double u = iu[r] >= 0 ? __ldg(vals0 + iu[r]) : u_tile;
+                const double v = iv[r] >= 0 ? __ldg(vals1 + iv[r]) : v_tile;
+                const double sx = clampd(xd + u, 0.0, wm1);
+                const double sy = clampd((yd0 + (double)r) + v, 0.0, hm1);
+                const int x0 = __double2int_rd(sx), y0 = __double2int_rd(sy);  // floor; sx, sy >= 0
+                const int x1 = min(x0 + 1, w - 1), y1 = min(y0 + 1, h - 1);
+                const double fx = sx - u32_to_d((unsigned)x0), fy = sy - u32_to_d((unsigned)y0);
+                const double w00 = (1 - fy) * (1 - fx), w01 = (1 - fy) * fx, w10 = fy * (1 - fx), w11 = fy * fx;
+                const int i00 = y0 * w + x0, i01 = y0 * w + x1, i10 = y1 * w + x0, i11 = y1 * w + x1;
+#pragma unroll
+                for (int c = 0; c < C; ++c) {
+                    const void* p = A.prev[c];
+                    pred[r][c] = ((w00 * ld_plane<RT>(p, i00) + w01 * ld_plane<RT>(p, i01)) + w10 * ld_plane<RT>(p, i10)) +
+                                 w11 * ld_plane<RT>(p, i11);
+                }
             }
         }
     } else {
 #pragma unroll
-        for (int rr = 0; rr < 2; ++rr) {
-            const int y = ty * 8 + ly + 4 * rr;
-            live[rr] = tile_ok && x < w && y < h;
+        for (int r = 0; r < 8; ++r)
 #pragma unroll
-            for (int c = 0; c < C; ++c) pred[rr][c] = live[rr] ? __ldg(A.u[c] + (size_t)y * w + x) : 0.0;
-        }
+            for (int c = 0; c < C; ++c)
+                pred[r][c] = (col_ok && r < rows) ? __ldg(A.u[c] + (size_t)(y_base + r) * w + x) : 0.0;
     }
-    // ---- residual block(s) of this tile
+    // ---- residual block(s): lanes 8g..8g+7 rebuild tile g's coded blocks
     bool coded[2] = {false, false};
     if (A.res.ngroups > 0 && tile_ok) {
-        const size_t t = (size_t)ty * nbx + tx;
+        const int t = ty * nbx + tx;
+        const unsigned mask8 = 0xFFu << (8 * grp);
         int chan = 0;
         for (int gi = 0; gi < A.res.ngroups; ++gi) {
             const ResGroupDev& G = A.res.g[gi];
-            uint64_t word = __ldg(G.tile_words + (t >> 6));
+            const uint64_t word = __ldg(G.tile_words + (t >> 6));
             coded[gi] = (word >> (t & 63)) & 1ull;
             if (coded[gi]) {
-                int b = __ldg(G.word_prefix + (t >> 6)) + __popcll(word & ((1ull << (t & 63)) - 1ull));
-                if (lane < 8)
-                    for (int ci = 0; ci < G.nplanes; ++ci) residual_block(A.res, G, b, ci, &s_res[chan + ci][wid][0], lane);
+                const int b = __ldg(G.word_prefix + (t >> 6)) + __popcll(word & ((1ull << (t & 63)) - 1ull));
+                for (int ci = 0; ci < G.nplanes; ++ci)
+                    residual_block(A.res, G, b, ci, &s_res[wid][chan + ci][grp][0], gl, mask8);
             }
             chan += G.nplanes;
         }
-        __syncwarp();
     }
+    __syncwarp();
+    if (!col_ok) return;
 #pragma unroll
-    for (int rr = 0; rr < 2; ++rr) {
-        if (!live[rr]) continue;
-        const int row = ly + 4 * rr;
-        const int y = ty * 8 + row;
-        const size_t k = (size_t)y * w + x;
+    for (int r = 0; r < 8; ++r) {
+        if (r >= rows) break;
+        const size_t k = (size_t)(y_base + r) * w + x;
         int rec[C];
 #pragma unroll
         for (int c = 0; c < C; ++c) {
             const int gi = c == 0 ? 0 : 1;
-            double res = coded[gi] ? s_res[c][wid][row * 8 + lx] : 0.0;
-            double v = rint(rint(pred[rr][c]) + res);
+            const double res = coded[gi] ? s_res[wid][c][grp][r * 8 + gl] : 0.0;
+            double v = rint_clip(rint_clip(pred[r][c]) + res);
             const double lo = (C == 3 && c > 0) ? -255.0 : 0.0;
-            v = fmin(fmax(v, lo), 255.0);
-            rec[c] = (int)v;
+            v = clampd(v, lo, 255.0);
+            rec[c] = d_to_int_exact(v);
             reinterpret_cast<RT*>(A.recon[c])[k] = (RT)rec[c];
         }
         if (C == 3) {
             // rct_inverse (frame.py:84-93) + clip to [0, 255] (codec.py:479-480)
-            int g = rec[0] - ((rec[1] + rec[2]) >> 2);
-            int r = rec[2] + g, b = rec[1] + g;
-            A.rgb[0][k] = (uint8_t)min(max(r, 0), 255);
+            const int g = rec[0] - ((rec[1] + rec[2]) >> 2);
+            const int rr = rec[2] + g, bb = rec[1] + g;
+            A.rgb[0][k] = (uint8_t)min(max(rr, 0), 255);
             A.rgb[1][k] = (uint8_t)min(max(g, 0), 255);
-            A.rgb[2][k] = (uint8_t)min(max(b, 0), 255);
+            A.rgb[2][k] = (uint8_t)min(max(bb, 0), 255);
         }
     }
 }
 
-void launch_frame(const FrameArgs& a, bool inter, cudaStream_t s) {
-    dim3 grid((((a.w + 7) / 8) + 7) / 8, (a.h + 7) / 8);
+void launch_frame(const FrameArgs& a_in, bool inter, cudaStream_t s) {
+    FrameArgs a = a_in;
+    static const int exp_mode = getenv("HIVC_P_EXPERIMENT") ? atoi(getenv("HIVC_P_EXPERIMENT")) : 0;
+    if (exp_mode & 1) a.res.ngroups = 0;  // timing experiments only: drop the residual
+    if (exp_mode & 2)                     // timing experiments only: force the tree walk everywhere
+        for (int c = 0; c < 2; ++c) a.flow.tiles[c] = nullptr;
+    a.exp_uniform = (exp_mode & 4) != 0;  // timing experiments only: treat every tile as one leaf
+    const int tiles_per_cta = kFrameWarps * kWarpTiles;
+    dim3 grid((((a.w + 7) / 8) + tiles_per_cta - 1) / tiles_per_cta, (a.h + 7) / 8);
+    const int nt = 32 * kFrameWarps;
     if (a.channels == 1) {
         if (inter)
-            frame_kernel<true, 1, uint8_t><<<grid, 256, 0, s>>>(a);
+            frame_kernel<true, 1, uint8_t><<<grid, nt, 0, s>>>(a);
         else
-            frame_kernel<false, 1, uint8_t><<<grid, 256, 0, s>>>(a);
+            frame_kernel<false, 1, uint8_t><<<grid, nt, 0, s>>>(a);
     } else {
         if (inter)
-            frame_kernel<true, 3, int16_t><<<grid, 256, 0, s>>>(a);
+            frame_kernel<true, 3, int16_t><<<grid, nt, 0, s>>>(a);
         else
-            frame_kernel<false, 3, int16_t><<<grid, 256, 0, s>>>(a);
+            frame_kernel<false, 3, int16_t><<<grid, nt, 0, s>>>(a);
     }
     CUDA_CHECK(cudaGetLastError());
 }

@@ -23,6 +23,9 @@ struct ResGroupDev {
 struct ResDev {
     int ngroups = 0;                            // 0: all-zero residual
     double dz_step = 0, c_scale = 0, a_scale = 0;  // dead-zone step 127/((L-1)/2), c_fp/65536, a_fp/65536
+    // optional: qtab[s + 127] = s * dz_step / 127.0 for |s| <= 127 (then one
+    // multiply by the scale dequantises a symbol, same rounding as the reference)
+    const double* qtab = nullptr;
     ResGroupDev g[2];
 };
 
@@ -30,6 +33,7 @@ struct FlowDev {
     const int32_t* nodes[2] = {nullptr, nullptr};  // u, v trees (parse.h: parse_flow_tree)
     const double* vals[2] = {nullptr, nullptr};
     const uint16_t* tiles[2] = {nullptr, nullptr};  // per-tile covering leaf, 0xFFFF = mixed
+    int nleaves[2] = {0, 0};                        // leaves (values) per tree; nodes = 2 * leaves - 1
 };
 
 struct FrameArgs {
@@ -40,6 +44,7 @@ struct FrameArgs {
     ResDev res;
     void* recon[3] = {nullptr, nullptr, nullptr};      // out: reconstruction (uint8 gray / int16 colour)
     uint8_t* rgb[3] = {nullptr, nullptr, nullptr};     // out: RGB planes (colour only)
+    int exp_uniform = 0;                               // timing experiments only (HIVC_P_EXPERIMENT)
 };
 
 // kInter: warp prediction from prev + flow trees; else prediction = u.
