@@ -83,28 +83,38 @@ __global__ void __launch_bounds__(kBandThreads, 1) cg_band2_kernel(const __grid_
             const size_t prev_par = (size_t)((k - 1) & 1) * pstride, cur_par = (size_t)(k & 1) * pstride;
             HIVC_TRACE(0);
             // ---- phase 1a: halo rows (neighbours' edge rows of r and p) and own p = r + beta p
-            for (int c = tid; c < w; c += kBandThreads) {
-                if (!top) {
-                    double rv, pv;
-                    if (k == 1) {
-                        rv = pv = __ldcg(P.r + (size_t)(y0 - 1) * w + c);
-                    } else {
-                        const size_t e = ((size_t)(band - 1) * 2 + 1) * w + c;
-                        rv = __ldcg(P.ex_r + e);
-                        pv = __ldcg(P.ex_p + prev_par + e);
+            {  // all KC columns' halo values are loaded before any is used (one L2 round trip)
+                double tr[KC], tp[KC], br[KC], bp[KC];
+#pragma unroll
+                for (int k2 = 0; k2 < KC; ++k2) {
+                    const int c = tid + kBandThreads * k2;
+                    tr[k2] = tp[k2] = br[k2] = bp[k2] = 0.0;
+                    if (c >= w) continue;
+                    if (!top) {
+                        if (k == 1) {
+                            tr[k2] = tp[k2] = __ldcg(P.r + (size_t)(y0 - 1) * w + c);
+                        } else {
+                            const size_t e = ((size_t)(band - 1) * 2 + 1) * w + c;
+                            tr[k2] = __ldcg(P.ex_r + e);
+                            tp[k2] = __ldcg(P.ex_p + prev_par + e);
+                        }
                     }
-                    sp[c + 1] = rv + beta * pv;
+                    if (!bottom) {
+                        if (k == 1) {
+                            br[k2] = bp[k2] = __ldcg(P.r + (size_t)(y0 + rows) * w + c);
+                        } else {
+                            const size_t e = ((size_t)(band + 1) * 2 + 0) * w + c;
+                            br[k2] = __ldcg(P.ex_r + e);
+                            bp[k2] = __ldcg(P.ex_p + prev_par + e);
+                        }
+                    }
                 }
-                if (!bottom) {
-                    double rv, pv;
-                    if (k == 1) {
-                        rv = pv = __ldcg(P.r + (size_t)(y0 + rows) * w + c);
-                    } else {
-                        const size_t e = ((size_t)(band + 1) * 2 + 0) * w + c;
-                        rv = __ldcg(P.ex_r + e);
-                        pv = __ldcg(P.ex_p + prev_par + e);
-                    }
-                    sp[(rows + 1) * W2 + c + 1] = rv + beta * pv;
+#pragma unroll
+                for (int k2 = 0; k2 < KC; ++k2) {
+                    const int c = tid + kBandThreads * k2;
+                    if (c >= w) continue;
+                    if (!top) sp[c + 1] = tr[k2] + beta * tp[k2];
+                    if (!bottom) sp[(rows + 1) * W2 + c + 1] = br[k2] + beta * bp[k2];
                 }
             }
 #pragma unroll
@@ -191,21 +201,36 @@ __global__ void __launch_bounds__(kBandThreads, 1) cg_band2_kernel(const __grid_
             }
             HIVC_TRACE(4);
             grid_reduce_arrive<1>(e1, sh, P, red, band);
-            // x += alpha p while the other CTAs arrive (x is not read until the level ends)
+            // x += alpha p while the other CTAs arrive (x is not read until the level ends):
+            // resident rows in smem; streamed rows 8 values at a time, all loads issued first
 #pragma unroll
             for (int k2 = 0; k2 < KC; ++k2) {
                 const int c = tid + kBandThreads * k2;
                 if (c >= w) continue;
 #pragma unroll
                 for (int row = 0; row < ROWS; ++row) {
-                    if (row >= rows) break;
-                    const double pi = sp[(row + 1) * W2 + c + 1];
-                    if (row < xr) {
-                        double& xs = sx[row * w + c];
-                        xs = xs + alpha * pi;
-                    } else {
-                        const size_t gi = (size_t)(y0 + row) * w + c;
-                        P.x[gi] = P.x[gi] + alpha * pi;
+                    if (row >= xr || row >= rows) break;
+                    double& xs = sx[row * w + c];
+                    xs = xs + alpha * sp[(row + 1) * W2 + c + 1];
+                }
+            }
+            if (xr < rows) {
+#pragma unroll
+                for (int g = 0; g < ROWS * KC; g += 8) {
+                    if ((g + 7) / KC < xr) continue;  // group entirely in resident rows
+                    double xv[8];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const int idx = g + j, row = idx / KC, c = tid + kBandThreads * (idx % KC);
+                        xv[j] = 0.0;
+                        if (idx < ROWS * KC && row >= xr && row < rows && c < w)
+                            xv[j] = P.x[(size_t)(y0 + row) * w + c];
+                    }
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const int idx = g + j, row = idx / KC, c = tid + kBandThreads * (idx % KC);
+                        if (idx < ROWS * KC && row >= xr && row < rows && c < w)
+                            P.x[(size_t)(y0 + row) * w + c] = xv[j] + alpha * sp[(row + 1) * W2 + c + 1];
                     }
                 }
             }
