@@ -11,6 +11,11 @@
 // for phase 2 (small bands) instead of being recomputed.
 #pragma once
 
+#ifndef HIVC_XG
+#define HIVC_XG 8
+#endif
+constexpr int kXG = HIVC_XG;  // streamed-x values per batch of loads
+
 template <int ROWS, int KC, bool STORE_AP>
 __global__ void __launch_bounds__(kBandThreads, 1) cg_band2_kernel(const __grid_constant__ BandBatch B) {
     static_assert(ROWS * KC <= 32, "mask bits");
@@ -202,7 +207,7 @@ __global__ void __launch_bounds__(kBandThreads, 1) cg_band2_kernel(const __grid_
             HIVC_TRACE(4);
             grid_reduce_arrive<1>(e1, sh, P, red, band);
             // x += alpha p while the other CTAs arrive (x is not read until the level ends):
-            // resident rows in smem; streamed rows 8 values at a time, all loads issued first
+            // resident rows in smem; streamed rows kXG values at a time, all loads issued first
 #pragma unroll
             for (int k2 = 0; k2 < KC; ++k2) {
                 const int c = tid + kBandThreads * k2;
@@ -216,24 +221,25 @@ __global__ void __launch_bounds__(kBandThreads, 1) cg_band2_kernel(const __grid_
             }
             if (xr < rows) {
 #pragma unroll
-                for (int g = 0; g < ROWS * KC; g += 8) {
-                    if ((g + 7) / KC < xr) continue;  // group entirely in resident rows
-                    double xv[8];
+                for (int g = 0; g < ROWS * KC; g += kXG) {
+                    if ((g + kXG - 1) / KC < xr) continue;  // group entirely in resident rows
+                    double xv[kXG];
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) {
+                    for (int j = 0; j < kXG; ++j) {
                         const int idx = g + j, row = idx / KC, c = tid + kBandThreads * (idx % KC);
                         xv[j] = 0.0;
                         if (idx < ROWS * KC && row >= xr && row < rows && c < w)
                             xv[j] = P.x[(size_t)(y0 + row) * w + c];
                     }
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) {
+                    for (int j = 0; j < kXG; ++j) {
                         const int idx = g + j, row = idx / KC, c = tid + kBandThreads * (idx % KC);
                         if (idx < ROWS * KC && row >= xr && row < rows && c < w)
                             P.x[(size_t)(y0 + row) * w + c] = xv[j] + alpha * sp[(row + 1) * W2 + c + 1];
                     }
                 }
             }
+            HIVC_TRACE(6);
             grid_reduce_finish<1>(e1, sh, P, red, nb);
             HIVC_TRACE(5);
             const double rs1 = e1[0];
