@@ -377,15 +377,20 @@ struct Item {
     int64_t h2d = 0, d2h = 0, inter_frames = 0, intra_frames = 0;
     EvPairs ev_inter, ev_intra, ev_ifin;
     cudaEvent_t done = nullptr;
+    bool issued = false;  // its batch is queued (under Shared::mu)
     double h_i0 = 0, h_i1 = 0, h_issue = 0, h_p0 = 0, h_p1 = 0;  // host timeline (HIVC_TIMELINE)
 };
 
-// Same-shape items whose I-frame solves are issued as batches.
+// Same-shape items whose I-frame solves are issued as batches: as soon as
+// kMinBatch of them are parsed (a packed band level runs 4 side by side), and
+// the rest when the last one is.
+constexpr int kMinBatch = 4;
 struct Group {
     int h = 0, w = 0, c = 0;
     std::vector<int> items;
-    std::atomic<int> pending{0};
-    bool issued = false;  // under Shared::mu
+    std::mutex mu;
+    int pending = 0;         // items whose intra phase has not finished (under mu)
+    std::vector<int> ready;  // parsed, not yet issued (under mu)
 };
 
 struct Shared {
@@ -512,7 +517,7 @@ void copy_out(CallState& cs, Slot& L, Item& it, size_t fi, size_t frame_bytes) {
 void issue_solves(CallState& cs, const std::vector<int>& idx, const StreamHeader& hd) {
     Context& ctx = cs.ctx;
     const int h = hd.height, w = hd.width, C = hd.channels;
-    const cudaStream_t pre = idx.empty() ? nullptr : ctx.pre[cs.items[idx[0]].group & 1];
+    const cudaStream_t pre = ctx.pre[ctx.pre_next++ % Context::kPre];
     for (size_t b0 = 0; b0 < idx.size(); b0 += kMaxBatch) {
         const int K = (int)std::min<size_t>(kMaxBatch, idx.size() - b0);
         for (int j = 0; j < K; ++j) CUDA_CHECK(cudaStreamWaitEvent(pre, cs.items[idx[b0 + j]].slot->intra_ready, 0));
@@ -608,26 +613,33 @@ void intra_phase(CallState& cs, Item& it) {
     }
     it.h_i1 = now_s() - cs.t0;
     Group& g = cs.groups[it.group];
-    if (g.pending.fetch_sub(1) == 1) {
-        for (int i : g.items) cs.items[i].h_issue = now_s() - cs.t0;
-        std::vector<int> ready;
-        for (int i : g.items)
-            if (cs.items[i].code == HIVC_OK && cs.items[i].solve0) ready.push_back(i);
+    std::vector<int> batch, done_items;
+    {
+        std::lock_guard<std::mutex> lk(g.mu);
+        const int self = (int)(&it - cs.items.data());
+        done_items.push_back(self);
+        if (it.code == HIVC_OK && it.solve0) g.ready.push_back(self);
+        --g.pending;
+        if ((int)g.ready.size() >= kMinBatch || g.pending == 0) batch.swap(g.ready);
+    }
+    if (!batch.empty()) {
+        for (int i : batch) cs.items[i].h_issue = now_s() - cs.t0;
         try {
             std::lock_guard<std::mutex> lk(cs.ctx.solver_mu);
             CUDA_CHECK(cudaSetDevice(cs.ctx.device));
-            issue_solves(cs, ready, hd);
+            issue_solves(cs, batch, hd);
         } catch (const Error& e) {
-            for (int i : ready) fail_item(cs.items[i], e.code, e.what());
+            for (int i : batch) fail_item(cs.items[i], e.code, e.what());
         } catch (const std::exception& e) {
-            for (int i : ready) fail_item(cs.items[i], HIVC_E_ARGUMENT, e.what());
+            for (int i : batch) fail_item(cs.items[i], HIVC_E_ARGUMENT, e.what());
         }
-        {
-            std::lock_guard<std::mutex> lk(cs.sh.mu);
-            g.issued = true;
-        }
-        cs.sh.cv.notify_all();
     }
+    {  // the failed / empty item itself and the batch are now final for their inter phases
+        std::lock_guard<std::mutex> lk(cs.sh.mu);
+        for (int i : batch) cs.items[i].issued = true;
+        if (!(it.code == HIVC_OK && it.solve0) || it.nf == 0) it.issued = true;
+    }
+    cs.sh.cv.notify_all();
 }
 
 // Phase 2 of an item: after its group's solves are queued, parse and run the
@@ -641,7 +653,7 @@ void inter_phase(CallState& cs, Item& it) {
     const size_t frame_bytes = (size_t)hd.height * hd.width * hd.channels;
     {
         std::unique_lock<std::mutex> lk(cs.sh.mu);
-        cs.sh.cv.wait(lk, [&] { return cs.groups[it.group].issued; });
+        cs.sh.cv.wait(lk, [&] { return it.issued; });
     }
     it.h_p0 = now_s() - cs.t0;
     try {

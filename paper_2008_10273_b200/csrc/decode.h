@@ -75,7 +75,9 @@ struct Context {
     BroxWorkspace brox;             // flow_brox scratch
     std::vector<std::unique_ptr<Slot>> slots;
     cudaStream_t solver = nullptr;  // every batched (grid-barrier) solve of a decode call, in order
-    cudaStream_t pre[2] = {nullptr, nullptr};  // pyramid + cluster levels of a batch (side streams)
+    static constexpr int kPre = 4;
+    cudaStream_t pre[kPre] = {};  // pyramid + cluster levels of a batch (side streams, round robin)
+    int pre_next = 0;             // (under solver_mu)
     std::mutex solver_mu;           // one batch's launches stay contiguous on the solver stream
     CgProbe probe;                  // solver-stream launches (stage timing on)
     std::atomic<int64_t> launches{0};

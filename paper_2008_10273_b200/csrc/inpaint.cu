@@ -102,7 +102,9 @@ struct CgParams {
     int band_rows;
     double* ex_r;  // [nbands][2][w]: first/last owned row of r
     double* ex_p;  // [2 parity][nbands][2][w]: first/last owned row of p
-    int x_rows = 0;  // band2: leading band rows whose x lives in shared memory (the rest streams)
+    int x_rows = 0;  // band2 / tile: leading rows whose x lives in shared memory (the rest streams)
+    // tile kernel: tiles of band_rows x tile_cols, ntc tiles per row of tiles
+    int tile_cols = 0, ntc = 1;
     unsigned long long* trace = nullptr;  // diagnostics: per-iteration phase timestamps of CTA 0
     unsigned long long* stamp = nullptr;  // probe: globaltimer at kernel entry / exit (CTA 0)
 };
@@ -132,20 +134,28 @@ __device__ __forceinline__ double lap_at(int y, int xx, int h, int w, double c, 
     return (((c * -4.0 + north) + south) + west) + east;
 }
 
+// Consecutive grid reductions alternate between two banks of partials (by
+// barrier epoch): a CTA released from barrier e may already publish its
+// partial for barrier e + 1 while a slower CTA still sums the partials of
+// barrier e; it cannot reach barrier e + 2 (same bank) before every CTA has
+// arrived at e + 1.
+constexpr int kPartialBank = 2048;  // doubles per bank (<= 512 CTAs x 4 values)
+
 template <bool kGrid, int NV>
 __device__ __forceinline__ void reduce(double (&v)[NV], double* sh, const CgParams& P, unsigned int& epoch) {
     block_sum<NV>(v, sh);
     if (!kGrid) return;
+    const double* part = P.partials + ((epoch + 1) & 1) * kPartialBank;  // see grid_reduce
     if (threadIdx.x == 0)
 #pragma unroll
-        for (int k = 0; k < NV; ++k) P.partials[blockIdx.x * 4 + k] = v[k];
+        for (int k = 0; k < NV; ++k) const_cast<double*>(part)[blockIdx.x * 4 + k] = v[k];
     grid_barrier(P.bar, gridDim.x, epoch);
     const int lane = threadIdx.x & 31;
     if (threadIdx.x < 32) {
 #pragma unroll
         for (int k = 0; k < NV; ++k) {
             double s = 0.0;
-            for (int g = lane; g < (int)gridDim.x; g += 32) s += __ldcg(P.partials + g * 4 + k);
+            for (int g = lane; g < (int)gridDim.x; g += 32) s += __ldcg(part + g * 4 + k);
             s = warp_sum(s);
             if (lane == 0) sh[k * 32] = s;
         }
@@ -163,14 +173,16 @@ struct RedState {
     unsigned int epoch = 0;
     int par = 0, bpar = 0;
 };
-// idx / n: this CTA's slot and the number of CTAs taking part (one solve of a batch)
+// idx / n: this CTA's slot and the number of CTAs taking part (one solve of a batch).
+// Consecutive reductions alternate between two banks of partials (kPartialBank).
 template <int NV>
 __device__ __forceinline__ void grid_reduce(double (&v)[NV], double* sh, const CgParams& P, RedState& st, int idx,
                                             int n) {
     block_sum1<NV>(v, sh, st.par);
+    double* part = P.partials + ((st.epoch + 1) & 1) * kPartialBank;
     if (threadIdx.x == 0)
 #pragma unroll
-        for (int k = 0; k < NV; ++k) P.partials[idx * 4 + k] = v[k];
+        for (int k = 0; k < NV; ++k) part[idx * 4 + k] = v[k];
     grid_arrive_wait(P.bar, n, st.epoch);
     double* bc = sh + 2 * 4 * 32 + st.bpar * 4;
     st.bpar ^= 1;
@@ -179,7 +191,7 @@ __device__ __forceinline__ void grid_reduce(double (&v)[NV], double* sh, const C
 #pragma unroll
         for (int k = 0; k < NV; ++k) {
             double s = 0.0;
-            for (int g = lane; g < n; g += 32) s += __ldcg(P.partials + g * 4 + k);
+            for (int g = lane; g < n; g += 32) s += __ldcg(part + g * 4 + k);
             s = warp_sum(s);
             if (lane == 0) bc[k] = s;
         }
@@ -193,15 +205,17 @@ template <int NV>
 __device__ __forceinline__ void grid_reduce_arrive(double (&v)[NV], double* sh, const CgParams& P, RedState& st,
                                                    int idx) {
     block_sum1<NV>(v, sh, st.par);
+    double* part = P.partials + ((st.epoch + 1) & 1) * kPartialBank;
     if (threadIdx.x == 0)
 #pragma unroll
-        for (int k = 0; k < NV; ++k) P.partials[idx * 4 + k] = v[k];
+        for (int k = 0; k < NV; ++k) part[idx * 4 + k] = v[k];
     grid_arrive(P.bar, st.epoch);
 }
 template <int NV>
 __device__ __forceinline__ void grid_reduce_finish(double (&v)[NV], double* sh, const CgParams& P, RedState& st,
                                                    int n) {
     grid_wait(P.bar, n, st.epoch);
+    const double* part = P.partials + (st.epoch & 1) * kPartialBank;
     double* bc = sh + 2 * 4 * 32 + st.bpar * 4;
     st.bpar ^= 1;
     if (threadIdx.x < 32) {
@@ -209,7 +223,7 @@ __device__ __forceinline__ void grid_reduce_finish(double (&v)[NV], double* sh, 
 #pragma unroll
         for (int k = 0; k < NV; ++k) {
             double s = 0.0;
-            for (int g = lane; g < n; g += 32) s += __ldcg(P.partials + g * 4 + k);
+            for (int g = lane; g < n; g += 32) s += __ldcg(part + g * 4 + k);
             s = warp_sum(s);
             if (lane == 0) bc[k] = s;
         }
@@ -348,6 +362,7 @@ __global__ void __launch_bounds__(kThreads, 1) cg_level_kernel(CgParams P) {
 
 #include "cg_band.cuh"
 #include "cg_band2.cuh"
+#include "cg_tile.cuh"
 #include "cg_small.cuh"
 #include "cg_cluster.cuh"
 
@@ -414,7 +429,8 @@ void InpaintWorkspace::reserve(int h, int w, int dev) {
     CUDA_CHECK(cudaMalloc(&iters, 64 * sizeof(int)));
     CUDA_CHECK(cudaMalloc(&margins, 64 * sizeof(double)));
     // band-kernel row exchange: r (nb x 2 rows) + p (2 parities x nb x 2 rows)
-    CUDA_CHECK(cudaMalloc(&ex, (size_t)6 * std::max(num_sms, 1) * w * sizeof(double)));
+    ex_cap = (size_t)6 * std::max(num_sms, 1) * w;
+    CUDA_CHECK(cudaMalloc(&ex, ex_cap * sizeof(double)));
     cap_px = n;
     cap_w = w;
     cap_coarse = coarse;
@@ -425,6 +441,9 @@ void InpaintWorkspace::reserve(int h, int w, int dev) {
     CUDA_CHECK(cudaFuncSetAttribute(cg_band2_kernel<8, 4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBand2Smem));
     CUDA_CHECK(cudaFuncSetAttribute(cg_band2_kernel<kPackRows, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     kBand2Smem));
+    CUDA_CHECK(cudaFuncSetAttribute(cg_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kBand2Smem));
+    const char* env_tile = getenv("HIVC_CG_TILE");
+    tile_enabled = !(env_tile && env_tile[0] == '0');
     const char* env_pack = getenv("HIVC_CG_PACK");
     pack_env_off = env_pack && env_pack[0] == '0';
     if (env_pack && env_pack[0] == '2') pack_bands = true;  // experiments: throughput mode for single solves too
@@ -496,6 +515,39 @@ size_t band2_smem(int rows_tpl, int band_rows, int w, CgParams* P, int K) {
         xr = (int)std::min<size_t>((size_t)band_rows, ((size_t)kBand2Smem - p_bytes) / ((size_t)w * sizeof(double)));
     for (int j = 0; j < K; ++j) P[j].x_rows = xr;
     return p_bytes + (size_t)xr * w * sizeof(double);
+}
+
+// 2-D tile layout of a grid level for cg_tile_kernel: at most `budget` tiles
+// of <= kTileRows rows x <= 512 columns, p + as many x rows as fit in smem.
+struct TilePlan {
+    bool ok = false;
+    int trows = 0, tcols = 0, ntc = 0, nt = 0, xr = 0;
+    size_t smem = 0, ex = 0;  // dynamic smem bytes, exchange doubles (r + 2 parities of p)
+};
+TilePlan plan_tiles(int h, int w, int budget) {
+    TilePlan T;
+    const int tc = (w + kTileThreads - 1) / kTileThreads;
+    const int tcols = (w + tc - 1) / tc;
+    const int tr_max = budget / tc;
+    if (tr_max < 1) return T;
+    const int trows = (h + tr_max - 1) / tr_max;
+    if (trows > kTileRows || trows < 1) return T;
+    const int ntr = (h + trows - 1) / trows;
+    const size_t p_bytes = (size_t)(trows + 2) * (tcols + 2) * sizeof(double);
+    if (p_bytes > (size_t)kBand2Smem) return T;
+    const char* e = getenv("HIVC_CG_XRES");
+    int xr = 0;
+    if (!(e && e[0] == '0'))
+        xr = (int)std::min<size_t>((size_t)trows, ((size_t)kBand2Smem - p_bytes) / ((size_t)tcols * sizeof(double)));
+    T.ok = true;
+    T.trows = trows;
+    T.tcols = tcols;
+    T.ntc = tc;
+    T.nt = ntr * tc;
+    T.xr = xr;
+    T.smem = p_bytes + (size_t)xr * tcols * sizeof(double);
+    T.ex = 3 * (size_t)T.nt * (2 * (size_t)tcols + 2 * (size_t)trows);
+    return T;
 }
 
 // Per-job views of its workspace: finest CG vectors + every level's f, m, u.
@@ -718,6 +770,10 @@ int solve_batch_async(const SolveJob* jobs, int K, int h, int w, double tol, int
         const size_t band_smem = (size_t)(kBandRows + 2) * (ww + 2) * sizeof(double) + (size_t)kBandRows * ww;
         const bool band = grid && ws0.band_enabled && P[0].uc != nullptr && (pack || band_rows <= kBandRows) &&
                           ww <= kBandCols * kBandThreads && band_smem <= 220 * 1024 && nbands <= ws0.num_sms;
+        // 2-D tiles (default for band levels): packed solves get a quarter of the SMs each
+        const bool pack_t = ws0.pack_bands && !ws0.pack_env_off && kc <= 2;
+        const TilePlan TP = plan_tiles(hh, ww, pack_t ? ws0.num_sms / 4 : ws0.num_sms);
+        const bool tile = band && ws0.tile_enabled && TP.ok && TP.ex <= ws0.ex_cap;
         CgProbe::Launch rec{};
         if (probe && grid) {
             rec.stamp_base = probe->next_stamp;
@@ -735,6 +791,62 @@ int solve_batch_async(const SolveJob* jobs, int K, int h, int w, double tol, int
             for (int j = 0; j < K; ++j) {
                 cg_level_kernel<false><<<1, kThreads, 0, s>>>(P[j]);
                 ++*launches;
+            }
+        } else if (tile) {
+            SetupBatch SB{};
+            TileBatch TB{};
+            const size_t E = 2 * (size_t)TP.tcols + 2 * (size_t)TP.trows;
+            for (int j = 0; j < K; ++j) {
+                InpaintWorkspace& ws = *jobs[j].ws;
+                P[j].band_rows = TP.trows;
+                P[j].tile_cols = TP.tcols;
+                P[j].ntc = TP.ntc;
+                P[j].x_rows = TP.xr;
+                P[j].ex_r = ws.ex;
+                P[j].ex_p = ws.ex + (size_t)TP.nt * E;
+                SB.P[j] = P[j];
+                SB.partials[j] = ws.partials + 4096;
+                TB.P[j] = P[j];
+                TB.setup[j] = ws.partials + 4096;
+            }
+            if (getenv("HIVC_CG_TRACE") && l == 0 && K == 1) {
+                if (!ws0.trace) CUDA_CHECK(cudaMalloc(&ws0.trace, kTraceLen * sizeof(unsigned long long)));
+                CUDA_CHECK(cudaMemsetAsync(ws0.trace, 0, kTraceLen * sizeof(unsigned long long), s));
+                SB.P[0].trace = TB.P[0].trace = ws0.trace;
+            }
+            unsigned int* ticket = ws0.bar + 32;
+            const bool ticketed = pack_t && K > 1;
+            SB.ticket = ticketed ? ticket : nullptr;
+            mb("setup l=" + std::to_string(l), s);
+            cg_setup_x_kernel<<<dim3(kSetupCtas, K), 512, 0, s>>>(SB);
+            cg_setup_kernel<<<dim3(kSetupCtas, K), 512, 0, s>>>(SB);
+            me(s);
+            *launches += 2;
+            mb(std::string(ticketed ? "tile-ticket" : "tile-coop") + " l=" + std::to_string(l) + " nt=" +
+                   std::to_string(TP.nt) + " " + std::to_string(TP.trows) + "x" + std::to_string(TP.tcols),
+               s);
+            rec_begin();
+            TB.nt = TP.nt;
+            if (ticketed) {
+                TB.ticket = ticket;
+                cg_tile_kernel<<<TP.nt * K, kTileThreads, TP.smem, s>>>(TB);
+                ++*launches;
+            } else {
+                for (int j = 0; j < K; ++j) {
+                    TileBatch one{};
+                    one.P[0] = TB.P[j];
+                    one.setup[0] = TB.setup[j];
+                    one.nt = TP.nt;
+                    one.ticket = nullptr;
+                    void* args[] = {&one};
+                    CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)cg_tile_kernel, dim3(TP.nt),
+                                                           dim3(kTileThreads), args, TP.smem, s));
+                    ++*launches;
+                    if (l == 0 && jobs[j].done) {
+                        CUDA_CHECK(cudaEventRecord(jobs[j].done, s));
+                        recorded[j] = true;
+                    }
+                }
             }
         } else if (band) {
             SetupBatch SB{};
@@ -817,7 +929,7 @@ int solve_batch_async(const SolveJob* jobs, int K, int h, int w, double tol, int
             }
         }
         CUDA_CHECK(cudaGetLastError());
-        if (band) me(s);
+        if (band || tile) me(s);
         if (probe && grid) {
             CUDA_CHECK(cudaEventRecord(rec.stop, s));
             rec.pixels = P[0].n;

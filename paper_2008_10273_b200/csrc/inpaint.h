@@ -40,6 +40,8 @@ struct InpaintWorkspace {
     // (HIVC_CG_PACK=0 disables); latency mode spreads a level over every SM
     bool pack_bands = false;
     bool pack_env_off = false;
+    bool tile_enabled = true;  // 2-D tile CG kernel for band levels (HIVC_CG_TILE=0: row bands)
+    size_t ex_cap = 0;         // doubles in ex
     double* dbl = nullptr;
     uint8_t* bytes = nullptr;
     double* partials = nullptr;

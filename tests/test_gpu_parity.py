@@ -212,3 +212,19 @@ def test_flow_brox_vs_oracle_larger():
     ru, rv = brox.brox(clip[1], clip[0])
     ff = flow_brox(clip[1], clip[0])
     assert max(np.abs(ff.u - ru).max(), np.abs(ff.v - rv).max()) <= 1e-6
+
+
+def test_solve_homogeneous_repeatable_across_shapes():
+    """Interleaved solves of different shapes (workspace reuse, both CG kernels) stay bit-identical."""
+    from paper_2008_10273_b200.homogeneous import solve_homogeneous
+
+    cases = []
+    for h, w, seed in [(300, 500, 5), (540, 960, 6), (301, 517, 7)]:
+        rng = np.random.default_rng(seed)
+        m = rng.uniform(size=(h, w)) < 0.03
+        f = np.where(m, rng.uniform(0, 255, m.shape), 0.0)
+        cases.append((f, m))
+    first = [solve_homogeneous(f, m, tol=1e-4, max_iter=160, strict=False) for f, m in cases]
+    for _ in range(3):
+        for (f, m), ref in zip(cases, first):
+            assert np.array_equal(solve_homogeneous(f, m, tol=1e-4, max_iter=160, strict=False), ref)
