@@ -358,7 +358,7 @@ def main():
             "stages_ms_per_step": {k: round(1e3 * v / args.steps, 3) for k, v in timings.items()},
             "roofline": {
                 "kernel": ("cg_level_kernel<grid> (streaming CG level, float64)" if os.environ.get("HIVC_CG_BAND") == "0"
-                           else "cg_band_kernel (on-chip CG level, float64; x streamed, r in registers, p in smem)"),
+                           else "cg_tile_kernel (on-chip CG level over 30x480 tiles, float64: r in registers, p + ~all of x in smem)"),
                 "algorithmic_bytes": "N_l*(49*it_l + 49) per level launch: float64 x, r, p read+write + mask byte "
                                      "per iteration, plus the setup/finalise pass",
                 "bound": "hbm",

@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cmath>
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <thread>
@@ -623,7 +624,11 @@ size_t parse_intra(const uint8_t* d, size_t len, size_t pos, int32_t h, int32_t 
     static const int kHw = (int)std::max(1u, std::thread::hardware_concurrency());
     // (the decoder already runs one parse per GOP on its own thread: only the
     // largest planes, whose I-frame parse is on the critical path, fan out)
-    const int tree_threads = npx >= (1u << 20) ? std::min(4, kHw) : 1;
+    static const int kTreeThreads = [] {
+        const char* e = getenv("HIVC_TREE_THREADS");
+        return e ? std::max(1, atoi(e)) : 4;
+    }();
+    const int tree_threads = npx >= (1u << 20) ? std::min(kTreeThreads, kHw) : 1;
     std::vector<int32_t>* idx = job.idx;
     std::exception_ptr verr[3], terr[2];
     auto decode_vals = [&]() {
