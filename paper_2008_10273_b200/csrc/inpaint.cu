@@ -770,9 +770,11 @@ int solve_batch_async(const SolveJob* jobs, int K, int h, int w, double tol, int
         const size_t band_smem = (size_t)(kBandRows + 2) * (ww + 2) * sizeof(double) + (size_t)kBandRows * ww;
         const bool band = grid && ws0.band_enabled && P[0].uc != nullptr && (pack || band_rows <= kBandRows) &&
                           ww <= kBandCols * kBandThreads && band_smem <= 220 * 1024 && nbands <= ws0.num_sms;
-        // 2-D tiles (default for band levels): packed solves get a quarter of the SMs each
-        const bool pack_t = ws0.pack_bands && !ws0.pack_env_off && kc <= 2;
-        const TilePlan TP = plan_tiles(hh, ww, pack_t ? ws0.num_sms / 4 : ws0.num_sms);
+        // 2-D tiles (default for band levels): packed solves share the SMs,
+        // at most 4 side by side (a lone solve gets the whole GPU)
+        const int side = std::min(K, 4);
+        const bool pack_t = ws0.pack_bands && !ws0.pack_env_off && kc <= 2 && side > 1;
+        const TilePlan TP = plan_tiles(hh, ww, pack_t ? ws0.num_sms / side : ws0.num_sms);
         const bool tile = band && ws0.tile_enabled && TP.ok && TP.ex <= ws0.ex_cap;
         CgProbe::Launch rec{};
         if (probe && grid) {

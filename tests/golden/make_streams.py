@@ -3,10 +3,12 @@ the reference decoder's output for them.
 
 Run here (the container that has /root/reference), never on the GPU box:
 
-    OMP_NUM_THREADS=1 OPENBLAS_NUM_THREADS=1 python tests/golden/make_streams.py [cfg0] [cfg3]
+    OMP_NUM_THREADS=1 OPENBLAS_NUM_THREADS=1 python tests/golden/make_streams.py [cfg0] [rgb] [cfg3]
 
 Outputs (committed, small):
   tests/golden/streams/cfg0.hivc            config 0: 320x180 gray, 10 frames, GOP 10, intra 4 %
+  tests/golden/streams/rgb.hivc             colour: 96x128 RGB, 7 frames, GOP 4 (RCT path)
+  tests/golden/rgb_frames.npz               reference-decoded colour frames (uint8, n x 3 x h x w)
   tests/golden/streams/cfg3_{Y,Cb,Cr}.hivc  config 3: 60-frame 1080p 4:2:0 as three gray streams, GOP 12
   tests/golden/cfg0_frames.npz              reference-decoded config-0 frames (uint8)
   tests/golden/cfg3_{plane}_sums.npz        per-frame sha256 + row/column sums of the reference decode
@@ -87,6 +89,32 @@ def make_cfg0():
             "timings": timings,
         }
     }
+
+
+# ----------------------------------------------------------------------------- colour (RCT) stream
+
+
+def make_rgb():
+    """A small 3-channel RGB clip (RCT domain inside the codec, frame.py:70-93):
+    7 frames of 96x128 in GOPs of 4 (I P P P | I P P), intra 6 %, encoded and
+    decoded by the reference; exercises the colour path (shared chroma tree,
+    the U/V intra levels 2L-1, the [-255, 255] chroma clip, RCT inverse)."""
+    codec, _, _, Frame = _ref()
+    clip = to_codec_planes(synth_clip(7, 96, 128, blobs=6, rects=3, v=2.0, seed=7, channels=3))
+    frames = [Frame(tuple(f[c] for c in range(3)), colorspace="rgb") for f in clip]
+    cfg = codec.EncoderConfig(gop_size=4, intra_mask_fraction=0.06)
+    t0 = time.perf_counter()
+    stream = codec.encode(frames, cfg)
+    t_enc = time.perf_counter() - t0
+    timings = {}
+    t0 = time.perf_counter()
+    dec = codec.decode(stream, timings)
+    t_dec = time.perf_counter() - t0
+    (STREAMS / "rgb.hivc").write_bytes(stream)
+    out = np.stack([np.stack(f.planes) for f in dec]).astype(np.uint8)
+    np.savez_compressed(HERE / "rgb_frames.npz", frames=out, colorspace=np.array([f.colorspace for f in dec]))
+    return {"rgb.hivc": {"sha256": _sha(stream), "bytes": len(stream), "encode_s": t_enc, "decode_s": t_dec,
+                         "timings": timings}}
 
 
 # ----------------------------------------------------------------------------- config 3
@@ -228,6 +256,9 @@ if __name__ == "__main__":
     manifest = json.loads(mpath.read_text()) if mpath.exists() else {}
     if "cfg0" in which:
         manifest.update(make_cfg0())
+        mpath.write_text(json.dumps(manifest, indent=1, sort_keys=True))
+    if "rgb" in which:
+        manifest.update(make_rgb())
         mpath.write_text(json.dumps(manifest, indent=1, sort_keys=True))
     if "cfg3" in which:
         manifest.update(make_cfg3())

@@ -132,6 +132,26 @@ def test_decode_config0_matches_reference(cfg0_stream, cfg0_frames):
         assert k in timings
 
 
+def test_decode_rgb_matches_reference():
+    """3-channel stream: shared chroma intra tree, RCT inverse, [-255, 255] chroma clip."""
+    from pathlib import Path
+
+    from paper_2008_10273_b200 import codec
+
+    g = Path(__file__).resolve().parent / "golden"
+    stream = (g / "streams" / "rgb.hivc").read_bytes()
+    ref = np.load(g / "rgb_frames.npz")["frames"]
+    frames = codec.decode(stream)
+    assert all(f.colorspace == "rgb" for f in frames)
+    got = np.stack([np.stack(f.planes) for f in frames]).astype(np.int32)
+    assert got.shape == ref.shape
+    diff = np.abs(got - ref.astype(np.int32))
+    assert diff.max() <= 1
+    assert int((diff != 0).sum()) == 0, f"{int((diff != 0).sum())} samples differ by one grey level"
+    dev = codec.decode_frames(stream, out=torch.empty(ref.shape, dtype=torch.uint8, device="cuda"))
+    assert np.array_equal(dev.cpu().numpy(), ref)
+
+
 def test_decode_is_deterministic(cfg0_stream):
     from paper_2008_10273_b200 import codec
 

@@ -8,6 +8,18 @@ import pytest
 from oracle import blocks, decoder, inpaint, motion, parse
 
 
+def test_oracle_decodes_rgb_like_the_reference():
+    """Colour stream (RCT, shared chroma tree, [-255, 255] chroma clip) decoded by the
+    reference decoder (tests/golden/make_streams.py rgb)."""
+    from conftest import GOLDEN
+
+    stream = (GOLDEN / "streams" / "rgb.hivc").read_bytes()
+    ref = np.load(GOLDEN / "rgb_frames.npz")["frames"]
+    got = np.stack([np.stack(f) for f in decoder.decode_stream(stream)])
+    assert got.shape == ref.shape
+    assert np.array_equal(got, ref)
+
+
 def test_oracle_decodes_config0_like_the_reference(cfg0_stream, cfg0_frames):
     frames = decoder.decode_stream(cfg0_stream)
     got = np.stack([f[0] for f in frames]).astype(np.uint8)
