@@ -442,6 +442,8 @@ void InpaintWorkspace::reserve(int h, int w, int dev) {
     CUDA_CHECK(cudaFuncSetAttribute(cg_band2_kernel<kPackRows, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     kBand2Smem));
     CUDA_CHECK(cudaFuncSetAttribute(cg_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kBand2Smem));
+    const char* env_clmax = getenv("HIVC_CL_MAXPX");
+    cluster_max_px = env_clmax ? (size_t)atoll(env_clmax) : (size_t)1 << 40;
     const char* env_tile = getenv("HIVC_CG_TILE");
     tile_enabled = !(env_tile && env_tile[0] == '0');
     const char* env_pack = getenv("HIVC_CG_PACK");
@@ -671,6 +673,7 @@ int solve_batch_async(const SolveJob* jobs, int K, int h, int w, double tol, int
             const size_t need =
                 ((size_t)(br + 2) * (ww + 2) + (size_t)br * ww + 6 * (size_t)ww) * sizeof(double) + (size_t)br * ww;
             if ((size_t)br * ww > (size_t)kClPx * kClThreads || ww > kClMaxW || need > 200 * 1024) break;
+            if ((size_t)hh * ww > ws0.cluster_max_px) break;  // larger levels go to the tile kernel
             for (int j = 0; j < K; ++j) {
                 ClusterLevels& S = CB.S[j];
                 S.h[nlev] = hh;

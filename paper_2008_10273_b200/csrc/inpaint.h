@@ -42,6 +42,7 @@ struct InpaintWorkspace {
     bool pack_env_off = false;
     bool tile_enabled = true;  // 2-D tile CG kernel for band levels (HIVC_CG_TILE=0: row bands)
     size_t ex_cap = 0;         // doubles in ex
+    size_t cluster_max_px = (size_t)1 << 40;  // cluster kernel only for levels up to this size
     double* dbl = nullptr;
     uint8_t* bytes = nullptr;
     double* partials = nullptr;
