@@ -123,6 +123,24 @@ int hivc_homog_solve(hivc_ctx* ctx, const double* f, const uint8_t* mask, int32_
                      double tol, int32_t max_iter, int32_t strict,
                      double* u, int32_t* level_sizes, int32_t* level_iters, int32_t* nlevels);
 
+/* ------------------------------------------------------------------ tonal optimisation operator
+ * The two solves of prediction.optimize_mask_values (prediction.py:43-96),
+ * whose LSQR operator is v -> A^-1 [v on the mask points] and its adjoint
+ * w -> (A^-T w)[mask points], A = diag(d) + diag(1 - d) L (prediction.py:43-61,
+ * factorised there with splu).  The forward solve is hivc_homog_solve; the
+ * adjoint needs the interior system L_II z_I = w_I (zeros on the mask) and
+ * then z_M = w_M - (L z)_M:
+ *   hivc_poisson_interior: CG from 0 until ||r|| <= tol ||w_I||; z gets the
+ *     full plane (zeros on the mask); *iters the CG iterations.
+ *   hivc_mask_adjoint: out[k] = w[pts[k]] - sum of z over pts[k]'s existing
+ *     4-neighbours.
+ * All pointers are device pointers.
+ */
+int hivc_poisson_interior(hivc_ctx* ctx, const double* w_full, const uint8_t* mask, int32_t h, int32_t w,
+                          double tol, int32_t max_iter, double* z, int32_t* iters);
+int hivc_mask_adjoint(hivc_ctx* ctx, const double* w_full, const double* z, const int32_t* pts, int32_t npts,
+                      int32_t h, int32_t w, double* out);
+
 /* ------------------------------------------------------------------ warp
  * Replaces flow.warp_planes (flow.py:94-127): every plane sampled at
  * (x+u, y+v), clamped bilinear, float64.  src/dst: host arrays of `nplanes`

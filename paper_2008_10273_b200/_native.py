@@ -61,6 +61,10 @@ _proto("hivc_parse_tree", C.c_int, C.c_void_p, C.c_size_t, C.c_uint64, C.c_uint6
        C.c_size_t, c_size_p, c_u64_p)
 _proto("hivc_homog_solve", C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_double, C.c_int32,
        C.c_int32, C.c_void_p, c_int_p, c_int_p, c_int_p)
+_proto("hivc_poisson_interior", C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_double,
+       C.c_int32, C.c_void_p, c_int_p)
+_proto("hivc_mask_adjoint", C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
+       C.c_void_p)
 _proto("hivc_warp", C.c_int, C.c_void_p, C.POINTER(C.c_void_p), C.c_int32, C.c_void_p, C.c_void_p, C.c_int32,
        C.c_int32, C.POINTER(C.c_void_p))
 _proto("hivc_block_reconstruct", C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p)

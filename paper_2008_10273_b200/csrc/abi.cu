@@ -239,6 +239,33 @@ int hivc_homog_solve(hivc_ctx* ctx, const double* f, const uint8_t* mask, int32_
     });
 }
 
+int hivc_poisson_interior(hivc_ctx* ctx, const double* w_full, const uint8_t* mask, int32_t h, int32_t w,
+                          double tol, int32_t max_iter, double* z, int32_t* iters) {
+    return guarded([&] {
+        if (!ctx) hivc::fail(HIVC_E_ARGUMENT, "null context");
+        if (h < 1 || w < 1) hivc::fail(HIVC_E_INPAINTING, "plane/mask shape mismatch");
+        hivc::Context& C = ctx->c;
+        CUDA_CHECK(cudaSetDevice(C.device));
+        C.ws.reserve(h, w, C.device);
+        int64_t launches = 0;
+        int it = hivc::solve_poisson_interior(C.ws, C.stream, w_full, mask, h, w, tol, max_iter, z, &launches);
+        C.launches += launches;
+        if (iters) *iters = it;
+    });
+}
+
+int hivc_mask_adjoint(hivc_ctx* ctx, const double* w_full, const double* z, const int32_t* pts, int32_t npts,
+                      int32_t h, int32_t w, double* out) {
+    return guarded([&] {
+        if (!ctx) hivc::fail(HIVC_E_ARGUMENT, "null context");
+        hivc::Context& C = ctx->c;
+        CUDA_CHECK(cudaSetDevice(C.device));
+        hivc::launch_mask_adjoint(w_full, z, pts, npts, h, w, out, C.stream);
+        C.launches += 1;
+        CUDA_CHECK(cudaStreamSynchronize(C.stream));
+    });
+}
+
 int hivc_warp(hivc_ctx* ctx, const double* const* src, int32_t nplanes, const double* u, const double* v, int32_t h,
               int32_t w, double* const* dst) {
     return guarded([&] {

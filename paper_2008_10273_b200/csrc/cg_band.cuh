@@ -60,6 +60,29 @@ __global__ void __launch_bounds__(512) cg_setup_x_kernel(const __grid_constant__
         P.x[i] = prolong_at(P, i / w, i % w) * (P.m[i] ? 0.0 : 1.0);
 }
 
+// Poisson mode (LSQR adjoint, prediction.optimize_mask_values): x = 0,
+// r = b = -rhs on the interior (zero on the mask) and the level partials
+// (r.r, b.b, 0, #interior), so the level kernel solves (-L_II) x = -rhs_I,
+// i.e. L_II x = rhs_I with zero values held on the mask.
+__global__ void __launch_bounds__(512) cg_setup_rhs_kernel(CgParams P, const double* __restrict__ rhs,
+                                                           double* partials) {
+    __shared__ double sh[4 * 32];
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    if (blockIdx.x == 0 && threadIdx.x == 0) P.bar[0] = 0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P.n; i += gridDim.x * blockDim.x) {
+        const bool mi = P.m[i] != 0;
+        const double b = mi ? 0.0 : -__ldg(rhs + i);
+        P.x[i] = 0.0;
+        P.r[i] = b;
+        acc[0] += b * b;
+        acc[1] += b * b;
+        acc[3] += mi ? 0.0 : 1.0;
+    }
+    block_sum<4>(acc, sh);
+    if (threadIdx.x == 0)
+        for (int k = 0; k < 4; ++k) partials[blockIdx.x * 4 + k] = acc[k];
+}
+
 // setup pass 2: b = L(u_D) * interior, r = b - A x and the level partials
 __global__ void __launch_bounds__(512) cg_setup_kernel(const __grid_constant__ SetupBatch B) {
     __shared__ double sh[4 * 32];

@@ -961,6 +961,84 @@ int solve_batch_async(const SolveJob* jobs, int K, int h, int w, double tol, int
     return L;
 }
 
+// out[k] = w[pts[k]] - sum of z over the existing 4-neighbours of pts[k]
+// (z is zero on the mask): the mask rows of A^T z = w solved for z_M once
+// z_I is known (A = diag(d) + diag(1 - d) L, L the reflecting graph Laplacian).
+__global__ void mask_adjoint_kernel(const double* __restrict__ w_full, const double* __restrict__ z,
+                                    const int32_t* __restrict__ pts, int npts, int h, int w, double* __restrict__ out) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= npts) return;
+    const int p = pts[k], y = p / w, x = p - y * w;
+    double s = 0.0;  // neighbours in the order of the sparse row (north, south, west, east)
+    if (y > 0) s += z[p - w];
+    if (y < h - 1) s += z[p + w];
+    if (x > 0) s += z[p - 1];
+    if (x < w - 1) s += z[p + 1];
+    out[k] = w_full[p] - s;
+}
+
+int solve_poisson_interior(InpaintWorkspace& ws, cudaStream_t s, const double* rhs, const uint8_t* m, int h, int w,
+                           double tol, int max_iter, double* z_out, int64_t* launches) {
+    // single level, x0 = 0; the level kernel writes u = (mask ? f : 0) + x with f = 0
+    const size_t n = (size_t)h * w;
+    double* x = ws.dbl;
+    double* r = x + n;
+    double* zero_f = r + 3 * n;  // (the ap slot: unused by the tile kernel) zeroed as f
+    CUDA_CHECK(cudaMemsetAsync(zero_f, 0, n * sizeof(double), s));
+    CgParams P{};
+    P.h = h;
+    P.w = w;
+    P.n = (int)n;
+    P.f = zero_f;
+    P.m = m;
+    P.uc = nullptr;
+    P.x = x;
+    P.r = r;
+    P.pa = r + n;
+    P.pb = r + 2 * n;
+    P.ap = zero_f;
+    P.u = z_out;
+    P.tol = tol;
+    P.max_iter = max_iter;
+    P.finest = 0;  // denominator ||b||
+    P.partials = ws.partials;
+    P.bar = ws.bar;
+    P.iters = ws.iters;
+    P.margin = ws.margins;
+    const TilePlan TP = plan_tiles(h, w, ws.num_sms);
+    if (!TP.ok || TP.ex > ws.ex_cap) fail(HIVC_E_ARGUMENT, "plane shape not supported by the interior solver");
+    const size_t E = 2 * (size_t)TP.tcols + 2 * (size_t)TP.trows;
+    P.band_rows = TP.trows;
+    P.tile_cols = TP.tcols;
+    P.ntc = TP.ntc;
+    P.x_rows = TP.xr;
+    P.ex_r = ws.ex;
+    P.ex_p = ws.ex + (size_t)TP.nt * E;
+    double* setup = ws.partials + 4096;
+    cg_setup_rhs_kernel<<<kSetupCtas, 512, 0, s>>>(P, rhs, setup);
+    TileBatch one{};
+    one.P[0] = P;
+    one.setup[0] = setup;
+    one.nt = TP.nt;
+    one.ticket = nullptr;
+    void* args[] = {&one};
+    CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)cg_tile_kernel, dim3(TP.nt), dim3(kTileThreads), args,
+                                           TP.smem, s));
+    *launches += 3;
+    CUDA_CHECK(cudaGetLastError());
+    int it = 0;
+    CUDA_CHECK(cudaMemcpyAsync(&it, ws.iters, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CUDA_CHECK(cudaStreamSynchronize(s));
+    return it;
+}
+
+void launch_mask_adjoint(const double* w_full, const double* z, const int32_t* pts, int npts, int h, int w, double* out,
+                         cudaStream_t s) {
+    if (npts <= 0) return;
+    mask_adjoint_kernel<<<(npts + 255) / 256, 256, 0, s>>>(w_full, z, pts, npts, h, w, out);
+    CUDA_CHECK(cudaGetLastError());
+}
+
 int* CgProbe::alloc_iters() {
     if (!host) {
         if (cudaHostAlloc(&host, kCap * 32 * sizeof(int), cudaHostAllocDefault) != cudaSuccess) host = nullptr;

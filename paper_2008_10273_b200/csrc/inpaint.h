@@ -134,6 +134,16 @@ struct SolveJob {
 int solve_batch_async(const SolveJob* jobs, int K, int h, int w, double tol, int max_iter, cudaStream_t s,
                       int64_t* launches, CgProbe* probe = nullptr, cudaStream_t s_pre = nullptr);
 
+// L_II z_I = rhs_I with z = 0 held on the mask (the interior rows of the
+// transpose inpainting system, for the LSQR adjoint of
+// prediction.optimize_mask_values): CG from 0 until ||r|| <= tol ||rhs_I||.
+// z_out receives the full plane (zeros on the mask).  Returns the iterations.
+int solve_poisson_interior(InpaintWorkspace& ws, cudaStream_t s, const double* rhs, const uint8_t* m, int h, int w,
+                           double tol, int max_iter, double* z_out, int64_t* launches);
+// out[k] = w[pts[k]] - (sum of z over pts[k]'s existing 4-neighbours)
+void launch_mask_adjoint(const double* w_full, const double* z, const int32_t* pts, int npts, int h, int w, double* out,
+                         cudaStream_t s);
+
 // Relative residual of the inpainting equation (homogeneous.py:206-211);
 // synchronises the stream.  Returns -1 when ||f|mask|| == 0.
 double strict_relative_residual(InpaintWorkspace& ws, cudaStream_t s, const double* u, const double* f,

@@ -112,11 +112,42 @@ def config4_brox(reps, cpu):
                           "cpu_reference_seconds_per_pair_survey": 948.2 if sc == 0.95 else 126.4}), flush=True)
 
 
+def tonal(reps, cpu):
+    """prediction.optimize_mask_values on a 1080p luma
+    I-frame with the reference encoder's own mask (config-3 Y stream, GOP 0)."""
+    import ctypes as C
+
+    from paper_2008_10273_b200 import _native as N
+    from paper_2008_10273_b200.prediction import optimize_mask_values
+    from paper_2008_10273_b200.synth import synth_420
+
+    data = (REPO / "tests/golden/streams/cfg3_Y.hivc").read_bytes()
+    h, w = 1080, 1920
+    # mask points of GOP 0's I-frame: the first frame record's tree (native parser)
+    pos = 22 + 4 + 2 + 5
+    nbits = int.from_bytes(data[pos:pos + 4], "little")
+    cap = h * w
+    rects = (C.c_int32 * (4 * cap))()
+    nl, used = C.c_size_t(), C.c_uint64()
+    blob = data[pos + 4: pos + 4 + (nbits + 7) // 8]
+    N.check(N.lib.hivc_parse_tree(blob, len(blob), nbits, 0, w, h, rects, cap, C.byref(nl), C.byref(used)))
+    r = np.frombuffer(rects, dtype=np.int32)[: 4 * nl.value].reshape(-1, 4)
+    mask = np.zeros((h, w), bool)
+    mask[r[:, 1] + r[:, 3] // 2, r[:, 0] + r[:, 2] // 2] = True
+    y = synth_420(1, h, w, blobs=40, rects=12, v=6.0, seed=3)[0][0].astype(np.float64)
+    st = {}
+    sec = timed(lambda: optimize_mask_values([y], mask, stats=st), reps)
+    print(json.dumps({"config": "f1", "what": "tonal optimisation (LSQR x12 over GPU inpainting solves), 1080p luma "
+                      "I-frame, reference encoder mask", "mask_points": int(mask.sum()), "seconds": sec,
+                      "solver_iterations": st.get("solver_iterations"),
+                      "cpu_reference_seconds_survey": 112.0}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--cpu", action="store_true")
-    ap.add_argument("--only", default="1,2,4")
+    ap.add_argument("--only", default="1,2,4,f1")
     a = ap.parse_args()
     only = a.only.split(",")
     if "1" in only:
@@ -125,6 +156,8 @@ def main():
         config2(a.reps, a.cpu)
     if "4" in only:
         config4_brox(max(1, a.reps // 2), a.cpu)
+    if "f1" in only:
+        tonal(max(1, a.reps // 2), a.cpu)
 
 
 if __name__ == "__main__":
