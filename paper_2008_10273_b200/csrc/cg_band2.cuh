@@ -11,10 +11,7 @@
 // for phase 2 (small bands) instead of being recomputed.
 #pragma once
 
-#ifndef HIVC_XG
-#define HIVC_XG 8
-#endif
-constexpr int kXG = HIVC_XG;  // streamed-x values per batch of loads
+constexpr int kXG = 8;  // streamed-x values per batch of loads
 
 template <int ROWS, int KC, bool STORE_AP>
 __global__ void __launch_bounds__(kBandThreads, 1) cg_band2_kernel(const __grid_constant__ BandBatch B) {

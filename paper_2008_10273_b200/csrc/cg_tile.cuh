@@ -16,10 +16,6 @@
 #pragma once
 
 constexpr int kTileRows = 32;
-#ifndef HIVC_XFUSE
-#define HIVC_XFUSE 0
-#endif
-constexpr bool kXFuse = HIVC_XFUSE;  // resident-x update inside the r update (one smem pass fewer)
 constexpr int kTileThreads = 512;
 
 struct TileBatch {
@@ -210,10 +206,6 @@ __global__ void __launch_bounds__(kTileThreads, 1) cg_tile_kernel(const __grid_c
                     double& rr = r[row];
                     rr = rr - alpha * api;
                     e1[0] += rr * rr;
-                    if (kXFuse && row < xr) {  // resident x += alpha p with p already in a register
-                        double& xs = sx[row * tcols + c];
-                        xs = xs + alpha * cur;
-                    }
                     up = cur;
                     cur = dn;
                 }
@@ -234,13 +226,12 @@ __global__ void __launch_bounds__(kTileThreads, 1) cg_tile_kernel(const __grid_c
             grid_reduce_arrive<1>(e1, sh, P, red, tile);
             // x += alpha p while the other CTAs arrive (x is not read until the level ends)
             if (act) {
-                if (!kXFuse)
 #pragma unroll
-                    for (int row = 0; row < ROWS; ++row) {
-                        if (row >= xr || row >= rows) break;
-                        double& xs = sx[row * tcols + c];
-                        xs = xs + alpha * sp[(row + 1) * W2 + c + 1];
-                    }
+                for (int row = 0; row < ROWS; ++row) {
+                    if (row >= xr || row >= rows) break;
+                    double& xs = sx[row * tcols + c];
+                    xs = xs + alpha * sp[(row + 1) * W2 + c + 1];
+                }
                 // streamed rows, 8 at a time with the loads issued first
 #pragma unroll
                 for (int g = 0; g < ROWS; g += 8) {

@@ -104,10 +104,7 @@ __device__ __forceinline__ double clampd(double v, double lo, double hi) {
 // the 4 groups of 8 lanes (lanes 8g..8g+7 for tile g).  2 warps per CTA.
 constexpr int kFrameWarps = 2;
 constexpr int kWarpTiles = 4;
-#ifndef HIVC_FRAME_MIN_BLOCKS
-#define HIVC_FRAME_MIN_BLOCKS 12  // 2-warp CTAs: <= 80 registers
-#endif
-constexpr int kFrameMinBlocks = HIVC_FRAME_MIN_BLOCKS;
+constexpr int kFrameMinBlocks = 12;  // 2-warp CTAs: <= 80 registers (measured best of 1/8/12/16)
 
 template <bool kInter, int C, typename RT>
 __global__ void __launch_bounds__(32 * kFrameWarps, kFrameMinBlocks) frame_kernel(FrameArgs A) {
@@ -129,17 +126,16 @@ __global__ void __launch_bounds__(32 * kFrameWarps, kFrameMinBlocks) frame_kerne
         // the host rasterised each flow tree to tiles: most tiles lie inside one
         // leaf (one (u, v) for the tile); tiles on a leaf boundary walk the tree
         const int tt = ty * nbx + (tile_ok ? tx : 0);
-        const int lu = A.flow.tiles[0] ? __ldg(A.flow.tiles[0] + tt) : 0xFFFF;
-        const int lv = A.flow.tiles[1] ? __ldg(A.flow.tiles[1] + tt) : 0xFFFF;
+        const int lu = __ldg(A.flow.tiles[0] + tt), lv = __ldg(A.flow.tiles[1] + tt);
         const double* __restrict__ vals0 = A.flow.vals[0];
         const double* __restrict__ vals1 = A.flow.vals[1];
         const double wm1 = (double)(w - 1), hm1 = (double)(h - 1);
         const double xd = u32_to_d((unsigned)x), yd0 = u32_to_d((unsigned)y_base);
         // tile map: < 0x8000 leaf (value) index; else walk per pixel from node (t - 0x8000), 0xFFFF: root
-        const bool mu = lu >= 0x8000 && !A.exp_uniform, mv = lv >= 0x8000 && !A.exp_uniform;
+        const bool mu = lu >= 0x8000, mv = lv >= 0x8000;
         const int su = lu == 0xFFFF ? 0 : lu - 0x8000, sv = lv == 0xFFFF ? 0 : lv - 0x8000;
-        const double u_tile = mu ? 0.0 : __ldg(vals0 + (lu & 0x7FFF) % max(1, A.flow.nleaves[0]));
-        const double v_tile = mv ? 0.0 : __ldg(vals1 + (lv & 0x7FFF) % max(1, A.flow.nleaves[1]));
+        const double u_tile = mu ? 0.0 : __ldg(vals0 + lu);
+        const double v_tile = mv ? 0.0 : __ldg(vals1 + lv);
 #pragma unroll
         for (int r = 0; r < 8; ++r)
 #pragma unroll
@@ -297,13 +293,7 @@ __global__ void __launch_bounds__(32 * kFrameWarps, kFrameMinBlocks) frame_kerne
     }
 }
 
-void launch_frame(const FrameArgs& a_in, bool inter, cudaStream_t s) {
-    FrameArgs a = a_in;
-    static const int exp_mode = getenv("HIVC_P_EXPERIMENT") ? atoi(getenv("HIVC_P_EXPERIMENT")) : 0;
-    if (exp_mode & 1) a.res.ngroups = 0;  // timing experiments only: drop the residual
-    if (exp_mode & 2)                     // timing experiments only: force the tree walk everywhere
-        for (int c = 0; c < 2; ++c) a.flow.tiles[c] = nullptr;
-    a.exp_uniform = (exp_mode & 4) != 0;  // timing experiments only: treat every tile as one leaf
+void launch_frame(const FrameArgs& a, bool inter, cudaStream_t s) {
     const int tiles_per_cta = kFrameWarps * kWarpTiles;
     dim3 grid((((a.w + 7) / 8) + tiles_per_cta - 1) / tiles_per_cta, (a.h + 7) / 8);
     const int nt = 32 * kFrameWarps;

@@ -44,7 +44,6 @@ struct FrameArgs {
     ResDev res;
     void* recon[3] = {nullptr, nullptr, nullptr};      // out: reconstruction (uint8 gray / int16 colour)
     uint8_t* rgb[3] = {nullptr, nullptr, nullptr};     // out: RGB planes (colour only)
-    int exp_uniform = 0;                               // timing experiments only (HIVC_P_EXPERIMENT)
 };
 
 // kInter: warp prediction from prev + flow trees; else prediction = u.
