@@ -270,30 +270,44 @@ def main():
     # warm-up (allocates lanes, pinned staging, JIT of nothing — all AOT)
     for _ in range(max(3, args.warmup)):
         step(dev_out, None)
-    N.check(N.lib.hivc_ctx_set_stage_timing(ctx.handle, 1))
-    stats = (C.c_double * 10)()
-    N.check(N.lib.hivc_ctx_decode_stats(ctx.handle, stats, 1))
+    # timed steps: no per-frame instrumentation (events) inside the timed region
+    N.check(N.lib.hivc_ctx_set_stage_timing(ctx.handle, 0))
     launches0 = ctx.launches
     times, spans = [], []
-    timings = {}
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
             flush.fill_(1)  # L2 flush between timed steps (256 MiB > 126 MB L2), outside the timed region
             if world > 1:
                 dist.barrier()
             torch.cuda.synchronize()
-            dt, span = step(dev_out, timings)
+            dt, span = step(dev_out, None)
             times.append(dt)
             spans.append(span)
     launches = ctx.launches - launches0
-    N.check(N.lib.hivc_ctx_decode_stats(ctx.handle, stats, 1))
     clocks = clk.summary()
+
+    # instrumented steps (not timed): per-stage times, the CG level launches'
+    # in-kernel spans and iteration counts for the roofline, P-kernel times
+    N.check(N.lib.hivc_ctx_set_stage_timing(ctx.handle, 1))
+    stats = (C.c_double * 10)()
+    N.check(N.lib.hivc_ctx_decode_stats(ctx.handle, stats, 1))
+    timings = {}
+    n_instr = max(1, min(3, args.steps))
+    instr_times = []
+    for _ in range(n_instr):
+        flush.fill_(1)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        dt, _ = step(dev_out, timings)
+        instr_times.append(dt)
+    N.check(N.lib.hivc_ctx_decode_stats(ctx.handle, stats, 1))
+    N.check(N.lib.hivc_ctx_set_stage_timing(ctx.handle, 0))
 
     # e2e: the public API with HOST (pinned) output buffers; H2D of the staged
     # frame descriptions and D2H of every decoded frame inside the timed region
     b0, d0 = C.c_int64(), C.c_int64()
     N.check(N.lib.hivc_ctx_bytes(ctx.handle, C.byref(b0), C.byref(d0)))
-    N.check(N.lib.hivc_ctx_set_stage_timing(ctx.handle, 0))
     e2e_times = []
     for _ in range(args.steps):
         flush.fill_(1)
@@ -371,7 +385,8 @@ def main():
             },
             "gpu_launches": int(launches),
             "device_span_ms": 1e3 * statistics.median(spans),
-            "stages_ms_per_step": {k: round(1e3 * v / args.steps, 3) for k, v in timings.items()},
+            "stages_ms_per_step": {k: round(1e3 * v / n_instr, 3) for k, v in timings.items()},
+            "stages_note": f"from {n_instr} separate instrumented (CUDA-event) steps, not the timed ones",
             "roofline": {
                 "kernel": ("cg_level_kernel<grid> (streaming CG level, float64)" if os.environ.get("HIVC_CG_BAND") == "0"
                            else "cg_tile_kernel (on-chip CG level over 30x480 tiles, float64: r in registers, p + ~all of x in smem)"),
@@ -385,7 +400,7 @@ def main():
                 "traffic": traffic,
                 "launches": int(glaunch),
                 "avg_launch_us": 1e6 * gsec / glaunch if glaunch else None,
-                "share_of_step": gsec / sum(times) if times else None,
+                "share_of_step": gsec / sum(instr_times) if instr_times else None,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)" if "hbm_gbs" in peaks else "fallback",
             },
             "p_kernel": {

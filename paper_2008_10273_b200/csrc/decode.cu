@@ -620,7 +620,11 @@ void intra_phase(CallState& cs, Item& it) {
         done_items.push_back(self);
         if (it.code == HIVC_OK && it.solve0) g.ready.push_back(self);
         --g.pending;
-        if ((int)g.ready.size() >= kMinBatch || g.pending == 0) batch.swap(g.ready);
+        static const int min_batch = [] {
+            const char* e = std::getenv("HIVC_MIN_BATCH");
+            return e ? std::max(1, std::atoi(e)) : kMinBatch;
+        }();
+        if ((int)g.ready.size() >= min_batch || g.pending == 0) batch.swap(g.ready);
     }
     if (!batch.empty()) {
         for (int i : batch) cs.items[i].h_issue = now_s() - cs.t0;
