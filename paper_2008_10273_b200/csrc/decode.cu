@@ -162,6 +162,8 @@ void Slot::init(int dev) {
     device = dev;
     CUDA_CHECK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     CUDA_CHECK(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking));
+    CUDA_CHECK(cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking));
+    for (auto& e : up_ev) CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto& e : frame_ev) CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     CUDA_CHECK(cudaEventCreateWithFlags(&out_free, cudaEventDisableTiming));
     CUDA_CHECK(cudaEventCreateWithFlags(&intra_ready, cudaEventDisableTiming));
@@ -260,6 +262,10 @@ Slot::~Slot() {
         if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : {out_free, intra_ready, intra_done})
         if (e) cudaEventDestroy(e);
+    if (up) cudaStreamSynchronize(up);
+    for (auto& e : up_ev)
+        if (e) cudaEventDestroy(e);
+    if (up) cudaStreamDestroy(up);
     if (copy) cudaStreamDestroy(copy);
     if (stream) cudaStreamDestroy(stream);
 }
@@ -418,7 +424,11 @@ const uint8_t* stage_chunk(Slot& L, Item& it, size_t fi, int cnt, FrameOffsets* 
     pk.measure = false;
     for (int k = 0; k < cnt; ++k) pack_frame(pk, it.slot->jobs[fi + k], offs[k]);
     if (table) pk.put(*table);
-    CUDA_CHECK(cudaMemcpyAsync(dev, host, pk.off, cudaMemcpyHostToDevice, L.stream));
+    // upload on the slot's own copy stream; the compute stream waits for it
+    CUDA_CHECK(cudaMemcpyAsync(dev, host, pk.off, cudaMemcpyHostToDevice, L.up));
+    cudaEvent_t ue = L.up_ev[L.up_next++ % Slot::kUpEv];
+    CUDA_CHECK(cudaEventRecord(ue, L.up));
+    CUDA_CHECK(cudaStreamWaitEvent(L.stream, ue, 0));
     it.h2d += (int64_t)pk.off;
     return dev;
 }
@@ -582,6 +592,7 @@ void intra_phase(CallState& cs, Item& it) {
         CUDA_CHECK(cudaSetDevice(L.device));
         CUDA_CHECK(cudaStreamWaitEvent(L.stream, cs.origin, 0));
         CUDA_CHECK(cudaStreamWaitEvent(L.copy, cs.origin, 0));
+        CUDA_CHECK(cudaStreamWaitEvent(L.up, cs.origin, 0));
         it.gop_dev = cs.out_on_device ? S.out + S.frame_base[it.gop] * frame_bytes : L.gop_out;
         it.gop_host = cs.out_on_device ? nullptr : S.out + S.frame_base[it.gop] * frame_bytes;
         if (!cs.out_on_device) CUDA_CHECK(cudaStreamWaitEvent(L.stream, L.out_free, 0));  // last call's copies
@@ -846,6 +857,7 @@ void decode_streams(Context& ctx, int nstreams, const uint8_t* const* data, cons
     for (auto& it : items) {
         cudaStreamSynchronize(it.slot->stream);
         cudaStreamSynchronize(it.slot->copy);
+        cudaStreamSynchronize(it.slot->up);
         float ms = 0;
         if (cudaEventElapsedTime(&ms, origin, it.done) == cudaSuccess) span = std::max(span, (double)ms * 1e-3);
     }
@@ -858,6 +870,13 @@ void decode_streams(Context& ctx, int nstreams, const uint8_t* const* data, cons
         gpu_intra += drain(it.ev_intra, origin, 'I', i, tl);
         gpu_inter += drain(it.ev_inter, origin, 'P', i, tl);
         gpu_ifin += drain(it.ev_ifin, origin, 'F', i, tl);
+        if (tl) {  // item completion (incl. its last D2H copy in host-output mode)
+            float d = 0;
+            cudaEventElapsedTime(&d, origin, it.done);
+            char line[96];
+            std::snprintf(line, sizeof line, "%d,D,%d,%d,0,%.1f,%.1f\n", i, it.stream, it.gop, d * 1e3, d * 1e3);
+            *tl += line;
+        }
         cudaEventDestroy(it.done);
         if (tl) {
             char line[200];

@@ -31,6 +31,10 @@ struct Slot {
     int device = 0;
     cudaStream_t stream = nullptr;
     cudaStream_t copy = nullptr;  // host output: D2H of finished frames
+    cudaStream_t up = nullptr;    // H2D of frame descriptions (never queued behind the solves)
+    static constexpr int kUpEv = 16;
+    cudaEvent_t up_ev[kUpEv] = {};
+    int up_next = 0;
     InpaintWorkspace ws;
     size_t plane_px = 0;
     int chans = 0;

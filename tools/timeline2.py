@@ -16,7 +16,7 @@ for l in sorted(by):
     ev = by[l]
     s, g = ev[0][1], ev[0][2]
     parts = []
-    for k in "HIFQ":
+    for k in "HIFQD":
         for kk, _, _, a, bb in ev:
             if kk == k:
                 parts.append(f"{k} {a / 1e3:6.2f}-{bb / 1e3:6.2f}")
