@@ -160,6 +160,8 @@ const T* at(const uint8_t* base, size_t off) {
 void Slot::init(int dev) {
     if (stream) return;
     device = dev;
+    // (a higher priority for the P-frame streams than for the solver stream
+    // measured slower: 4270 vs 4400 frames/s)
     CUDA_CHECK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     CUDA_CHECK(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking));
     CUDA_CHECK(cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking));
