@@ -365,6 +365,7 @@ __global__ void __launch_bounds__(kThreads, 1) cg_level_kernel(CgParams P) {
 #include "cg_tile.cuh"
 #include "cg_small.cuh"
 #include "cg_cluster.cuh"
+#include "cg_cluster_col.cuh"
 
 // ---------------------------------------------------------------- strict residual check
 
@@ -477,7 +478,14 @@ void InpaintWorkspace::reserve(int h, int w, int dev) {
             cluster_ok = cudaOccupancyMaxActiveClusters(&nclusters, cg_cluster_kernel, &cfg) == cudaSuccess &&
                          nclusters > 0;
         }
+        if (cluster_ok)
+            cluster_ok = cudaFuncSetAttribute(cg_cluster_col_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed,
+                                              1) == cudaSuccess &&
+                         cudaFuncSetAttribute(cg_cluster_col_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              200 * 1024) == cudaSuccess;
         cudaGetLastError();  // clear a rejected attribute
+        const char* env_col = getenv("HIVC_CG_CLUSTER_COL");
+        cluster_col = !(env_col && env_col[0] == '0');
     }
 }
 
@@ -702,6 +710,10 @@ int solve_batch_async(const SolveJob* jobs, int K, int h, int w, double tol, int
                 CUDA_CHECK(cudaMemsetAsync(ws0.trace, 0, kTraceLen * sizeof(unsigned long long), sp));
                 CB.S[0].trace = ws0.trace;
             }
+            // column-walk variant when every band is <= kColRows x kClThreads
+            bool col = ws0.cluster_col;
+            for (int i = 0; i < nlev && col; ++i)
+                col = CB.S[0].w[i] <= kClThreads && (CB.S[0].h[i] + kClusterSize - 1) / kClusterSize <= kColRows;
             cudaLaunchConfig_t cfg = {};
             cfg.gridDim = dim3(kClusterSize * K);
             cfg.blockDim = dim3(kClThreads);
@@ -715,7 +727,10 @@ int solve_batch_async(const SolveJob* jobs, int K, int h, int w, double tol, int
             cfg.attrs = attr;
             cfg.numAttrs = 1;
             mb("cluster nlev=" + std::to_string(nlev), sp);
-            CUDA_CHECK(cudaLaunchKernelEx(&cfg, cg_cluster_kernel, CB));
+            if (col)
+                CUDA_CHECK(cudaLaunchKernelEx(&cfg, cg_cluster_col_kernel, CB));
+            else
+                CUDA_CHECK(cudaLaunchKernelEx(&cfg, cg_cluster_kernel, CB));
             me(sp);
             ++*launches;
             l_start = l;

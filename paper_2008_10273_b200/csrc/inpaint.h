@@ -35,6 +35,7 @@ struct InpaintWorkspace {
     int band_variant = 2;       // HIVC_CG_BAND=1: row-mapped band kernel; default: column-streaming
     bool small_enabled = true;  // HIVC_CG_SMALL=0: one single-CTA launch per coarse level instead
     bool cluster_ok = false;    // 16-CTA cluster kernel for coarse/mid levels (HIVC_CG_CLUSTER=0 disables)
+    bool cluster_col = true;    // its column-walk variant when the bands fit (HIVC_CG_CLUSTER_COL=0 disables)
     // throughput mode (decode lanes): band levels use the fewest CTAs whose
     // bands still fit on chip, so solves of several lanes run side by side
     // (HIVC_CG_PACK=0 disables); latency mode spreads a level over every SM
