@@ -637,7 +637,9 @@ void intra_phase(CallState& cs, Item& it) {
             const char* e = std::getenv("HIVC_MIN_BATCH");
             return e ? std::max(1, std::atoi(e)) : kMinBatch;
         }();
-        if ((int)g.ready.size() >= min_batch || g.pending == 0) batch.swap(g.ready);
+        // (never leave a lone straggler behind a batch: its cluster levels could
+        // not start until the batch's full-GPU levels are done)
+        if (g.pending == 0 || ((int)g.ready.size() >= min_batch && g.pending >= 2)) batch.swap(g.ready);
     }
     if (!batch.empty()) {
         for (int i : batch) cs.items[i].h_issue = now_s() - cs.t0;

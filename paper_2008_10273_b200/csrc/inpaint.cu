@@ -790,7 +790,8 @@ int solve_batch_async(const SolveJob* jobs, int K, int h, int w, double tol, int
                           ww <= kBandCols * kBandThreads && band_smem <= 220 * 1024 && nbands <= ws0.num_sms;
         // 2-D tiles (default for band levels): packed solves share the SMs,
         // at most 4 side by side (a lone solve gets the whole GPU)
-        const int side = std::min(K, 4);
+        const int waves = (K + 3) / 4;
+        const int side = (K + waves - 1) / waves;  // even waves: 5 solves -> 3 + 2, not 4 + 1
         const bool pack_t = ws0.pack_bands && !ws0.pack_env_off && kc <= 2 && side > 1;
         const TilePlan TP = plan_tiles(hh, ww, pack_t ? ws0.num_sms / side : ws0.num_sms);
         const bool tile = band && ws0.tile_enabled && TP.ok && TP.ex <= ws0.ex_cap;
