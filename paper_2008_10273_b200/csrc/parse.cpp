@@ -626,9 +626,15 @@ size_t parse_intra(const uint8_t* d, size_t len, size_t pos, int32_t h, int32_t 
     // largest planes, whose I-frame parse is on the critical path, fan out)
     static const int kTreeThreads = [] {
         const char* e = getenv("HIVC_TREE_THREADS");
-        return e ? std::max(1, atoi(e)) : 4;
+        return e ? std::max(1, atoi(e)) : 3;
     }();
-    const int tree_threads = npx >= (1u << 20) ? std::min(kTreeThreads, kHw) : 1;
+    static const int kTreeThreadsSmall = [] {
+        const char* e = getenv("HIVC_TREE_THREADS_SMALL");
+        return e ? std::max(1, atoi(e)) : 1;
+    }();
+    const int tree_threads = npx >= (1u << 20) ? std::min(kTreeThreads, kHw)
+                             : npx >= (1u << 18) ? std::min(kTreeThreadsSmall, kHw)
+                                                 : 1;
     std::vector<int32_t>* idx = job.idx;
     std::exception_ptr verr[3], terr[2];
     auto decode_vals = [&]() {
