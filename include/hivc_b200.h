@@ -193,6 +193,12 @@ int hivc_brox(hivc_ctx* ctx, const double* frame_t, const double* frame_prev, in
               const hivc_brox_params* params, const double* taps_presmooth, int32_t ntaps_presmooth,
               const double* taps_antialias, int32_t ntaps_antialias, double* u, double* v);
 
+/* Replaces flow.flow_horn_schunck (flow.py:281-316): the quadratic-penalty
+ * baseline flow, `iterations` Jacobi sweeps in float64 replayed operation for
+ * operation (device pointers, planes h x w >= 2 x 2). */
+int hivc_horn_schunck(hivc_ctx* ctx, const double* frame_t, const double* frame_prev, int32_t h, int32_t w,
+                      double alpha, int32_t iterations, double* u, double* v);
+
 /* ------------------------------------------------------------------ stream decode
  * Replaces codec.decode (codec.py:484-563) for the GOP range [gop_begin, gop_end):
  * frames are written as uint8 planes, layout [frame][channel][h][w] (gray: the
@@ -221,6 +227,37 @@ int hivc_ctx_bytes(hivc_ctx* ctx, int64_t* h2d, int64_t* d2h);
 int hivc_ctx_decode_stats(hivc_ctx* ctx, double* out, int32_t reset);
 /* Per-frame CUDA-event stage breakdown on (default) or off (pure throughput runs). */
 int hivc_ctx_set_stage_timing(hivc_ctx* ctx, int32_t enable);
+
+/* ------------------------------------------------------------------ encoder primitives (host, bit-exact)
+ * Output buffers: `cap` bytes at `out`; *size receives the payload size.  A
+ * payload larger than `cap` is not written (call again with *size bytes). */
+/* Replaces entropy.encode_symbols (entropy.py:255-273); table_log < 0 = automatic
+ * (entropy.py:243-252), else 5..12. */
+int hivc_encode_symbols(const int64_t* symbols, size_t n, int32_t table_log, uint8_t* out, size_t cap,
+                        size_t* size);
+/* Replaces entropy.encode_signed_values (entropy.py:294-308). */
+int hivc_encode_signed_values(const int64_t* values, size_t n, int32_t table_log, uint8_t* out, size_t cap,
+                              size_t* size);
+/* Replaces subdivision.subdivide_by_error + serialize_tree + SubdivisionTree.leaves
+ * (subdivision.py:76-130, 178-181, 53-69) over C-contiguous float64 planes of
+ * width x height: error = region_ssd (nplanes == 1) or joint_ssd_error (nplanes > 1,
+ * subdivision.py:133-144) in numpy's float64 summation order; min_error applies when
+ * use_min_error != 0.  Tree bits MSB-first into `bits` (ceil(2*target-1 / 8) bytes
+ * suffice), *nbits; preorder leaves (x, y, w, h) into `rects` (4*target int32), *nleaves. */
+int hivc_subdivide(const double* const* planes, int32_t nplanes, int32_t width, int32_t height, int64_t target,
+                   int32_t use_min_error, double min_error, uint8_t* bits, uint64_t* nbits, int32_t* rects,
+                   size_t* nleaves);
+/* Replaces subdivision.leaf_means (subdivision.py:155-159): numpy-order mean of
+ * a float64 plane over each (x, y, w, h) rectangle. */
+int hivc_region_means(const double* plane, int32_t width, int32_t height, const int32_t* rects, size_t n,
+                      double* out);
+/* Replaces codec._plan_group (codec.py:118-137) for one channel group of 1 or 2
+ * int64 residual planes (h x w): per raster 8x8 tile t, coded[t] (0: zero in every
+ * plane), mask word masks[t] (bit y*8+x), tree bits at tree_bits[16*t] (MSB first)
+ * and tree_nbits[t].  threads <= 0: all hardware threads. */
+int hivc_plan_residual_tiles(const int64_t* const* planes, int32_t nplanes, int32_t h, int32_t w, int32_t points,
+                             int32_t threads, uint8_t* coded, uint64_t* masks, uint8_t* tree_bits,
+                             uint8_t* tree_nbits);
 
 #ifdef __cplusplus
 }

@@ -18,9 +18,9 @@ OBJ = PKG / "build"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # -fmad=false: no FMA contraction, so float64 expressions round exactly like numpy's
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC,-O3", "-I", str(PKG.parent / "include")]
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC,-O3,-ffp-contract=off", "-I", str(PKG.parent / "include")]
 FLAGS += os.environ.get("HIVC_NVCC_EXTRA", "").split()  # experiments (e.g. -DHIVC_FRAME_MIN_BLOCKS=12)
-SOURCES = ["parse.cpp", "inpaint.cu", "recon.cu", "brox.cu", "blockgemm.cu", "decode.cu", "abi.cu"]
+SOURCES = ["parse.cpp", "encode.cpp", "inpaint.cu", "recon.cu", "brox.cu", "blockgemm.cu", "decode.cu", "abi.cu"]
 
 
 def _compile(src: str) -> Path:

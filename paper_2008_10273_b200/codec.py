@@ -191,3 +191,7 @@ def _decode_residual(data, pos, shape, channels, levels, timings=None):
                 view[coded // nbx, coded % nbx] = rec[ci]
             planes.append(pad[:h, :w])
     return planes, pos
+
+
+# the encoder lives in encoder.py; codec.encode & co. keep the reference's import path (codec.py:74-105, 426-471, 604-642)
+from paper_2008_10273_b200.encoder import EncoderConfig, encode, encode_target_ratio  # noqa: E402,F401

@@ -385,6 +385,21 @@ int hivc_brox(hivc_ctx* ctx, const double* frame_t, const double* frame_prev, in
     });
 }
 
+int hivc_horn_schunck(hivc_ctx* ctx, const double* frame_t, const double* frame_prev, int32_t h, int32_t w,
+                      double alpha, int32_t iterations, double* u, double* v) {
+    return guarded([&] {
+        if (!ctx) hivc::fail(HIVC_E_ARGUMENT, "null argument");
+        if (h < 2 || w < 2) hivc::fail(HIVC_E_FLOW, "flow needs planes of at least 2x2");
+        if (iterations < 0) hivc::fail(HIVC_E_ARGUMENT, "iterations must be >= 0");
+        hivc::Context& C = ctx->c;
+        CUDA_CHECK(cudaSetDevice(C.device));
+        int64_t launches = 0;
+        hivc::horn_schunck_flow(C.brox, C.stream, frame_t, frame_prev, h, w, alpha, iterations, u, v, &launches);
+        C.launches += launches;
+        CUDA_CHECK(cudaStreamSynchronize(C.stream));
+    });
+}
+
 int hivc_decode(hivc_ctx* ctx, const uint8_t* data, size_t len, int32_t gop_begin, int32_t gop_end, uint8_t* out,
                 int32_t out_on_device, double* stage_seconds) {
     return guarded([&] {

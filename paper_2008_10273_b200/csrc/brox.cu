@@ -418,4 +418,82 @@ void brox_flow(BroxWorkspace& ws, cudaStream_t s, const double* frame_t, const d
     CUDA_CHECK(cudaGetLastError());
 }
 
+// ---------------------------------------------------------------- Horn-Schunck (flow.py:281-316)
+
+namespace {
+
+// fx = 0.5 (dx(im1) + dx(im2)), fy likewise, ft = im2 - im1, denom = alpha^2 + fx^2 + fy^2
+__global__ void hs_deriv_kernel(const double* __restrict__ im1, const double* __restrict__ im2, double* __restrict__ fx,
+                                double* __restrict__ fy, double* __restrict__ ft, double* __restrict__ den, int h,
+                                int w, double alpha) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (size_t)h * w) return;
+    const int y = (int)(i / w), x = (int)(i % w);
+    // _dx: interior 0.5 (a[x+1] - a[x-1]); x = 0: a[1] - a[0]; x = w-1: a[w-1] - a[w-2]
+    const bool ix = x > 0 && x < w - 1;
+    const size_t xl = ix ? i - 1 : (x == 0 ? i : i - 1), xr = ix ? i + 1 : (x == 0 ? i + 1 : i);
+    const bool iy = y > 0 && y < h - 1;
+    const size_t yu = iy ? i - w : (y == 0 ? i : i - w), yd = iy ? i + w : (y == 0 ? i + w : i);
+    auto dx = [&](const double* a) { return ix ? 0.5 * (a[xr] - a[xl]) : a[xr] - a[xl]; };
+    auto dy = [&](const double* a) { return iy ? 0.5 * (a[yd] - a[yu]) : a[yd] - a[yu]; };
+    const double gx = 0.5 * (dx(im1) + dx(im2)), gy = 0.5 * (dy(im1) + dy(im2));
+    fx[i] = gx;
+    fy[i] = gy;
+    ft[i] = im2[i] - im1[i];
+    den[i] = alpha * alpha + gx * gx + gy * gy;
+}
+
+// one Jacobi sweep: 8-neighbour average (edge padding, taps in the reference's
+// (dy, dx) order), then u = ua - fx c, v = va - fy c, c = (fx ua + fy va + ft) / denom
+__global__ void hs_iter_kernel(const double* __restrict__ u, const double* __restrict__ v,
+                               const double* __restrict__ fx, const double* __restrict__ fy,
+                               const double* __restrict__ ft, const double* __restrict__ den, double* __restrict__ u2,
+                               double* __restrict__ v2, int h, int w) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (size_t)h * w) return;
+    const int y = (int)(i / w), x = (int)(i % w);
+    const double k1 = 1.0 / 12.0, k2 = 1.0 / 6.0;
+    const int ys[3] = {max(y - 1, 0), y, min(y + 1, h - 1)};
+    const int xs[3] = {max(x - 1, 0), x, min(x + 1, w - 1)};
+    const double kk[3][3] = {{k1, k2, k1}, {k2, 0.0, k2}, {k1, k2, k1}};
+    double ua = 0.0, va = 0.0;
+#pragma unroll
+    for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+        for (int dx = 0; dx < 3; ++dx) {
+            if (dy == 1 && dx == 1) continue;
+            const size_t j = (size_t)ys[dy] * w + xs[dx];
+            ua = ua + kk[dy][dx] * u[j];
+            va = va + kk[dy][dx] * v[j];
+        }
+    const double gx = fx[i], gy = fy[i];
+    const double c = (gx * ua + gy * va + ft[i]) / den[i];
+    u2[i] = ua - gx * c;
+    v2[i] = va - gy * c;
+}
+
+}  // namespace
+
+void horn_schunck_flow(BroxWorkspace& ws, cudaStream_t s, const double* frame_t, const double* frame_prev, int h,
+                       int w, double alpha, int iterations, double* u_out, double* v_out, int64_t* launches) {
+    ws.reserve(h, w, 0);
+    const size_t N = (size_t)h * w;
+    double* fx = ws.base;
+    double *fy = fx + N, *ft = fy + N, *den = ft + N, *ua = den + N, *va = ua + N;
+    const int nb = (int)((N + 255) / 256);
+    hs_deriv_kernel<<<nb, 256, 0, s>>>(frame_t, frame_prev, fx, fy, ft, den, h, w, alpha);
+    // ping-pong so that the last sweep writes u_out / v_out
+    double *a_u = (iterations % 2 == 0) ? u_out : ua, *a_v = (iterations % 2 == 0) ? v_out : va;
+    double *b_u = (iterations % 2 == 0) ? ua : u_out, *b_v = (iterations % 2 == 0) ? va : v_out;
+    CUDA_CHECK(cudaMemsetAsync(a_u, 0, N * sizeof(double), s));
+    CUDA_CHECK(cudaMemsetAsync(a_v, 0, N * sizeof(double), s));
+    for (int it = 0; it < iterations; ++it) {
+        hs_iter_kernel<<<nb, 256, 0, s>>>(a_u, a_v, fx, fy, ft, den, b_u, b_v, h, w);
+        std::swap(a_u, b_u);
+        std::swap(a_v, b_v);
+    }
+    *launches += 1 + iterations;
+    CUDA_CHECK(cudaGetLastError());
+}
+
 }  // namespace hivc

@@ -33,4 +33,8 @@ void brox_flow(BroxWorkspace& ws, cudaStream_t s, const double* frame_t, const d
                const BroxParamsC& P, const double* taps_pre, int ntaps_pre, const double* taps_aa, int ntaps_aa,
                double* u_out, double* v_out, int64_t* launches);
 
+// flow.flow_horn_schunck (flow.py:281-316): `iterations` Jacobi sweeps, float64, on stream s.
+void horn_schunck_flow(BroxWorkspace& ws, cudaStream_t s, const double* frame_t, const double* frame_prev, int h,
+                       int w, double alpha, int iterations, double* u_out, double* v_out, int64_t* launches);
+
 }  // namespace hivc

@@ -1,0 +1,363 @@
+"""Encoder orchestration on the B200 (reference: codec.py:74-475, 576-642).
+
+``encode(frames, cfg, _flows)`` produces the reference encoder's stream byte
+for byte (tests/test_gpu_encoder.py pins it against streams made by the
+reference).  Heavy steps run natively:
+
+* Brox flow between source frames: GPU (``flow.flow_brox``, csrc/brox.cu);
+* intra mask subdivision, tANS coding, residual tile planning: C++
+  (csrc/encode.cpp), numpy's float64 summation order replayed exactly;
+* tonal optimisation of the intra mask values: GPU LSQR over CG solves
+  (``prediction.optimize_mask_values``);
+* closed loop: the decoder's own GPU kernels rebuild every frame
+  (``prediction.decode_intra``, ``flow.decompress_flow`` +
+  ``prediction.predict_inter``, ``codec._decode_residual``);
+* residual block fits and the keep-decision rebuilds: GPU
+  (``pseudodiff.solve_blocks_any_k``, ``pseudodiff.reconstruct_blocks``).
+
+GOPs are independent (``prev`` resets per GOP): ``encode`` runs them on a
+small thread pool so the host-side steps of one GOP overlap the GPU work of
+another.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import struct
+from concurrent.futures import ThreadPoolExecutor
+from dataclasses import dataclass, replace
+
+import numpy as np
+
+from paper_2008_10273_b200 import _native as N
+from paper_2008_10273_b200.bitstream import StreamHeader, write_stream
+from paper_2008_10273_b200.errors import CodecError, FrameError
+from paper_2008_10273_b200.frame import Frame, clip_plane, rct_forward, rct_inverse
+
+MAX_RESIDUAL_POINTS = 48  # codec.py:65
+_SCALE_FP = 65536.0  # codec.py:66
+
+
+@dataclass(frozen=True)
+class EncoderConfig:  # codec.py:74-105
+    gop_size: int = 16
+    intra_mask_fraction: float = 0.09
+    residual_points: int = 4
+    flow_points: int = 100
+    intra_levels: int = 256
+    flow_levels: int = 256
+    residual_levels: int = 63
+    residual_lambda: float = 1.0
+    fps_num: int = 25
+    fps_den: int = 1
+    flow_method: str = "brox"
+    self_check: bool = False
+
+    def __post_init__(self):
+        if not 0.0 < self.intra_mask_fraction <= 1.0:
+            raise ValueError("intra_mask_fraction must lie in (0, 1]")
+        if not 1 <= self.residual_points <= MAX_RESIDUAL_POINTS:
+            raise ValueError(f"residual_points must lie in [1, {MAX_RESIDUAL_POINTS}]")
+        if self.flow_points < 1:
+            raise ValueError("flow_points must be >= 1")
+        if self.flow_method not in ("brox", "horn-schunck"):
+            raise ValueError(f"unknown flow method {self.flow_method!r}")
+        if self.gop_size < 1 or self.gop_size > 255:
+            raise ValueError("gop_size must lie in [1, 255]")
+        if self.residual_lambda < 0.0:
+            raise ValueError("residual_lambda must be >= 0")
+
+
+# ----------------------------------------------------------------------------- residual coding
+
+
+def _pairwise64(x: np.ndarray) -> np.ndarray:
+    """numpy's pairwise sum of 64 contiguous doubles (8 accumulators, tree combine),
+    over the last axis: np.sum of one 8x8 block, vectorised across blocks."""
+    x = x.reshape(*x.shape[:-1], 8, 8)
+    r = x[..., 0, :].copy()
+    for i in range(1, 8):
+        r += x[..., i, :]
+    return ((r[..., 0] + r[..., 1]) + (r[..., 2] + r[..., 3])) + ((r[..., 4] + r[..., 5]) + (r[..., 6] + r[..., 7]))
+
+
+def _plan_group(gplanes, points: int):
+    """codec._plan_group (codec.py:118-137) in C++: coded tiles, their 8x8 mask words and tree bits."""
+    h, w = gplanes[0].shape
+    arrs = [np.ascontiguousarray(p, dtype=np.int64) for p in gplanes]
+    nt = ((h + 7) // 8) * ((w + 7) // 8)
+    coded = np.empty(nt, dtype=np.uint8)
+    masks = np.empty(nt, dtype=np.uint64)
+    tbits = np.empty((nt, 16), dtype=np.uint8)
+    tnb = np.empty(nt, dtype=np.uint8)
+    pp = (C.c_void_p * len(arrs))(*[a.ctypes.data for a in arrs])
+    N.check(N.lib.hivc_plan_residual_tiles(pp, len(arrs), h, w, points, 0, coded.ctypes.data, masks.ctypes.data,
+                                           tbits.ctypes.data, tnb.ctypes.data))
+    idx = np.flatnonzero(coded)
+    return idx, masks[idx], tbits[idx], tnb[idx]
+
+
+def _tile_blocks(plane, idx) -> np.ndarray:
+    """Tiles `idx` of a plane embedded top-left into zero-padded 8x8 blocks (codec.py:108-115)."""
+    h, w = plane.shape
+    nby, nbx = (h + 7) // 8, (w + 7) // 8
+    pad = np.zeros((nby * 8, nbx * 8))
+    pad[:h, :w] = plane
+    return pad.reshape(nby, 8, nbx, 8).transpose(0, 2, 1, 3).reshape(-1, 8, 8)[idx]
+
+
+def _encode_residual(planes, points: int, levels: int, lam: float = 0.0) -> bytes:
+    """Serialise integer residual planes, Y alone and U,V jointly (codec.py:156-245)."""
+    from paper_2008_10273_b200.entropy import encode_signed_values
+    from paper_2008_10273_b200.pseudodiff import reconstruct_blocks, solve_blocks_any_k
+    from paper_2008_10273_b200.quantize import (coefficient_scale, deadzone_dequantize, deadzone_quantize,
+                                                map_coefficients, unmap_coefficients)
+
+    h, w = planes[0].shape
+    ntiles = ((h + 7) // 8) * ((w + 7) // 8)
+    groups = [[planes[0]]] + ([[planes[1], planes[2]]] if len(planes) == 3 else [])
+    plans, all_c, all_a = [], [], []
+    for gplanes in groups:
+        idx, words, tbits, tnb = _plan_group(gplanes, points)
+        bitmask = ((words[:, None] >> np.arange(64, dtype=np.uint64)) & np.uint64(1)).astype(bool)  # (n, 64)
+        fb = np.stack([_tile_blocks(p, idx) for p in gplanes])  # (np, n, 8, 8)
+        per_plane = []
+        for ci in range(len(gplanes)):
+            if idx.size:
+                c_sc, a = solve_blocks_any_k(fb[ci], words)  # GPU bordered-system fits
+                c = c_sc.reshape(-1, 64).cpu().numpy()[bitmask]  # block by block, raster mask order
+                a = a.cpu().numpy()
+            else:
+                c, a = np.zeros(0), np.zeros(0)
+            per_plane.append((c, a))
+            all_c.append(c)
+            all_a.append(a)
+        plans.append((idx, words, bitmask, tbits, tnb, per_plane, fb))
+
+    c_flat, a_flat = np.concatenate(all_c), np.concatenate(all_a)
+    c_scale = coefficient_scale(c_flat) if c_flat.size else 1.0
+    a_scale = coefficient_scale(a_flat) if a_flat.size else 1.0
+    c_fp = min(int(round(c_scale * _SCALE_FP)), 0xFFFFFFFF) or 1
+    a_fp = min(int(round(a_scale * _SCALE_FP)), 0xFFFFFFFF) or 1
+    c_scale, a_scale = c_fp / _SCALE_FP, a_fp / _SCALE_FP
+    bits_per_sym = max(1, int(np.ceil(np.log2(levels))))
+
+    kept_total = 0
+    out = bytearray(struct.pack("<II", c_fp, a_fp))
+    for idx, words, bitmask, tbits, tnb, per_plane, fb in plans:
+        n, npl = idx.size, len(per_plane)
+        k = bitmask.sum(axis=1)
+        qc = [deadzone_quantize(map_coefficients(c, c_scale), levels) if c.size else np.zeros(0, np.int64)
+              for c, _ in per_plane]
+        qa = [deadzone_quantize(map_coefficients(a, a_scale), levels) if a.size else np.zeros(0, np.int64)
+              for _, a in per_plane]
+        keep = np.zeros(0, dtype=np.int64)
+        if n:
+            nz = np.zeros(n, dtype=bool)
+            mc = np.zeros((npl, n, 64))
+            for ci in range(npl):
+                q64 = np.zeros((n, 64), dtype=np.int64)
+                q64[bitmask] = qc[ci]
+                nz |= (q64 != 0).any(axis=1) | (qa[ci] != 0)
+                mc[ci][bitmask] = unmap_coefficients(deadzone_dequantize(qc[ci], levels), c_scale)
+            a_hat = np.stack([unmap_coefficients(deadzone_dequantize(q, levels), a_scale) for q in qa])
+            # keep a block only when its error drop pays for its bits (codec.py:203-221)
+            rec = np.asarray(reconstruct_blocks(mc.reshape(-1, 8, 8), a_hat.reshape(-1))).reshape(npl, n, 64)
+            r = fb.reshape(npl, n, 64)
+            gain = np.zeros(n)
+            for ci in range(npl):
+                d = r[ci] - rec[ci]
+                gain = gain + (_pairwise64(r[ci] * r[ci]) - _pairwise64(d * d))
+            cost = 8 + npl * (k + 1) * bits_per_sym
+            keep = np.flatnonzero(nz & (gain > lam * cost))
+        kept_total += keep.size
+        coded_bits = np.zeros(ntiles, dtype=np.uint8)
+        coded_bits[idx[keep]] = 1
+        out += np.packbits(coded_bits).tobytes()
+        tb = np.unpackbits(tbits[keep], axis=1)[np.arange(128)[None, :] < tnb[keep, None].astype(np.int64)]
+        out += struct.pack("<I", int(tb.size))
+        out += np.packbits(tb).tobytes()
+        # plane-major: every kept block's coefficients of plane 0, then plane 1 (codec.py:232-241)
+        c_sym, a_sym = [], []
+        for ci in range(npl):
+            if n:
+                q64 = np.zeros((n, 64), dtype=np.int64)
+                q64[bitmask] = qc[ci]
+                c_sym.append(q64[keep][bitmask[keep]])
+                a_sym.append(qa[ci][keep])
+        out += encode_signed_values(np.concatenate(c_sym) if c_sym else np.zeros(0, np.int64))
+        out += encode_signed_values(np.concatenate(a_sym) if a_sym else np.zeros(0, np.int64))
+    if kept_total == 0:
+        return b"\x00"  # nothing survived quantisation anywhere
+    return b"\x01" + bytes(out)
+
+
+# ----------------------------------------------------------------------------- frame and group coding
+
+
+def _reconstruct(pred_int, res_planes, colorspace):
+    return [clip_plane(p + r, ci, colorspace) for ci, (p, r) in enumerate(zip(pred_int, res_planes))]
+
+
+def _code_frame(planes, pred_planes, cfg: EncoderConfig, colorspace: str):
+    """Residual-code one frame against its prediction, closed loop (codec.py:355-366)."""
+    from paper_2008_10273_b200.codec import _decode_residual
+
+    pred_int = [np.rint(np.asarray(p)).astype(np.int64) for p in pred_planes]
+    residual = [np.asarray(o, dtype=np.int64) - p for o, p in zip(planes, pred_int)]
+    payload = _encode_residual(residual, cfg.residual_points, cfg.residual_levels, cfg.residual_lambda)
+    res_dec, consumed = _decode_residual(payload, 0, planes[0].shape, len(planes), cfg.residual_levels)
+    if consumed != len(payload):
+        raise CodecError("residual payload not consumed exactly")
+    return payload, _reconstruct(pred_int, res_dec, colorspace)
+
+
+def _estimate_flow(y_t, y_prev, method: str):
+    from paper_2008_10273_b200.flow import BroxParams, flow_brox, flow_horn_schunck
+
+    if method == "horn-schunck":
+        return flow_horn_schunck(y_t, y_prev)
+    return flow_brox(y_t, y_prev, BroxParams())
+
+
+def _encode_gop(frames_planes, cfg: EncoderConfig, colorspace: str, flows_raw):
+    """One group: I-frame, then P-frames against the previous reconstruction (codec.py:375-400)."""
+    from paper_2008_10273_b200.flow import compress_flow, decompress_flow
+    from paper_2008_10273_b200.prediction import decode_intra, encode_intra, predict_inter
+
+    h, w = frames_planes[0][0].shape
+    luma_budget = max(1, int(round(cfg.intra_mask_fraction * h * w)))
+    out = bytearray(struct.pack("<H", len(frames_planes)))
+    recons = []
+    for i, planes in enumerate(frames_planes):
+        if i == 0:
+            pred_payload = encode_intra(planes, luma_budget, cfg.intra_levels)
+            pred, consumed = decode_intra(pred_payload, 0, (h, w), len(planes), cfg.intra_levels)
+            ftype = 0
+        else:
+            pred_payload = compress_flow(flows_raw[i - 1], cfg.flow_points, cfg.flow_levels)
+            flow_dec, consumed = decompress_flow(pred_payload, 0, (h, w), cfg.flow_levels)
+            pred = predict_inter(recons[-1], flow_dec)
+            ftype = 1
+        if consumed != len(pred_payload):
+            raise CodecError("prediction payload not consumed exactly")
+        res_payload, recon = _code_frame(planes, pred, cfg, colorspace)
+        recons.append(recon)
+        out += struct.pack("<BI", ftype, len(pred_payload))
+        out += pred_payload
+        out += struct.pack("<I", len(res_payload))
+        out += res_payload
+    return bytes(out), recons
+
+
+def _split_gops(n: int, gop_size: int):
+    return [(s, min(s + gop_size, n)) for s in range(0, n, gop_size)]
+
+
+def _to_yuv_planes(frame: Frame):
+    if frame.colorspace == "rgb":
+        frame = rct_forward(frame)
+    return [p.astype(np.int64) for p in frame.planes]
+
+
+def _compute_gop_flows(y_planes, cfg: EncoderConfig):
+    """Flow fields between consecutive source frames, one list per group (codec.py:413-423)."""
+    return [[_estimate_flow(y_planes[i], y_planes[i - 1], cfg.flow_method) for i in range(s + 1, e)]
+            for s, e in _split_gops(len(y_planes), cfg.gop_size)]
+
+
+def _finalize_frame(recon_planes, channels: int) -> Frame:
+    if channels == 1:
+        return Frame((recon_planes[0],), colorspace="gray")
+    rgb = rct_inverse(Frame(tuple(recon_planes), colorspace="yuv"))
+    return Frame(tuple(np.clip(p, 0, 255).astype(np.int32) for p in rgb.planes), colorspace="rgb")
+
+
+def encode(frames, cfg: EncoderConfig | None = None, _flows=None, workers: int = 2) -> bytes:
+    """Compress a frame sequence into a self-contained byte stream (codec.py:426-471)."""
+    from paper_2008_10273_b200.codec import decode
+
+    cfg = cfg or EncoderConfig()
+    if not frames:
+        raise FrameError("nothing to encode")
+    first = frames[0]
+    if any(f.width != first.width or f.height != first.height or f.channels != first.channels for f in frames):
+        raise FrameError("all frames must share geometry and channel count")
+    if first.colorspace not in ("rgb", "gray"):
+        raise FrameError(f"unsupported input colorspace {first.colorspace!r}")
+    colorspace = "yuv" if first.channels == 3 else "gray"
+    yuv = [_to_yuv_planes(f) for f in frames]
+    if _flows is None:
+        _flows = _compute_gop_flows([p[0].astype(np.float64) for p in yuv], cfg)
+    header = StreamHeader(first.width, first.height, len(frames), cfg.fps_num, cfg.fps_den, cfg.gop_size,
+                          first.channels, cfg.intra_levels, cfg.flow_levels, cfg.residual_levels)
+    spans = _split_gops(len(frames), cfg.gop_size)
+
+    def one(gi):
+        s, e = spans[gi]
+        return _encode_gop(yuv[s:e], cfg, colorspace, _flows[gi])
+
+    if workers > 1 and len(spans) > 1:
+        with ThreadPoolExecutor(max_workers=min(workers, len(spans))) as ex:
+            results = list(ex.map(one, range(len(spans))))
+    else:
+        results = [one(gi) for gi in range(len(spans))]
+    stream = write_stream(header, [r[0] for r in results])
+    if cfg.self_check:
+        recons = [rc for r in results for rc in r[1]]
+        for i, frame in enumerate(decode(stream)):
+            if frame != _finalize_frame(recons[i], first.channels):
+                raise CodecError(f"self-check failed at frame {i}")
+    return stream
+
+
+# ----------------------------------------------------------------------------- rate control
+
+
+def _scaled_config(cfg: EncoderConfig, m: float, pixels: int) -> EncoderConfig:
+    """Budgets scaled by the multiplier m (codec.py:576-601)."""
+    frac = min(1.0, max(cfg.intra_mask_fraction * m**0.15, 1.0 / pixels))
+    pts = min(MAX_RESIDUAL_POINTS, max(1, int(round(cfg.residual_points * m))))
+    fpts = max(1, int(round(cfg.flow_points * m**1.5)))
+    lam = cfg.residual_lambda / m**6
+    lv, ilv = cfg.residual_levels, cfg.intra_levels
+    if m < 1.0:
+        lv = max(3, int(round(cfg.residual_levels * m)) | 1)
+        ilv = max(16, int(round(cfg.intra_levels * m**0.5)))
+    return replace(cfg, intra_mask_fraction=frac, residual_points=pts, flow_points=fpts, intra_levels=ilv,
+                   residual_levels=lv, residual_lambda=lam)
+
+
+def encode_target_ratio(frames, cfg: EncoderConfig, target_ratio: float, tol=0.03, max_iter=14):
+    """Bisect a budget multiplier until raw/stream bytes hits the target (codec.py:604-642).
+    Returns (stream, achieved ratio, config used)."""
+    if target_ratio <= 1.0:
+        raise ValueError("target ratio must exceed 1")
+    first = frames[0]
+    raw = len(frames) * first.width * first.height * first.channels
+    pixels = first.width * first.height
+    flows = _compute_gop_flows([_to_yuv_planes(f)[0].astype(np.float64) for f in frames], cfg)
+
+    def run(m):
+        stream = encode(frames, _scaled_config(cfg, m, pixels), _flows=flows)
+        return stream, raw / len(stream)
+
+    lo = hi = None
+    m = 1.0
+    stream, ratio = run(m)
+    best = (stream, ratio, m)
+    for _ in range(max_iter):
+        if abs(ratio - target_ratio) / target_ratio <= tol:
+            break
+        if ratio > target_ratio:
+            lo = m
+            m = m * 2 if hi is None else (lo * hi) ** 0.5
+        else:
+            hi = m
+            m = m / 2 if lo is None else (lo * hi) ** 0.5
+        stream, ratio = run(m)
+        if abs(ratio - target_ratio) < abs(best[1] - target_ratio):
+            best = (stream, ratio, m)
+    else:
+        stream, ratio, m = best
+    return stream, ratio, _scaled_config(cfg, m, pixels)

@@ -1,8 +1,10 @@
-"""tANS / category payload decoding through the native parser (reference: entropy.py).
+"""tANS / category payloads through the native coder (reference: entropy.py).
 
-``decode_symbols`` (entropy.py:276-291) and ``decode_signed_values``
-(entropy.py:311-338) keep their signatures and run the bit-exact C++
-parser of libhivc_b200 (csrc/parse.cpp) — host code, no GPU needed.
+``decode_symbols`` (entropy.py:276-291), ``decode_signed_values``
+(entropy.py:311-338), ``encode_symbols`` (entropy.py:255-273) and
+``encode_signed_values`` (entropy.py:294-308) keep their signatures and run
+the bit-exact C++ coder of libhivc_b200 (csrc/parse.cpp, csrc/encode.cpp) —
+host code, no GPU needed.
 """
 
 from __future__ import annotations
@@ -34,3 +36,27 @@ def decode_symbols(data: bytes, pos: int = 0):
 def decode_signed_values(data: bytes, pos: int = 0):
     """Inverse of encode_signed_values; returns (values, next position)."""
     return _call(N.lib.hivc_parse_signed_values, data, pos)
+
+
+def _encode(fn, values, table_log):
+    v = np.ascontiguousarray(np.asarray(values, dtype=np.int64).reshape(-1))
+    tl = -1 if table_log is None else int(table_log)
+    cap = 64 + 4 * v.size
+    for _ in range(2):
+        buf = C.create_string_buffer(cap)
+        size = C.c_size_t()
+        N.check(fn(v.ctypes.data if v.size else None, v.size, tl, buf, cap, C.byref(size)))
+        if size.value <= cap:
+            return buf.raw[: size.value]
+        cap = size.value
+    raise RuntimeError("encoder payload size changed between calls")
+
+
+def encode_symbols(symbols, table_log: int | None = None) -> bytes:
+    """Self-contained FSE payload of a nonnegative integer symbol stream."""
+    return _encode(N.lib.hivc_encode_symbols, symbols, table_log)
+
+
+def encode_signed_values(values, table_log: int | None = None) -> bytes:
+    """Category + extra-bits + FSE payload for signed integer streams."""
+    return _encode(N.lib.hivc_encode_signed_values, values, table_log)

@@ -117,6 +117,26 @@ def flow_brox(frame_t, frame_prev, params: BroxParams | None = None) -> FlowFiel
     return FlowField(back(u, frame_t), back(v, frame_t))
 
 
+def flow_horn_schunck(frame_t, frame_prev, alpha: float = 15.0, iterations: int = 400) -> FlowField:
+    """Quadratic-penalty flow, Jacobi sweeps on the Euler-Lagrange equations (flow.py:281-316),
+    on the GPU in float64 (csrc/brox.cu: hs_deriv_kernel, hs_iter_kernel)."""
+    t = torch()
+    f1 = to_device(frame_t, t.float64)
+    f0 = to_device(frame_prev, t.float64, f1.device)
+    if tuple(f1.shape) != tuple(f0.shape) or f1.dim() != 2:
+        raise FlowError("frame shape mismatch")
+    if not (bool(t.isfinite(f1).all()) and bool(t.isfinite(f0).all())):
+        raise FlowError("non-finite input planes")
+    h, w = f1.shape
+    u = t.empty_like(f1)
+    v = t.empty_like(f1)
+    ctx = N.context(f1.device.index)
+    t.cuda.current_stream(f1.device).synchronize()
+    N.check(N.lib.hivc_horn_schunck(ctx.handle, ptr(f1), ptr(f0), h, w, float(alpha), int(iterations), ptr(u),
+                                    ptr(v)))
+    return FlowField(back(u, frame_t), back(v, frame_t))
+
+
 def _tree_leaves(data: bytes, pos: int, nbits: int, width: int, height: int, bit_offset: int = 0, with_used=False):
     """Preorder leaf rectangles (x, y, w, h) via the native parser (subdivision.py:183-222)."""
     nbytes = (nbits + 7) // 8
@@ -165,3 +185,26 @@ def decompress_flow(data: bytes, pos: int, shape, quant_levels: int):
     u, pos = _decompress_plane(data, pos, shape, quant_levels)
     v, pos = _decompress_plane(data, pos, shape, quant_levels)
     return FlowField(u, v), pos
+
+
+def _compress_plane(plane, budget: int, levels: int) -> bytes:
+    """Tree bits + quantised leaf means of one flow component (flow.py:324-340)."""
+    from paper_2008_10273_b200.entropy import encode_symbols
+    from paper_2008_10273_b200.quantize import uniform_quantize
+    from paper_2008_10273_b200.subdivision import leaf_means, subdivide_by_error
+
+    p = np.ascontiguousarray(plane.cpu().numpy() if is_cuda_tensor(plane) else plane, dtype=np.float64)
+    tree = subdivide_by_error(p, budget, min_error=0.0)  # early stop on exactly representable regions
+    means = leaf_means(tree, p)
+    lo, hi = float(means.min()), float(means.max())
+    if hi <= lo:
+        hi = lo + 1e-6
+    idx = uniform_quantize(means, lo, hi, levels)
+    return struct.pack("<ffI", lo, hi, len(tree.bits)) + tree.packed + encode_symbols(idx, table_log=8)
+
+
+def compress_flow(flow: FlowField, points_budget: int, quant_levels: int) -> bytes:
+    """Encode u and v independently: tree bits + quantized leaf averages (flow.py:359-365)."""
+    if points_budget < 1:
+        raise FlowError("points budget must be >= 1")
+    return _compress_plane(flow.u, points_budget, quant_levels) + _compress_plane(flow.v, points_budget, quant_levels)

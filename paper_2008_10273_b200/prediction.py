@@ -260,3 +260,55 @@ def optimize_mask_values(planes, mask, stats: dict | None = None):
     if stats is not None:
         stats["solver_iterations"] = list(op.solver_iters)
     return out
+
+
+# ----------------------------------------------------------------------------- intra payload (encoder)
+
+
+def chroma_budget(luma_budget: int, plane_size: int) -> int:
+    """Chroma shares one mask with half the luma points; a full luma mask stays full (prediction.py:99-108)."""
+    if luma_budget >= plane_size:
+        return plane_size
+    return (luma_budget + 1) // 2
+
+
+def _encode_plane_values(values, levels: int) -> bytes:
+    from paper_2008_10273_b200.entropy import encode_symbols
+    from paper_2008_10273_b200.quantize import uniform_quantize
+
+    values = np.asarray(values, dtype=np.float64)  # prediction.py:122-130
+    lo = int(np.floor(values.min()))
+    hi = int(np.ceil(values.max()))
+    if hi <= lo:
+        hi = lo + 1
+    idx = uniform_quantize(values, float(lo), float(hi), levels)
+    return struct.pack("<hh", lo, hi) + encode_symbols(idx)
+
+
+def _tree_record(tree) -> bytes:
+    return struct.pack("<I", len(tree.bits)) + tree.packed  # prediction.py:142-146
+
+
+def encode_intra(planes, luma_budget: int, levels: int, stats: dict | None = None) -> bytes:
+    """Subdivision masks (native), tonal optimisation (GPU LSQR), quantised
+    values (native tANS): the intra payload of prediction.encode_intra
+    (prediction.py:162-182), byte for byte."""
+    from paper_2008_10273_b200.subdivision import joint_ssd_error, mask_from_tree, subdivide_by_error
+
+    if luma_budget < 1:
+        raise ValueError("luma mask budget must be >= 1")
+    y = np.ascontiguousarray(planes[0], dtype=np.float64)
+    tree_y = subdivide_by_error(y, min(luma_budget, y.size))
+    (vals_y,) = optimize_mask_values([y], mask_from_tree(tree_y), stats)
+    out = bytearray(_tree_record(tree_y))
+    out += _encode_plane_values(vals_y, levels)
+    if len(planes) == 3:
+        u = np.ascontiguousarray(planes[1], dtype=np.float64)
+        v = np.ascontiguousarray(planes[2], dtype=np.float64)
+        tree_c = subdivide_by_error(u, chroma_budget(min(luma_budget, y.size), u.size),
+                                    error_fn=joint_ssd_error([u, v]))
+        vals_u, vals_v = optimize_mask_values([u, v], mask_from_tree(tree_c))
+        out += _tree_record(tree_c)
+        out += _encode_plane_values(vals_u, chroma_levels(levels))
+        out += _encode_plane_values(vals_v, chroma_levels(levels))
+    return bytes(out)

@@ -31,3 +31,8 @@ def cfg0_stream():
 @pytest.fixture(scope="session")
 def cfg0_frames():
     return np.load(GOLDEN / "cfg0_frames.npz")["frames"]
+
+
+@pytest.fixture(scope="session")
+def enc_golden():
+    return dict(np.load(GOLDEN / "golden_encoder.npz"))

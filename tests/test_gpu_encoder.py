@@ -38,3 +38,86 @@ def test_tonal_adjoint_is_the_transpose():
     lhs = float(torch.dot(op.matvec(v), w))
     rhs = float(torch.dot(v, op.rmatvec(w)))
     assert abs(lhs - rhs) <= 1e-9 * max(1.0, abs(lhs))
+
+
+# ----------------------------------------------------------------------------- full encoder (§8(f) ranks 2-4)
+
+ENC = Path(__file__).resolve().parent / "golden" / "golden_encoder.npz"
+
+
+@pytest.mark.parametrize("i", range(6))
+def test_encode_residual_matches_reference(i):
+    """codec._encode_residual: native tile plans, GPU fits + keep-decision rebuilds, byte for byte."""
+    from paper_2008_10273_b200.encoder import _encode_residual
+
+    g = np.load(ENC)
+    pts, levels, lam = g[f"res{i}_cfg"]
+    got = _encode_residual(list(g[f"res{i}_planes"]), int(pts), int(levels), float(lam))
+    assert got == g[f"res{i}_payload"].tobytes()
+
+
+@pytest.mark.parametrize("i", range(3))
+def test_encode_intra_matches_reference(i):
+    """prediction.encode_intra: native subdivision + GPU tonal optimisation + native tANS."""
+    from paper_2008_10273_b200.prediction import encode_intra
+
+    g = np.load(ENC)
+    budget, levels = (int(v) for v in g[f"intra{i}_cfg"])
+    got = encode_intra(list(g[f"intra{i}_planes"]), budget, levels)
+    assert got == g[f"intra{i}_payload"].tobytes()
+
+
+def test_horn_schunck_matches_reference():
+    from paper_2008_10273_b200.flow import flow_horn_schunck
+
+    g = np.load(ENC)
+    pair = g["hs_pair"]
+    f = flow_horn_schunck(pair[1], pair[0])
+    assert np.array_equal(f.u, g["hs_u"]) and np.array_equal(f.v, g["hs_v"])
+    f2 = flow_horn_schunck(pair[1], pair[0], alpha=5.0, iterations=7)
+    assert np.array_equal(f2.u, g["hs2_u"]) and np.array_equal(f2.v, g["hs2_v"])
+
+
+def test_encode_config0_reproduces_reference_stream(cfg0_stream):
+    """codec.encode on config 0's source frames (GPU Brox flows, closed loop on the
+    GPU decoder kernels) emits the reference encoder's stream byte for byte."""
+    from paper_2008_10273_b200 import codec
+    from paper_2008_10273_b200.frame import Frame
+
+    src = np.load(Path(__file__).resolve().parent / "golden" / "cfg0_frames.npz")["source"]
+    frames = [Frame((p.astype(np.int32),), colorspace="gray") for p in src]
+    stream = codec.encode(frames, codec.EncoderConfig(gop_size=10, intra_mask_fraction=0.04))
+    assert len(stream) == len(cfg0_stream)
+    assert stream == cfg0_stream
+
+
+def test_encode_rgb_reproduces_reference_stream():
+    from paper_2008_10273_b200 import codec
+    from paper_2008_10273_b200.frame import Frame
+    from paper_2008_10273_b200.synth import synth_clip, to_codec_planes
+
+    ref = (Path(__file__).resolve().parent / "golden" / "streams" / "rgb.hivc").read_bytes()
+    clip = to_codec_planes(synth_clip(7, 96, 128, blobs=6, rects=3, v=2.0, seed=7, channels=3))
+    frames = [Frame(tuple(f[c] for c in range(3)), colorspace="rgb") for f in clip]
+    stream = codec.encode(frames, codec.EncoderConfig(gop_size=4, intra_mask_fraction=0.06, self_check=True))
+    assert stream == ref
+
+
+def test_encode_self_check_and_errors():
+    from paper_2008_10273_b200 import codec
+    from paper_2008_10273_b200.errors import FrameError
+    from paper_2008_10273_b200.frame import Frame
+    from paper_2008_10273_b200.synth import synth_clip, to_codec_planes
+
+    clip = to_codec_planes(synth_clip(5, 40, 52, blobs=3, rects=2, v=2.0, seed=5))
+    frames = [Frame((p[0],), colorspace="gray") for p in clip]
+    cfg = codec.EncoderConfig(gop_size=3, intra_mask_fraction=0.1, flow_method="horn-schunck", self_check=True)
+    stream = codec.encode(frames, cfg)
+    dec = codec.decode(stream)
+    assert len(dec) == 5 and all(d.planes[0].shape == (40, 52) for d in dec)
+    with pytest.raises(FrameError):
+        codec.encode([])
+    with pytest.raises(FrameError):
+        codec.encode(frames[:1] + [Frame((np.zeros((8, 8), np.int32),), colorspace="gray")])
+    with pytest.raises(ValueError):
+        codec.EncoderConfig(residual_points=49)
