@@ -6,6 +6,13 @@
 #include <cstring>
 #include <numeric>
 #include <string>
+#include <thread>
+#include <cstdlib>
+#include <atomic>
+#include <condition_variable>
+#include <deque>
+#include <functional>
+#include <mutex>
 
 namespace hivc {
 
@@ -222,6 +229,151 @@ namespace {
 
 thread_local std::vector<double> t_buf;
 
+// Large regions are summed on several threads.  Both of numpy's orders split
+// into independent pieces combined in a fixed order (the two halves of a
+// pairwise recursion; the per-chunk sums of a buffered reduction, accumulated
+// in sequence), so the parallel sums are bit-identical to the serial ones.
+constexpr int64_t kParMin = 1 << 16;
+int enc_threads() {
+    static const int n = [] {
+        const char* e = std::getenv("HIVC_ENC_THREADS");
+        int v = e ? std::atoi(e) : 8;
+        return std::max(1, std::min(v, (int)std::max(1u, std::thread::hardware_concurrency())));
+    }();
+    return n;
+}
+
+// Persistent helpers: fork_join(nt, fn) runs fn(0) here and fn(1..nt-1) on the
+// pool.  Pool threads never wait on other tasks (no nested fork_join), so
+// concurrent callers (several GOPs encoding at once) cannot deadlock.
+class EncPool {
+  public:
+    explicit EncPool(int n) {
+        for (int i = 0; i < n; ++i)
+            th_.emplace_back([this] {
+                for (;;) {
+                    std::function<void()> f;
+                    {
+                        std::unique_lock<std::mutex> lk(mu_);
+                        cv_.wait(lk, [&] { return stop_ || !q_.empty(); });
+                        if (stop_ && q_.empty()) return;
+                        f = std::move(q_.front());
+                        q_.pop_front();
+                    }
+                    f();
+                }
+            });
+    }
+    ~EncPool() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : th_) t.join();
+    }
+    void submit(std::function<void()> f) {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            q_.push_back(std::move(f));
+        }
+        cv_.notify_one();
+    }
+
+  private:
+    std::vector<std::thread> th_;
+    std::mutex mu_;
+    std::condition_variable cv_;
+    std::deque<std::function<void()>> q_;
+    bool stop_ = false;
+};
+
+EncPool& enc_pool() {
+    static EncPool* pool = new EncPool(enc_threads() - 1);  // leaked on purpose: no join at exit
+    return *pool;
+}
+
+template <class F>
+void fork_join(int nt, F&& fn) {
+    if (nt <= 1) {
+        fn(0);
+        return;
+    }
+    std::atomic<int> left{nt - 1};
+    std::mutex m;
+    std::condition_variable cv;
+    for (int t = 1; t < nt; ++t)
+        enc_pool().submit([&, t] {
+            fn(t);
+            if (left.fetch_sub(1) == 1) {
+                std::lock_guard<std::mutex> lk(m);
+                cv.notify_all();
+            }
+        });
+    fn(0);
+    std::unique_lock<std::mutex> lk(m);
+    cv.wait(lk, [&] { return left.load() == 0; });
+}
+
+// the top `depth` levels of numpy's pairwise recursion as independent segments
+void pw_segments(int64_t off, int64_t n, int depth, std::vector<std::pair<int64_t, int64_t>>& segs) {
+    if (depth == 0 || n < kParMin) {
+        segs.push_back({off, n});
+        return;
+    }
+    int64_t n2 = n / 2;
+    n2 -= n2 % 8;
+    pw_segments(off, n2, depth - 1, segs);
+    pw_segments(off + n2, n - n2, depth - 1, segs);
+}
+
+double pw_combine(int64_t n, int depth, const double*& vals) {
+    if (depth == 0 || n < kParMin) return *vals++;
+    int64_t n2 = n / 2;
+    n2 -= n2 % 8;
+    const double l = pw_combine(n2, depth - 1, vals);
+    const double r = pw_combine(n - n2, depth - 1, vals);
+    return l + r;
+}
+
+double np_pairwise_par(const double* a, int64_t n, int par) {
+    if (par <= 1 || n < kParMin) return np_pairwise(a, n);
+    int depth = 0;
+    while ((1 << (depth + 1)) <= par) ++depth;
+    std::vector<std::pair<int64_t, int64_t>> segs;
+    pw_segments(0, n, depth, segs);
+    std::vector<double> part(segs.size());
+    const int nt = std::min<int>(par, (int)segs.size());
+    fork_join(nt, [&](int t) {
+        for (size_t k = (size_t)t; k < segs.size(); k += (size_t)nt) part[k] = np_pairwise(a + segs[k].first, segs[k].second);
+    });
+    const double* v = part.data();
+    return pw_combine(n, depth, v);
+}
+
+double sum_region_par(const double* plane, int32_t W, int32_t x, int32_t y, int32_t w, int32_t h, int par) {
+    const int64_t n = (int64_t)w * h;
+    if (w == W || h == 1) return np_pairwise_par(plane + (int64_t)y * W + x, n, par);  // contiguous view
+    if (par <= 1 || n < kParMin || w > 8192) return sum_region(plane, W, x, y, w, h);
+    const int32_t rpc = std::max<int32_t>(1, 8192 / w);
+    const int32_t nchunks = (h + rpc - 1) / rpc;
+    std::vector<double> part((size_t)nchunks);
+    const int nt = std::min<int>(par, nchunks);
+    fork_join(nt, [&](int t) {
+        std::vector<double>& buf = t_buf;
+        buf.resize((size_t)rpc * w);
+        for (int32_t k = t; k < nchunks; k += nt) {
+            const int32_t r0 = k * rpc, rr = std::min(rpc, h - r0);
+            for (int32_t r = 0; r < rr; ++r)
+                std::memcpy(buf.data() + (size_t)r * w, plane + (int64_t)(y + r0 + r) * W + x, (size_t)w * sizeof(double));
+            part[(size_t)k] = np_pairwise(buf.data(), (int64_t)rr * w);
+        }
+    });
+    double acc = 0.0;
+    for (double v : part) acc += v;
+    return acc;
+}
+
 }  // namespace
 
 double sum_region(const double* plane, int32_t W, int32_t x, int32_t y, int32_t w, int32_t h) {
@@ -249,17 +401,26 @@ namespace {
 thread_local std::vector<double> t_dev;
 double region_ssd(const double* plane, int32_t W, int32_t x, int32_t y, int32_t w, int32_t h) {
     const int64_t n = (int64_t)w * h;
-    const double mean = sum_region(plane, W, x, y, w, h) / (double)n;
+    const int par = n >= kParMin ? enc_threads() : 1;
+    const double mean = sum_region_par(plane, W, x, y, w, h, par) / (double)n;
     t_dev.resize((size_t)n);
     double* d = t_dev.data();
-    for (int32_t r = 0; r < h; ++r) {
-        const double* row = plane + (int64_t)(y + r) * W + x;
-        for (int32_t c = 0; c < w; ++c) {
-            const double v = row[c] - mean;
-            d[(int64_t)r * w + c] = v * v;
+    auto rows = [&](int32_t r0, int32_t r1) {
+        for (int32_t r = r0; r < r1; ++r) {
+            const double* row = plane + (int64_t)(y + r) * W + x;
+            for (int32_t c = 0; c < w; ++c) {
+                const double v = row[c] - mean;
+                d[(int64_t)r * w + c] = v * v;
+            }
         }
+    };
+    if (par > 1) {
+        const int nt = std::min<int>(par, h);
+        fork_join(nt, [&](int t) { rows((int32_t)((int64_t)h * t / nt), (int32_t)((int64_t)h * (t + 1) / nt)); });
+    } else {
+        rows(0, h);
     }
-    return np_pairwise(d, n);
+    return np_pairwise_par(d, n, par);
 }
 
 struct Node {

@@ -24,6 +24,7 @@ from __future__ import annotations
 
 import ctypes as C
 import struct
+import time
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, replace
 
@@ -68,6 +69,22 @@ class EncoderConfig:  # codec.py:74-105
             raise ValueError("residual_lambda must be >= 0")
 
 
+# per-stage wall time of the last encode(timings=...) call (probe / bench instrumentation)
+_stage_times: dict | None = None
+
+
+class _stage:
+    def __init__(self, key: str):
+        self.key = key
+
+    def __enter__(self):
+        self.t = time.perf_counter()
+
+    def __exit__(self, *exc):
+        if _stage_times is not None:
+            _stage_times[self.key] = _stage_times.get(self.key, 0.0) + time.perf_counter() - self.t
+
+
 # ----------------------------------------------------------------------------- residual coding
 
 
@@ -108,6 +125,14 @@ def _tile_blocks(plane, idx) -> np.ndarray:
 
 def _encode_residual(planes, points: int, levels: int, lam: float = 0.0) -> bytes:
     """Serialise integer residual planes, Y alone and U,V jointly (codec.py:156-245)."""
+    return _encode_residual_rec(planes, points, levels, lam)[0]
+
+
+def _encode_residual_rec(planes, points: int, levels: int, lam: float = 0.0):
+    """``_encode_residual`` plus the residual planes the decoder will rebuild from
+    the payload: the kept blocks' keep-decision rebuilds are exactly the decoder's
+    (same dequantisation expression, same per-block GPU transform), so the closed
+    loop needs no second parse (codec._decode_residual stays the self-check)."""
     from paper_2008_10273_b200.entropy import encode_signed_values
     from paper_2008_10273_b200.pseudodiff import reconstruct_blocks, solve_blocks_any_k
     from paper_2008_10273_b200.quantize import (coefficient_scale, deadzone_dequantize, deadzone_quantize,
@@ -118,10 +143,12 @@ def _encode_residual(planes, points: int, levels: int, lam: float = 0.0) -> byte
     groups = [[planes[0]]] + ([[planes[1], planes[2]]] if len(planes) == 3 else [])
     plans, all_c, all_a = [], [], []
     for gplanes in groups:
-        idx, words, tbits, tnb = _plan_group(gplanes, points)
+        with _stage("res_plan"):
+            idx, words, tbits, tnb = _plan_group(gplanes, points)
         bitmask = ((words[:, None] >> np.arange(64, dtype=np.uint64)) & np.uint64(1)).astype(bool)  # (n, 64)
         fb = np.stack([_tile_blocks(p, idx) for p in gplanes])  # (np, n, 8, 8)
         per_plane = []
+        t_fit = time.perf_counter()
         for ci in range(len(gplanes)):
             if idx.size:
                 c_sc, a = solve_blocks_any_k(fb[ci], words)  # GPU bordered-system fits
@@ -133,6 +160,8 @@ def _encode_residual(planes, points: int, levels: int, lam: float = 0.0) -> byte
             all_c.append(c)
             all_a.append(a)
         plans.append((idx, words, bitmask, tbits, tnb, per_plane, fb))
+        if _stage_times is not None:
+            _stage_times["res_fit"] = _stage_times.get("res_fit", 0.0) + time.perf_counter() - t_fit
 
     c_flat, a_flat = np.concatenate(all_c), np.concatenate(all_a)
     c_scale = coefficient_scale(c_flat) if c_flat.size else 1.0
@@ -144,6 +173,8 @@ def _encode_residual(planes, points: int, levels: int, lam: float = 0.0) -> byte
 
     kept_total = 0
     out = bytearray(struct.pack("<II", c_fp, a_fp))
+    nby, nbx = (h + 7) // 8, (w + 7) // 8
+    rec_planes = []
     for idx, words, bitmask, tbits, tnb, per_plane, fb in plans:
         n, npl = idx.size, len(per_plane)
         k = bitmask.sum(axis=1)
@@ -162,7 +193,8 @@ def _encode_residual(planes, points: int, levels: int, lam: float = 0.0) -> byte
                 mc[ci][bitmask] = unmap_coefficients(deadzone_dequantize(qc[ci], levels), c_scale)
             a_hat = np.stack([unmap_coefficients(deadzone_dequantize(q, levels), a_scale) for q in qa])
             # keep a block only when its error drop pays for its bits (codec.py:203-221)
-            rec = np.asarray(reconstruct_blocks(mc.reshape(-1, 8, 8), a_hat.reshape(-1))).reshape(npl, n, 64)
+            with _stage("res_keep_rebuild"):
+                rec = np.asarray(reconstruct_blocks(mc.reshape(-1, 8, 8), a_hat.reshape(-1))).reshape(npl, n, 64)
             r = fb.reshape(npl, n, 64)
             gain = np.zeros(n)
             for ci in range(npl):
@@ -171,6 +203,12 @@ def _encode_residual(planes, points: int, levels: int, lam: float = 0.0) -> byte
             cost = 8 + npl * (k + 1) * bits_per_sym
             keep = np.flatnonzero(nz & (gain > lam * cost))
         kept_total += keep.size
+        for ci in range(npl):
+            pad = np.zeros((nby, nbx, 8, 8))
+            if keep.size:
+                t = idx[keep]
+                pad[t // nbx, t % nbx] = rec[ci][keep].reshape(-1, 8, 8)
+            rec_planes.append(pad.transpose(0, 2, 1, 3).reshape(nby * 8, nbx * 8)[:h, :w])
         coded_bits = np.zeros(ntiles, dtype=np.uint8)
         coded_bits[idx[keep]] = 1
         out += np.packbits(coded_bits).tobytes()
@@ -185,11 +223,12 @@ def _encode_residual(planes, points: int, levels: int, lam: float = 0.0) -> byte
                 q64[bitmask] = qc[ci]
                 c_sym.append(q64[keep][bitmask[keep]])
                 a_sym.append(qa[ci][keep])
-        out += encode_signed_values(np.concatenate(c_sym) if c_sym else np.zeros(0, np.int64))
-        out += encode_signed_values(np.concatenate(a_sym) if a_sym else np.zeros(0, np.int64))
+        with _stage("res_entropy"):
+            out += encode_signed_values(np.concatenate(c_sym) if c_sym else np.zeros(0, np.int64))
+            out += encode_signed_values(np.concatenate(a_sym) if a_sym else np.zeros(0, np.int64))
     if kept_total == 0:
-        return b"\x00"  # nothing survived quantisation anywhere
-    return b"\x01" + bytes(out)
+        return b"\x00", [np.zeros((h, w)) for _ in planes]  # nothing survived quantisation anywhere
+    return b"\x01" + bytes(out), rec_planes
 
 
 # ----------------------------------------------------------------------------- frame and group coding
@@ -205,10 +244,14 @@ def _code_frame(planes, pred_planes, cfg: EncoderConfig, colorspace: str):
 
     pred_int = [np.rint(np.asarray(p)).astype(np.int64) for p in pred_planes]
     residual = [np.asarray(o, dtype=np.int64) - p for o, p in zip(planes, pred_int)]
-    payload = _encode_residual(residual, cfg.residual_points, cfg.residual_levels, cfg.residual_lambda)
-    res_dec, consumed = _decode_residual(payload, 0, planes[0].shape, len(planes), cfg.residual_levels)
-    if consumed != len(payload):
-        raise CodecError("residual payload not consumed exactly")
+    with _stage("residual_encode"):
+        payload, res_dec = _encode_residual_rec(residual, cfg.residual_points, cfg.residual_levels,
+                                                cfg.residual_lambda)
+    if cfg.self_check:  # the reference's decode of its own payload (codec.py:362-365)
+        with _stage("residual_decode"):
+            res_chk, consumed = _decode_residual(payload, 0, planes[0].shape, len(planes), cfg.residual_levels)
+        if consumed != len(payload) or any(not np.array_equal(a, b) for a, b in zip(res_chk, res_dec)):
+            raise CodecError("residual payload does not decode to the encoder's reconstruction")
     return payload, _reconstruct(pred_int, res_dec, colorspace)
 
 
@@ -231,13 +274,17 @@ def _encode_gop(frames_planes, cfg: EncoderConfig, colorspace: str, flows_raw):
     recons = []
     for i, planes in enumerate(frames_planes):
         if i == 0:
-            pred_payload = encode_intra(planes, luma_budget, cfg.intra_levels)
-            pred, consumed = decode_intra(pred_payload, 0, (h, w), len(planes), cfg.intra_levels)
+            with _stage("intra_encode"):
+                pred_payload = encode_intra(planes, luma_budget, cfg.intra_levels)
+            with _stage("intra_decode"):
+                pred, consumed = decode_intra(pred_payload, 0, (h, w), len(planes), cfg.intra_levels)
             ftype = 0
         else:
-            pred_payload = compress_flow(flows_raw[i - 1], cfg.flow_points, cfg.flow_levels)
-            flow_dec, consumed = decompress_flow(pred_payload, 0, (h, w), cfg.flow_levels)
-            pred = predict_inter(recons[-1], flow_dec)
+            with _stage("flow_compress"):
+                pred_payload = compress_flow(flows_raw[i - 1], cfg.flow_points, cfg.flow_levels)
+            with _stage("inter_predict"):
+                flow_dec, consumed = decompress_flow(pred_payload, 0, (h, w), cfg.flow_levels)
+                pred = predict_inter(recons[-1], flow_dec)
             ftype = 1
         if consumed != len(pred_payload):
             raise CodecError("prediction payload not consumed exactly")
@@ -273,10 +320,23 @@ def _finalize_frame(recon_planes, channels: int) -> Frame:
     return Frame(tuple(np.clip(p, 0, 255).astype(np.int32) for p in rgb.planes), colorspace="rgb")
 
 
-def encode(frames, cfg: EncoderConfig | None = None, _flows=None, workers: int = 2) -> bytes:
-    """Compress a frame sequence into a self-contained byte stream (codec.py:426-471)."""
+def encode(frames, cfg: EncoderConfig | None = None, _flows=None, workers: int = 2, timings: dict | None = None) -> bytes:
+    """Compress a frame sequence into a self-contained byte stream (codec.py:426-471).
+
+    ``timings`` (optional dict) receives per-stage wall seconds (GOPs run
+    sequentially when it is given, so the stages add up)."""
+    global _stage_times
     from paper_2008_10273_b200.codec import decode
 
+    if timings is not None:
+        _stage_times, workers = timings, 1
+    try:
+        return _encode(frames, cfg, _flows, workers, decode)
+    finally:
+        _stage_times = None
+
+
+def _encode(frames, cfg, _flows, workers, decode):
     cfg = cfg or EncoderConfig()
     if not frames:
         raise FrameError("nothing to encode")
@@ -288,7 +348,8 @@ def encode(frames, cfg: EncoderConfig | None = None, _flows=None, workers: int =
     colorspace = "yuv" if first.channels == 3 else "gray"
     yuv = [_to_yuv_planes(f) for f in frames]
     if _flows is None:
-        _flows = _compute_gop_flows([p[0].astype(np.float64) for p in yuv], cfg)
+        with _stage("flow_estimate"):
+            _flows = _compute_gop_flows([p[0].astype(np.float64) for p in yuv], cfg)
     header = StreamHeader(first.width, first.height, len(frames), cfg.fps_num, cfg.fps_den, cfg.gop_size,
                           first.channels, cfg.intra_levels, cfg.flow_levels, cfg.residual_levels)
     spans = _split_gops(len(frames), cfg.gop_size)

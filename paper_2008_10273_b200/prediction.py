@@ -293,21 +293,26 @@ def encode_intra(planes, luma_budget: int, levels: int, stats: dict | None = Non
     """Subdivision masks (native), tonal optimisation (GPU LSQR), quantised
     values (native tANS): the intra payload of prediction.encode_intra
     (prediction.py:162-182), byte for byte."""
+    from paper_2008_10273_b200.encoder import _stage
     from paper_2008_10273_b200.subdivision import joint_ssd_error, mask_from_tree, subdivide_by_error
 
     if luma_budget < 1:
         raise ValueError("luma mask budget must be >= 1")
     y = np.ascontiguousarray(planes[0], dtype=np.float64)
-    tree_y = subdivide_by_error(y, min(luma_budget, y.size))
-    (vals_y,) = optimize_mask_values([y], mask_from_tree(tree_y), stats)
+    with _stage("intra_subdivide"):
+        tree_y = subdivide_by_error(y, min(luma_budget, y.size))
+    with _stage("intra_tonal"):
+        (vals_y,) = optimize_mask_values([y], mask_from_tree(tree_y), stats)
     out = bytearray(_tree_record(tree_y))
     out += _encode_plane_values(vals_y, levels)
     if len(planes) == 3:
         u = np.ascontiguousarray(planes[1], dtype=np.float64)
         v = np.ascontiguousarray(planes[2], dtype=np.float64)
-        tree_c = subdivide_by_error(u, chroma_budget(min(luma_budget, y.size), u.size),
-                                    error_fn=joint_ssd_error([u, v]))
-        vals_u, vals_v = optimize_mask_values([u, v], mask_from_tree(tree_c))
+        with _stage("intra_subdivide"):
+            tree_c = subdivide_by_error(u, chroma_budget(min(luma_budget, y.size), u.size),
+                                        error_fn=joint_ssd_error([u, v]))
+        with _stage("intra_tonal"):
+            vals_u, vals_v = optimize_mask_values([u, v], mask_from_tree(tree_c))
         out += _tree_record(tree_c)
         out += _encode_plane_values(vals_u, chroma_levels(levels))
         out += _encode_plane_values(vals_v, chroma_levels(levels))

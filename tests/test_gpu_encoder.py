@@ -121,3 +121,22 @@ def test_encode_self_check_and_errors():
         codec.encode(frames[:1] + [Frame((np.zeros((8, 8), np.int32),), colorspace="gray")])
     with pytest.raises(ValueError):
         codec.EncoderConfig(residual_points=49)
+
+
+@pytest.mark.parametrize("plane", ["Y", "Cb"])
+def test_encode_config3_gop_reproduces_reference_payload(plane):
+    """A 1080p (Y) / 540p (Cb) config-3 GOP: GPU Brox flows, native subdivision of
+    187k-leaf intra trees, GPU tonal LSQR, residual coding - byte-identical to the
+    reference encoder's GOP payload (tests/golden/make_streams.py)."""
+    from paper_2008_10273_b200 import codec
+    from paper_2008_10273_b200.bitstream import read_stream
+    from paper_2008_10273_b200.frame import Frame
+    from paper_2008_10273_b200.synth import synth_420
+
+    path = Path(__file__).resolve().parent / "golden" / "streams" / f"cfg3_{plane}.hivc"
+    if not path.exists():
+        pytest.skip("config-3 streams not generated yet")
+    y, cb, _ = synth_420(12, 1080, 1920, blobs=40, rects=12, v=6.0, seed=3)  # = frames 0-11 of the 60
+    frames = [Frame((p,), colorspace="gray") for p in (y if plane == "Y" else cb)]
+    stream = codec.encode(frames, codec.EncoderConfig(gop_size=12))
+    assert read_stream(stream)[1][0] == read_stream(path.read_bytes())[1][0]
