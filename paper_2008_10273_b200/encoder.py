@@ -336,7 +336,7 @@ def encode(frames, cfg: EncoderConfig | None = None, _flows=None, workers: int =
         _stage_times = None
 
 
-def _encode(frames, cfg, _flows, workers, decode):
+def _check_frames(frames, cfg):
     cfg = cfg or EncoderConfig()
     if not frames:
         raise FrameError("nothing to encode")
@@ -345,27 +345,54 @@ def _encode(frames, cfg, _flows, workers, decode):
         raise FrameError("all frames must share geometry and channel count")
     if first.colorspace not in ("rgb", "gray"):
         raise FrameError(f"unsupported input colorspace {first.colorspace!r}")
+    return cfg, first
+
+
+def stream_header(frames, cfg: EncoderConfig | None = None) -> StreamHeader:
+    """The container header ``encode`` writes for these frames (codec.py:442-453)."""
+    cfg, first = _check_frames(frames, cfg)
+    return StreamHeader(first.width, first.height, len(frames), cfg.fps_num, cfg.fps_den, cfg.gop_size,
+                        first.channels, cfg.intra_levels, cfg.flow_levels, cfg.residual_levels)
+
+
+def encode_gops(frames, cfg: EncoderConfig | None = None, gop_begin: int = 0, gop_end: int | None = None,
+                _flows=None, workers: int = 2):
+    """GOP payloads [gop_begin, gop_end) of ``encode(frames, cfg)`` and their
+    reconstructions: GOPs are independent (codec.py:459-462), so ranks (or
+    threads) encode disjoint ranges.  ``_flows``: all GOPs' flow lists, or
+    None to estimate each GOP's flows inside its job (codec.py:413-423)."""
+    cfg, first = _check_frames(frames, cfg)
     colorspace = "yuv" if first.channels == 3 else "gray"
-    yuv = [_to_yuv_planes(f) for f in frames]
-    if _flows is None:
-        with _stage("flow_estimate"):
-            _flows = _compute_gop_flows([p[0].astype(np.float64) for p in yuv], cfg)
-    header = StreamHeader(first.width, first.height, len(frames), cfg.fps_num, cfg.fps_den, cfg.gop_size,
-                          first.channels, cfg.intra_levels, cfg.flow_levels, cfg.residual_levels)
     spans = _split_gops(len(frames), cfg.gop_size)
+    gop_end = len(spans) if gop_end is None else gop_end
 
     def one(gi):
         s, e = spans[gi]
-        return _encode_gop(yuv[s:e], cfg, colorspace, _flows[gi])
+        yuv = [_to_yuv_planes(f) for f in frames[s:e]]
+        if _flows is None:
+            with _stage("flow_estimate"):
+                y = [p[0].astype(np.float64) for p in yuv]
+                flows = [_estimate_flow(y[i], y[i - 1], cfg.flow_method) for i in range(1, len(y))]
+        else:
+            flows = _flows[gi]
+        return _encode_gop(yuv, cfg, colorspace, flows)
 
-    if workers > 1 and len(spans) > 1:
-        with ThreadPoolExecutor(max_workers=min(workers, len(spans))) as ex:
-            results = list(ex.map(one, range(len(spans))))
+    gis = range(gop_begin, gop_end)
+    if workers > 1 and len(gis) > 1:
+        with ThreadPoolExecutor(max_workers=min(workers, len(gis))) as ex:
+            results = list(ex.map(one, gis))
     else:
-        results = [one(gi) for gi in range(len(spans))]
-    stream = write_stream(header, [r[0] for r in results])
+        results = [one(gi) for gi in gis]
+    return [r[0] for r in results], [r[1] for r in results]
+
+
+def _encode(frames, cfg, _flows, workers, decode):
+    cfg, first = _check_frames(frames, cfg)
+    header = stream_header(frames, cfg)
+    payloads, recons = encode_gops(frames, cfg, 0, None, _flows, workers)
+    stream = write_stream(header, payloads)
     if cfg.self_check:
-        recons = [rc for r in results for rc in r[1]]
+        recons = [rc for r in recons for rc in r]
         for i, frame in enumerate(decode(stream)):
             if frame != _finalize_frame(recons[i], first.channels):
                 raise CodecError(f"self-check failed at frame {i}")

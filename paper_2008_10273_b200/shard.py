@@ -53,3 +53,55 @@ def gather_frames(local, world: int, rank: int, dst: int = 0):
     if rank != dst:
         return None
     return torch.cat([p[:s] for p, s in zip(parts, sizes)])
+
+
+def gather_payloads(payloads, world: int, rank: int, dst: int = 0):
+    """Gather every rank's list of byte strings on `dst`, in rank order
+    (one flat uint8 gather of [u32 count, (u32 len, bytes)...] records)."""
+    import numpy as np
+    import torch
+
+    rec = bytearray(struct.pack("<I", len(payloads)))
+    for p in payloads:
+        rec += struct.pack("<I", len(p)) + p
+    local = torch.from_numpy(np.frombuffer(bytes(rec), dtype=np.uint8).copy())
+    if world > 1:
+        import torch.distributed as dist
+
+        if dist.get_backend() == "nccl":  # NCCL moves device buffers only
+            local = local.cuda()
+    full = gather_frames(local, world, rank, dst) if world > 1 else local
+    if full is None:
+        return None
+    data = full.cpu().numpy().tobytes()
+    out, pos = [], 0
+    while pos < len(data):  # one record per rank
+        (n,) = struct.unpack_from("<I", data, pos)
+        pos += 4
+        for _ in range(n):
+            (ln,) = struct.unpack_from("<I", data, pos)
+            out.append(data[pos + 4 : pos + 4 + ln])
+            pos += 4 + ln
+    return out
+
+
+def encode_sharded(frames, cfg=None, world: int = 1, rank: int = 0, _flows=None, encode_gops=None):
+    """codec.encode across ranks: rank r encodes GOPs [r*G/P, (r+1)*G/P)
+    (flows estimated on its own GPU), the GOP payloads (kB each) are gathered
+    to rank 0, which writes the container.  Returns
+    the stream on rank 0 (identical to a single-process encode), None elsewhere.
+    ``encode_gops`` defaults to ``encoder.encode_gops`` (override for tests)."""
+    from paper_2008_10273_b200 import encoder
+
+    enc = encode_gops or encoder.encode_gops
+    cfg = cfg or encoder.EncoderConfig()
+    header = encoder.stream_header(frames, cfg)
+    n_gops = -(-len(frames) // cfg.gop_size)
+    b, e = gop_ranges(n_gops, world)[rank]
+    payloads = enc(frames, cfg, b, e, _flows)[0] if e > b else []
+    allp = gather_payloads(payloads, world, rank)
+    if allp is None:
+        return None
+    from paper_2008_10273_b200.bitstream import write_stream
+
+    return write_stream(header, allp)
