@@ -32,11 +32,16 @@ inline int nblk(size_t n) { return (int)std::min<size_t>((n + kT - 1) / kT, 148 
 
 #define GRID_LOOP(i, n) for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < (n); i += (size_t)gridDim.x * blockDim.x)
 
-__constant__ double c_taps[64];
+// Gaussian taps travel as a kernel parameter (not a __constant__ symbol):
+// several contexts may run flows concurrently on their own streams.
+struct Taps {
+    double t[64];
+};
 
 // scipy.ndimage.correlate1d, mode 'reflect' (symmetric weights path)
 __global__ void gauss_axis_kernel(const double* __restrict__ src, double* __restrict__ dst, int h, int w, int r,
-                                  int axis) {
+                                  int axis, const __grid_constant__ Taps T) {
+    const double* c_taps = T.t;
     const size_t n = (size_t)h * w;
     GRID_LOOP(i, n) {
         const int y = (int)(i / w), x = (int)(i % w);
@@ -308,10 +313,9 @@ void BroxWorkspace::release() {
     cap = cap_pyr = 0;
 }
 
-static void set_taps(double sigma, int& radius, cudaStream_t s, const double* host_taps, int ntaps) {
+static void set_taps(Taps& T, int& radius, const double* host_taps, int ntaps) {
     radius = (ntaps - 1) / 2;
-    CUDA_CHECK(cudaMemcpyToSymbolAsync(c_taps, host_taps, ntaps * sizeof(double), 0, cudaMemcpyHostToDevice, s));
-    (void)sigma;
+    for (int i = 0; i < ntaps && i < 64; ++i) T.t[i] = host_taps[i];
 }
 
 void brox_flow(BroxWorkspace& ws, cudaStream_t s, const double* frame_t, const double* frame_prev, int h, int w,
@@ -337,14 +341,15 @@ void brox_flow(BroxWorkspace& ws, cudaStream_t s, const double* frame_t, const d
     Lin Lz{plane(11), plane(12), plane(13), plane(14), plane(15), plane(16), plane(17), plane(18)};
     Sys Sz{plane(19), plane(20), plane(21), plane(22), plane(23), plane(24), plane(25), plane(26), plane(27), plane(28)};
     int r = 0;
+    Taps taps{};
     auto gauss = [&](const double* src, double* dst, int hh, int ww) {
-        gauss_axis_kernel<<<nblk((size_t)hh * ww), kT, 0, s>>>(src, tmp2, hh, ww, r, 0);
-        gauss_axis_kernel<<<nblk((size_t)hh * ww), kT, 0, s>>>(tmp2, dst, hh, ww, r, 1);
+        gauss_axis_kernel<<<nblk((size_t)hh * ww), kT, 0, s>>>(src, tmp2, hh, ww, r, 0, taps);
+        gauss_axis_kernel<<<nblk((size_t)hh * ww), kT, 0, s>>>(tmp2, dst, hh, ww, r, 1, taps);
         *launches += 2;
     };
     // presmoothing (flow.py:197-199) into pyramid level 0
     if (P.presmooth_sigma > 0) {
-        set_taps(P.presmooth_sigma, r, s, taps_pre, ntaps_pre);
+        set_taps(taps, r, taps_pre, ntaps_pre);
         gauss(frame_t, refs, h, w);
         gauss(frame_prev, tgts, h, w);
     } else {
@@ -352,7 +357,7 @@ void brox_flow(BroxWorkspace& ws, cudaStream_t s, const double* frame_t, const d
         CUDA_CHECK(cudaMemcpyAsync(tgts, frame_prev, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
     }
     // recursive pyramid (flow.py:201-208): smooth the previous level, then resample
-    set_taps(0.5 / P.pyramid_scale, r, s, taps_aa, ntaps_aa);
+    set_taps(taps, r, taps_aa, ntaps_aa);
     for (int l = 1; l < L; ++l) {
         const int ph = shapes[l - 1].first, pw = shapes[l - 1].second, hh = shapes[l].first, ww = shapes[l].second;
         for (double* pyr : {refs, tgts}) {

@@ -135,6 +135,21 @@ def main():
     hs2 = rf.flow_horn_schunck(pair[1], pair[0], alpha=5.0, iterations=7)
     g["hs2_u"], g["hs2_v"] = hs2.u, hs2.v
 
+    # whole-encoder cases: Horn-Schunck flows, and encode_target_ratio's bisection (codec.py:604-642)
+    from hivc.frame import Frame
+
+    clip5 = np.clip(np.rint(synth_clip(5, 40, 52, blobs=3, rects=2, v=2.0, seed=35)[:, 0]), 0, 255).astype(np.int32)
+    frames = [Frame((p,), colorspace="gray") for p in clip5]
+    g["enc_hs_frames"] = clip5
+    g["enc_hs_stream"] = np.frombuffer(
+        rc.encode(frames, rc.EncoderConfig(gop_size=3, intra_mask_fraction=0.1, flow_method="horn-schunck")),
+        dtype=np.uint8)
+    stream, ratio, cfg = rc.encode_target_ratio(frames, rc.EncoderConfig(gop_size=5, intra_mask_fraction=0.05), 10.0)
+    g["enc_tr_stream"] = np.frombuffer(stream, dtype=np.uint8)
+    g["enc_tr_ratio"] = np.array(ratio)
+    g["enc_tr_cfg"] = np.array([cfg.intra_mask_fraction, cfg.residual_points, cfg.flow_points, cfg.intra_levels,
+                                cfg.residual_levels, cfg.residual_lambda])
+
     np.savez_compressed(HERE / "golden_encoder.npz", **g)
     print(f"wrote {len(g)} arrays")
 

@@ -140,3 +140,46 @@ def test_encode_config3_gop_reproduces_reference_payload(plane):
     frames = [Frame((p,), colorspace="gray") for p in (y if plane == "Y" else cb)]
     stream = codec.encode(frames, codec.EncoderConfig(gop_size=12))
     assert read_stream(stream)[1][0] == read_stream(path.read_bytes())[1][0]
+
+
+def test_encode_horn_schunck_stream_matches_reference():
+    from paper_2008_10273_b200 import codec
+    from paper_2008_10273_b200.frame import Frame
+
+    g = np.load(ENC)
+    frames = [Frame((p,), colorspace="gray") for p in g["enc_hs_frames"]]
+    cfg = codec.EncoderConfig(gop_size=3, intra_mask_fraction=0.1, flow_method="horn-schunck")
+    assert codec.encode(frames, cfg) == g["enc_hs_stream"].tobytes()
+
+
+def test_encode_target_ratio_matches_reference():
+    """Rate control's bisection over budget multipliers (codec.py:604-642): same
+    chosen multiplier, same stream, same ratio."""
+    from paper_2008_10273_b200 import codec
+    from paper_2008_10273_b200.frame import Frame
+
+    g = np.load(ENC)
+    frames = [Frame((p,), colorspace="gray") for p in g["enc_hs_frames"]]
+    stream, ratio, cfg = codec.encode_target_ratio(frames, codec.EncoderConfig(gop_size=5, intra_mask_fraction=0.05),
+                                                   10.0)
+    assert stream == g["enc_tr_stream"].tobytes()
+    assert ratio == float(g["enc_tr_ratio"])
+    got = np.array([cfg.intra_mask_fraction, cfg.residual_points, cfg.flow_points, cfg.intra_levels,
+                    cfg.residual_levels, cfg.residual_lambda])
+    assert np.array_equal(got, g["enc_tr_cfg"])
+
+
+def test_concurrent_brox_flows_match_sequential():
+    """Per-thread contexts run flows concurrently (encode's GOP workers): no shared device state."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from paper_2008_10273_b200.flow import BroxParams, flow_brox
+    from paper_2008_10273_b200.synth import synth_clip
+
+    clip = synth_clip(5, 90, 120, blobs=5, rects=2, v=2.0, seed=41)[:, 0].astype(np.float64)
+    jobs = [(clip[i + 1], clip[i], BroxParams(pyramid_scale=0.5 if i % 2 else 0.8)) for i in range(4)]
+    seq = [flow_brox(*j) for j in jobs]
+    with ThreadPoolExecutor(4) as ex:
+        par = list(ex.map(lambda j: flow_brox(*j), jobs * 3))
+    for k, f in enumerate(par):
+        assert np.array_equal(f.u, seq[k % 4].u) and np.array_equal(f.v, seq[k % 4].v)
