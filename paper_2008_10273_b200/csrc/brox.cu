@@ -11,12 +11,15 @@
 // of ~1 ulp (tests/test_gpu_parity.py).
 //
 // Structure-of-arrays float64 planes; one launch per stage (the 30 Jacobi
-// sweeps are 30 launches of one small kernel) — captured per level in a
-// CUDA graph by the host driver.
+// sweeps are 30 launches of one small kernel).  The whole launch sequence
+// (~500 kernels per pyramid level) is captured once per shape / parameter set
+// into a CUDA graph and replayed (HIVC_BROX_GRAPH=0: direct launches).
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cmath>
+#include <cstdint>
+#include <cstdlib>
 #include <vector>
 
 #include "brox.h"
@@ -301,13 +304,16 @@ void BroxWorkspace::reserve(int h, int w, int levels_px) {
     size_t n = (size_t)h * w;
     if (n <= cap && (size_t)levels_px <= cap_pyr) return;
     release();
-    size_t total = (size_t)kPlanes * n + 2 * (size_t)levels_px;
+    size_t total = (size_t)kPlanes * n + 2 * (size_t)levels_px + 4 * n;  // + graph I/O planes
     CUDA_CHECK(cudaMalloc(&base, total * sizeof(double)));
     cap = n;
     cap_pyr = levels_px;
 }
 
 void BroxWorkspace::release() {
+    if (exec) cudaGraphExecDestroy(exec);
+    exec = nullptr;
+    key.clear();
     if (base) cudaFree(base);
     base = nullptr;
     cap = cap_pyr = 0;
@@ -318,18 +324,14 @@ static void set_taps(Taps& T, int& radius, const double* host_taps, int ntaps) {
     for (int i = 0; i < ntaps && i < 64; ++i) T.t[i] = host_taps[i];
 }
 
-void brox_flow(BroxWorkspace& ws, cudaStream_t s, const double* frame_t, const double* frame_prev, int h, int w,
-               const BroxParamsC& P, const double* taps_pre, int ntaps_pre, const double* taps_aa, int ntaps_aa,
-               double* u_out, double* v_out, int64_t* launches) {
-    auto shapes = brox_shapes(h, w, P.pyramid_scale, P.min_size);
+// The whole estimator as a launch sequence on stream s (captured once per
+// shape/parameter set into a CUDA graph by brox_flow).
+static void enqueue_brox(BroxWorkspace& ws, cudaStream_t s, const std::vector<std::pair<int, int>>& shapes,
+                         const std::vector<size_t>& lofs, int levels_px, const double* frame_t,
+                         const double* frame_prev, int h, int w, const BroxParamsC& P, const double* taps_pre,
+                         int ntaps_pre, const double* taps_aa, int ntaps_aa, double* u_out, double* v_out,
+                         int64_t* launches) {
     const int L = (int)shapes.size();
-    int levels_px = 0;
-    std::vector<size_t> lofs(L);
-    for (int l = 0; l < L; ++l) {
-        lofs[l] = levels_px;
-        levels_px += shapes[l].first * shapes[l].second;
-    }
-    ws.reserve(h, w, levels_px);
     const size_t N = (size_t)h * w;
     double* pl = ws.base;
     auto plane = [&](int i) { return pl + (size_t)i * N; };
@@ -421,6 +423,58 @@ void brox_flow(BroxWorkspace& ws, cudaStream_t s, const double* frame_t, const d
     CUDA_CHECK(cudaMemcpyAsync(u_out, u, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
     CUDA_CHECK(cudaMemcpyAsync(v_out, v, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
     CUDA_CHECK(cudaGetLastError());
+}
+
+void brox_flow(BroxWorkspace& ws, cudaStream_t s, const double* frame_t, const double* frame_prev, int h, int w,
+               const BroxParamsC& P, const double* taps_pre, int ntaps_pre, const double* taps_aa, int ntaps_aa,
+               double* u_out, double* v_out, int64_t* launches) {
+    auto shapes = brox_shapes(h, w, P.pyramid_scale, P.min_size);
+    const int L = (int)shapes.size();
+    int levels_px = 0;
+    std::vector<size_t> lofs(L);
+    for (int l = 0; l < L; ++l) {
+        lofs[l] = levels_px;
+        levels_px += shapes[l].first * shapes[l].second;
+    }
+    ws.reserve(h, w, levels_px);
+    static const bool use_graph = [] {
+        const char* e = std::getenv("HIVC_BROX_GRAPH");
+        return !(e && e[0] == '0');
+    }();
+    if (!use_graph) {
+        enqueue_brox(ws, s, shapes, lofs, levels_px, frame_t, frame_prev, h, w, P, taps_pre, ntaps_pre, taps_aa,
+                     ntaps_aa, u_out, v_out, launches);
+        return;
+    }
+    // ~500 launches per pyramid level (84 levels at pyramid_scale 0.95): replay a
+    // captured graph over fixed workspace planes instead of launching each kernel
+    const size_t N = (size_t)h * w;
+    double* io = ws.base + (size_t)BroxWorkspace::kPlanes * N + 2 * (size_t)levels_px;  // in_t, in_p, out_u, out_v
+    std::vector<double> key{(double)h, (double)w, P.alpha, P.gamma, P.pyramid_scale, (double)P.min_size,
+                            (double)P.warps, (double)P.fixed_point_iters, (double)P.solver_iters, P.eps,
+                            P.presmooth_sigma, (double)ntaps_pre, (double)ntaps_aa, (double)(uintptr_t)ws.base};
+    key.insert(key.end(), taps_pre, taps_pre + ntaps_pre);
+    key.insert(key.end(), taps_aa, taps_aa + ntaps_aa);
+    if (!ws.exec || ws.key != key) {
+        if (ws.exec) cudaGraphExecDestroy(ws.exec);
+        ws.exec = nullptr;
+        int64_t n = 0;
+        cudaGraph_t g;
+        CUDA_CHECK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        enqueue_brox(ws, s, shapes, lofs, levels_px, io, io + N, h, w, P, taps_pre, ntaps_pre, taps_aa, ntaps_aa,
+                     io + 2 * N, io + 3 * N, &n);
+        CUDA_CHECK(cudaStreamEndCapture(s, &g));
+        CUDA_CHECK(cudaGraphInstantiate(&ws.exec, g, 0));
+        CUDA_CHECK(cudaGraphDestroy(g));
+        ws.key = key;
+        ws.graph_launches = n;
+    }
+    CUDA_CHECK(cudaMemcpyAsync(io, frame_t, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    CUDA_CHECK(cudaMemcpyAsync(io + N, frame_prev, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    CUDA_CHECK(cudaGraphLaunch(ws.exec, s));
+    CUDA_CHECK(cudaMemcpyAsync(u_out, io + 2 * N, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    CUDA_CHECK(cudaMemcpyAsync(v_out, io + 3 * N, N * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    *launches += ws.graph_launches;
 }
 
 // ---------------------------------------------------------------- Horn-Schunck (flow.py:281-316)

@@ -19,6 +19,9 @@ struct BroxWorkspace {
     static constexpr int kPlanes = 29;  // full-resolution float64 scratch planes
     double* base = nullptr;
     size_t cap = 0, cap_pyr = 0;
+    cudaGraphExec_t exec = nullptr;  // captured launch sequence (brox_flow)
+    std::vector<double> key;         // shape, parameters, taps, workspace base of `exec`
+    int64_t graph_launches = 0;
     void reserve(int h, int w, int levels_px);
     void release();
     ~BroxWorkspace() { release(); }
