@@ -34,6 +34,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gops", type=int, default=2)
     ap.add_argument("--json", default=None)
+    ap.add_argument("--workers", type=int, default=1, help="GOPs encoded concurrently (threads, one context each)")
     a = ap.parse_args()
     import torch
 
@@ -48,10 +49,8 @@ def main():
     print(f"synth {time.perf_counter() - t0:.1f}s", flush=True)
     cfg = codec.EncoderConfig(gop_size=G)
     bp = BroxParams(pyramid_scale=0.95)
-    per_gop = []
-    for g in range(a.gops):
+    def one_gop(g):
         s, e = g * G, (g + 1) * G
-        torch.cuda.synchronize()
         t0 = time.perf_counter()
         y = planes[0][s:e].astype(np.float64)
         lflows = [flow_brox(y[i], y[i - 1], bp) for i in range(1, G)]
@@ -75,14 +74,28 @@ def main():
         rec = {"gop": g, "brox_s": round(t_flow, 3), "brox_ms_per_pair": round(1e3 * t_flow / (G - 1), 1),
                "encode_s": round(t_enc, 3), "decode_s": round(t_dec, 4),
                "bytes": [len(st) for st in streams], "psnr_db": psnr}
-        per_gop.append(rec)
         print(json.dumps(rec), flush=True)
-    steady = per_gop[1:] or per_gop
-    gop_s = float(np.mean([r["brox_s"] + r["encode_s"] for r in steady]))
-    dec_s = float(np.mean([r["decode_s"] for r in steady]))
+        return rec
+
+    one_gop(0)  # warm-up (graphs, workspaces, first-touch)
+    torch.cuda.synchronize()
+    t_all = time.perf_counter()
+    if a.workers > 1:
+        from concurrent.futures import ThreadPoolExecutor
+
+        with ThreadPoolExecutor(a.workers) as ex:
+            per_gop = list(ex.map(one_gop, range(a.gops)))
+    else:
+        per_gop = [one_gop(g) for g in range(a.gops)]
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t_all
+    gop_s = wall / a.gops  # throughput: wall time per GOP (GOPs overlap when workers > 1)
+    dec_s = float(np.mean([r["decode_s"] for r in per_gop]))
     summary = {
         "config": "config4 sample: 1080p 4:2:0, GOP 12, Brox 0.95 on luma, injected chroma flows",
         "gops_measured": a.gops,
+        "workers": a.workers,
+        "wall_s": round(wall, 3),
         "encode_gop_s": round(gop_s, 3),
         "encode_fps_per_gpu": round(G / gop_s, 2),
         "decode_gop_s": round(dec_s, 4),
