@@ -847,7 +847,9 @@ void decode_streams(Context& ctx, int nstreams, const uint8_t* const* data, cons
     static const int kMaxWorkers = [] {
         const char* e = std::getenv("HIVC_WORKERS");
         const int hw = (int)std::max(2u, std::thread::hardware_concurrency());
-        return e ? std::max(1, std::min(64, std::atoi(e))) : std::min(hw, 32);
+        // half the hardware threads: each large I-frame parse also runs tree
+        // and value helper threads (measured on 16 cores: 8 workers beat 16 by 3 %)
+        return e ? std::max(1, std::min(64, std::atoi(e))) : std::max(2, std::min(hw / 2, 32));
     }();
     const int nworkers = std::max(1, std::min(n, kMaxWorkers));
     if (nworkers == 1 || n == 0) {
