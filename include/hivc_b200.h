@@ -235,6 +235,9 @@ int hivc_ctx_set_stage_timing(hivc_ctx* ctx, int32_t enable);
  * (entropy.py:243-252), else 5..12. */
 int hivc_encode_symbols(const int64_t* symbols, size_t n, int32_t table_log, uint8_t* out, size_t cap,
                         size_t* size);
+/* Replaces entropy.normalize_counts (entropy.py:68-106): histogram of n symbols -> table
+ * counts summing to 2^table_log (every present symbol keeps >= 1), written to out[n]. */
+int hivc_normalize_counts(const int64_t* hist, size_t n, int32_t table_log, int64_t* out);
 /* Replaces entropy.encode_signed_values (entropy.py:294-308). */
 int hivc_encode_signed_values(const int64_t* values, size_t n, int32_t table_log, uint8_t* out, size_t cap,
                               size_t* size);

@@ -75,6 +75,7 @@ _proto("hivc_decode_multi", C.c_int, C.c_void_p, C.c_int32, C.POINTER(C.c_void_p
        C.POINTER(C.c_void_p), C.c_int32, c_dbl_p)
 _proto("hivc_ctx_bytes", C.c_int, C.c_void_p, c_i64_p, c_i64_p)
 _proto("hivc_encode_symbols", C.c_int, C.c_void_p, C.c_size_t, C.c_int32, C.c_void_p, C.c_size_t, c_size_p)
+_proto("hivc_normalize_counts", C.c_int, C.c_void_p, C.c_size_t, C.c_int32, C.c_void_p)
 _proto("hivc_encode_signed_values", C.c_int, C.c_void_p, C.c_size_t, C.c_int32, C.c_void_p, C.c_size_t, c_size_p)
 _proto("hivc_subdivide", C.c_int, C.POINTER(C.c_void_p), C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_int32,
        C.c_double, C.c_void_p, c_u64_p, C.c_void_p, c_size_p)

@@ -608,6 +608,14 @@ int hivc_encode_symbols(const int64_t* symbols, size_t n, int32_t table_log, uin
     });
 }
 
+int hivc_normalize_counts(const int64_t* hist, size_t n, int32_t table_log, int64_t* out) {
+    return hivc::guarded([&] {
+        std::vector<int64_t> h(hist, hist + n);
+        const std::vector<int64_t> c = hivc::normalize_counts(h, table_log);
+        std::copy(c.begin(), c.end(), out);
+    });
+}
+
 int hivc_encode_signed_values(const int64_t* values, size_t n, int32_t table_log, uint8_t* out, size_t cap,
                               size_t* size) {
     return hivc::guarded([&] {

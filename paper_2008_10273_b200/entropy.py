@@ -60,3 +60,33 @@ def encode_symbols(symbols, table_log: int | None = None) -> bytes:
 def encode_signed_values(values, table_log: int | None = None) -> bytes:
     """Category + extra-bits + FSE payload for signed integer streams."""
     return _encode(N.lib.hivc_encode_signed_values, values, table_log)
+
+
+MAX_MAGNITUDE = (1 << 15) - 1  # entropy.py:26
+
+
+def to_category(v: int):
+    """(category, extra-bits value) of a signed integer, bijective (entropy.py:40-49)."""
+    if abs(v) > MAX_MAGNITUDE:
+        raise EntropyError(f"magnitude overflow: {v}")
+    if v == 0:
+        return 0, 0
+    k = int(abs(v)).bit_length()
+    return (k, v) if v > 0 else (k, v + (1 << k) - 1)
+
+
+def from_category(category: int, extra: int) -> int:
+    """Inverse of to_category (entropy.py:52-60)."""
+    if category == 0:
+        return 0
+    if category > 16:
+        raise EntropyError(f"bad category {category}")
+    return extra if extra >= 1 << (category - 1) else extra - (1 << category) + 1
+
+
+def normalize_counts(hist, table_log: int) -> np.ndarray:
+    """Histogram -> tANS table counts summing to 2**table_log (entropy.py:68-106), native."""
+    h = np.ascontiguousarray(np.asarray(hist, dtype=np.int64).reshape(-1))
+    out = np.empty(h.size, dtype=np.int64)
+    N.check(N.lib.hivc_normalize_counts(h.ctypes.data if h.size else None, h.size, int(table_log), out.ctypes.data))
+    return out
