@@ -50,9 +50,11 @@ __global__ void gauss_axis_kernel(const double* __restrict__ src, double* __rest
         const int y = (int)(i / w), x = (int)(i % w);
         const int len = axis == 0 ? h : w;
         const int pos = axis == 0 ? y : x;
-        auto at = [&](int p) -> double {
-            if (p < 0) p = -p - 1;
-            if (p >= len) p = 2 * len - p - 1;
+        auto at = [&](int p) -> double {  // 'reflect' (d c b a | a b c d | d c b a), any number of periods
+            const int period = 2 * len;
+            p %= period;
+            if (p < 0) p += period;
+            if (p >= len) p = period - 1 - p;
             return axis == 0 ? src[(size_t)p * w + x] : src[(size_t)y * w + p];
         };
         double acc = at(pos) * c_taps[r];

@@ -128,3 +128,16 @@ def test_oracle_brox_matches_reference(golden, tag, scale):
     pair = golden["brox_pair"]
     u, v = brox.brox(pair[1], pair[0], brox.Params(pyramid_scale=scale))
     assert np.array_equal(u, golden[f"brox{tag}_u"]) and np.array_equal(v, golden[f"brox{tag}_v"])
+
+
+def test_oracle_decodes_edge_size_streams():
+    """The oracle against the reference decoder on edge frame sizes (tests/golden/make_edge_streams.py)."""
+    from pathlib import Path
+
+    from oracle import decoder
+
+    g = np.load(Path(__file__).resolve().parent / "golden" / "golden_edge.npz")
+    for name in (str(n) for n in g["names"]):
+        ref = g[f"{name}_frames"].astype(np.int32)
+        got = np.stack([np.stack(f) for f in decoder.decode_stream(g[f"{name}_stream"].tobytes())])
+        assert np.array_equal(got, ref), name

@@ -143,11 +143,40 @@ def tonal(reps, cpu):
                       "cpu_reference_seconds_survey": 112.0}), flush=True)
 
 
+def encoder_parts(reps, cpu):
+    """SURVEY §8(f) ranks 2-3 on 1080p content (config-3 luma, frames 0-1):
+    the residual encoder on the frame-difference residual, the 9 % intra
+    subdivision and the tANS encode of its 186,624 values.  Reference CPU
+    times (1 core, measured in the build container with the reference package):
+    _encode_residual 6.08 s, subdivide_by_error 7.38 s, encode_symbols 0.177 s."""
+    import torch
+
+    from paper_2008_10273_b200.encoder import _encode_residual_rec
+    from paper_2008_10273_b200.entropy import encode_symbols
+    from paper_2008_10273_b200.subdivision import subdivide_by_error
+    from paper_2008_10273_b200.synth import synth_420
+
+    y, _, _ = synth_420(2, 1080, 1920, blobs=40, rects=12, v=6.0, seed=3)
+    res = y[1].astype(np.int64) - y[0].astype(np.int64)
+    dt = timed(lambda: (_encode_residual_rec([res], 4, 63, 1.0), torch.cuda.synchronize()), reps)
+    print(json.dumps({"config": "f2", "what": "residual encoder, 1080p frame-difference residual (tile plans C++, "
+                      "GPU fits + keep rebuilds, tANS)", "seconds": dt, "cpu_reference_seconds": 6.08}), flush=True)
+    p = y[0].astype(np.float64)
+    target = int(round(0.09 * p.size))
+    dt = timed(lambda: subdivide_by_error(p, target), reps)
+    print(json.dumps({"config": "f3", "what": "intra subdivision 1080p, 9 % (186,624 leaves), numpy-order float64",
+                      "seconds": dt, "cpu_reference_seconds": 7.38}), flush=True)
+    sym = np.random.default_rng(0).integers(0, 256, 186624)
+    dt = timed(lambda: encode_symbols(sym), reps)
+    print(json.dumps({"config": "f3", "what": "tANS encode of 186,624 symbols (256-letter alphabet)",
+                      "seconds": dt, "cpu_reference_seconds": 0.177}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--cpu", action="store_true")
-    ap.add_argument("--only", default="1,2,4,f1")
+    ap.add_argument("--only", default="1,2,4,f1,f2")
     a = ap.parse_args()
     only = a.only.split(",")
     if "1" in only:
@@ -158,6 +187,8 @@ def main():
         config4_brox(max(1, a.reps // 2), a.cpu)
     if "f1" in only:
         tonal(max(1, a.reps // 2), a.cpu)
+    if "f2" in only:
+        encoder_parts(max(1, a.reps // 2), a.cpu)
 
 
 if __name__ == "__main__":
