@@ -250,3 +250,21 @@ def test_solve_homogeneous_repeatable_across_shapes():
     for _ in range(3):
         for (f, m), ref in zip(cases, first):
             assert np.array_equal(solve_homogeneous(f, m, tol=1e-4, max_iter=160, strict=False), ref)
+
+
+@pytest.mark.parametrize("shape", [(1081, 1919), (1440, 2560)])
+def test_solve_homogeneous_large_odd_shapes_vs_oracle(shape):
+    """Shapes off the benchmark grid: odd 1080p (tile kernel with ragged tiles) and
+    QHD (beyond the on-chip tile plan: the streaming level kernel)."""
+    from oracle import inpaint
+    from paper_2008_10273_b200.homogeneous import solve_homogeneous
+    from paper_2008_10273_b200.synth import random_mask, synth_clip
+
+    plane = synth_clip(1, *shape, blobs=40, rects=12, v=6.0, seed=1)[0, 0].astype(np.float64)
+    m = random_mask(plane.shape, 0.04, 1001)
+    f = np.where(m, plane, 0.0)
+    s_ref, s_gpu = {}, {}
+    ref = inpaint.solve(f, m, tol=1e-4, max_iter=160, strict=False, stats=s_ref)
+    got = solve_homogeneous(f, m, tol=1e-4, max_iter=160, strict=False, stats=s_gpu)
+    assert s_ref["level_iterations"] == s_gpu["level_iterations"]
+    assert np.abs(got - ref).max() < 1e-9
