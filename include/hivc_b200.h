@@ -165,6 +165,15 @@ int hivc_block_reconstruct(hivc_ctx* ctx, const double* mc, const double* a, con
 int hivc_block_fit(hivc_ctx* ctx, const double* f_blocks, const uint64_t* masks, int32_t n,
                    double* c_out, double* a_out);
 
+/* Replaces the per-block quantise / rebuild / keep loop of codec._encode_residual
+ * (codec.py:181-221) for one channel group of npl (1 or 2) planes: all device
+ * pointers, per plane c (n x 64 fitted M c), a (n), fb (n x 64 residual tiles);
+ * words (n) 8x8 mask words; outputs q (n x 64 int32 indices, 0 off the mask),
+ * qa (n), rec (n x 64 rebuilt blocks = the decoder's residual), keep (n). */
+int hivc_residual_keep(hivc_ctx* ctx, int32_t npl, const double* const* c, const double* const* a,
+                       const double* const* fb, const uint64_t* words, int32_t n, int32_t levels,
+                       int32_t bits_per_sym, double c_scale, double a_scale, double lam, int32_t* const* q,
+                       int32_t* const* qa, double* const* rec, uint8_t* keep);
 /* Fit + rebuild of every 8x8 tile of a float32 residual plane (config 2;
  * solve_block_coefficients_batch + reconstruct_blocks, pseudodiff.py:243-279,
  * edge tiles embedded top-left as in inpaint_plane_blockwise, 299-324).
@@ -254,6 +263,10 @@ int hivc_subdivide(const double* const* planes, int32_t nplanes, int32_t width, 
  * a float64 plane over each (x, y, w, h) rectangle. */
 int hivc_region_means(const double* plane, int32_t width, int32_t height, const int32_t* rects, size_t n,
                       double* out);
+/* codec._tile_residuals (codec.py:108-115): tiles `tiles[0..n)` of nplanes int64
+ * planes (h x w) embedded top-left into zero-padded 8x8 float64 blocks, out[p][i][64]. */
+int hivc_gather_tiles(const int64_t* const* planes, int32_t nplanes, int32_t h, int32_t w, const int64_t* tiles,
+                      size_t n, double* out);
 /* Replaces codec._plan_group (codec.py:118-137) for one channel group of 1 or 2
  * int64 residual planes (h x w): per raster 8x8 tile t, coded[t] (0: zero in every
  * plane), mask word masks[t] (bit y*8+x), tree bits at tree_bits[16*t] (MSB first)

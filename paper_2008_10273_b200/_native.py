@@ -80,6 +80,11 @@ _proto("hivc_encode_signed_values", C.c_int, C.c_void_p, C.c_size_t, C.c_int32, 
 _proto("hivc_subdivide", C.c_int, C.POINTER(C.c_void_p), C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_int32,
        C.c_double, C.c_void_p, c_u64_p, C.c_void_p, c_size_p)
 _proto("hivc_region_means", C.c_int, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_size_t, C.c_void_p)
+_proto("hivc_gather_tiles", C.c_int, C.POINTER(C.c_void_p), C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_size_t,
+       C.c_void_p)
+_proto("hivc_residual_keep", C.c_int, C.c_void_p, C.c_int32, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p),
+       C.POINTER(C.c_void_p), C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_double,
+       C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.c_void_p)
 _proto("hivc_plan_residual_tiles", C.c_int, C.POINTER(C.c_void_p), C.c_int32, C.c_int32, C.c_int32, C.c_int32,
        C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p)
 _proto("hivc_horn_schunck", C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_double,

@@ -307,6 +307,42 @@ int hivc_block_fit(hivc_ctx* ctx, const double* f_blocks, const uint64_t* masks,
     });
 }
 
+int hivc_residual_keep(hivc_ctx* ctx, int32_t npl, const double* const* c, const double* const* a,
+                       const double* const* fb, const uint64_t* words, int32_t n, int32_t levels,
+                       int32_t bits_per_sym, double c_scale, double a_scale, double lam, int32_t* const* q,
+                       int32_t* const* qa, double* const* rec, uint8_t* keep) {
+    return guarded([&] {
+        if (!ctx) hivc::fail(HIVC_E_ARGUMENT, "null context");
+        if (npl < 1 || npl > 2) hivc::fail(HIVC_E_ARGUMENT, "a residual channel group has 1 or 2 planes");
+        if (levels < 3 || levels % 2 == 0) hivc::fail(HIVC_E_QUANTIZE, "dead-zone levels must be odd and >= 3");
+        if (!(c_scale > 0) || !(a_scale > 0)) hivc::fail(HIVC_E_QUANTIZE, "global_scale must be positive");
+        hivc::Context& C = ctx->c;
+        CUDA_CHECK(cudaSetDevice(C.device));
+        hivc::KeepArgs A{};
+        for (int i = 0; i < npl; ++i) {
+            A.c[i] = c[i];
+            A.a[i] = a[i];
+            A.fb[i] = fb[i];
+            A.q[i] = q[i];
+            A.qa[i] = qa[i];
+            A.rec[i] = rec[i];
+        }
+        A.words = words;
+        A.n = n;
+        A.npl = npl;
+        A.lmax = (levels - 1) / 2;
+        A.bits_per_sym = bits_per_sym;
+        A.c_scale = c_scale;
+        A.a_scale = a_scale;
+        A.step = 127.0 / (double)((levels - 1) / 2);  // quantize.deadzone_step
+        A.lam = lam;
+        A.keep = keep;
+        hivc::launch_residual_keep(A, C.stream);
+        C.launches += n > 0;
+        CUDA_CHECK(cudaStreamSynchronize(C.stream));
+    });
+}
+
 int hivc_block_operator(hivc_ctx* ctx, const float* plane, int32_t h, int32_t w, uint64_t mask, float* out) {
     return guarded([&] {
         if (!ctx) hivc::fail(HIVC_E_ARGUMENT, "null context");

@@ -654,6 +654,24 @@ int hivc_region_means(const double* plane, int32_t width, int32_t height, const 
     });
 }
 
+int hivc_gather_tiles(const int64_t* const* planes, int32_t nplanes, int32_t h, int32_t w, const int64_t* tiles,
+                      size_t n, double* out) {
+    return hivc::guarded([&] {
+        const int32_t nbx = (w + 7) / 8, nby = (h + 7) / 8;
+        for (int p = 0; p < nplanes; ++p)
+            for (size_t i = 0; i < n; ++i) {
+                const int64_t t = tiles[i];
+                if (t < 0 || t >= (int64_t)nbx * nby) hivc::fail(HIVC_E_ARGUMENT, "tile index out of range");
+                const int32_t y0 = (int32_t)(t / nbx) * 8, x0 = (int32_t)(t % nbx) * 8;
+                const int32_t bh = std::min(8, h - y0), bw = std::min(8, w - x0);
+                double* o = out + ((size_t)p * n + i) * 64;
+                for (int k = 0; k < 64; ++k) o[k] = 0.0;
+                for (int32_t r = 0; r < bh; ++r)
+                    for (int32_t c = 0; c < bw; ++c) o[r * 8 + c] = (double)planes[p][(int64_t)(y0 + r) * w + x0 + c];
+            }
+    });
+}
+
 int hivc_plan_residual_tiles(const int64_t* const* planes, int32_t nplanes, int32_t h, int32_t w, int32_t points,
                              int32_t threads, uint8_t* coded, uint64_t* masks, uint8_t* tree_bits,
                              uint8_t* tree_nbits) {

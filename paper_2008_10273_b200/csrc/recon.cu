@@ -408,6 +408,97 @@ void launch_block_reconstruct(const double* mc, const double* a, const double* e
     CUDA_CHECK(cudaGetLastError());
 }
 
+// ---------------------------------------------------------------- residual encoder: quantise + keep decision
+// codec._encode_residual's per-block loop (codec.py:181-221) for one channel
+// group of npl planes, 8 lanes (rows) per block: map + dead-zone quantise the
+// fitted coefficients and constant (quantize.py:32-58), dequantise + unmap,
+// rebuild the block (the decoder's AAN path), and keep it when it has a
+// nonzero index and gain = sum_planes(sum(r*r) - sum((r-rec)^2)) exceeds
+// lam * (8 + npl (K+1) bits_per_sym).  Sums in numpy's order for 64 terms
+// (8 column accumulators over rows, then the pairwise tree).
+
+__device__ __forceinline__ int32_t deadzone_q(double c, double scale, double step, int lmax) {
+    double m = c / scale * 127.0;  // map_coefficients
+    m = fmin(fmax(m, -127.0), 127.0);
+    const double sg = m > 0.0 ? 1.0 : (m < 0.0 ? -1.0 : 0.0);
+    double idx = sg * floor(fabs(m) / step);  // deadzone_quantize
+    idx = fmin(fmax(idx, (double)-lmax), (double)lmax);
+    return (int32_t)idx;
+}
+
+__global__ void residual_keep_kernel(const __grid_constant__ KeepArgs A) {
+    __shared__ double t[8][64];
+    __shared__ double u[8][64];
+    __shared__ double g[8][8];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int b = blockIdx.x * 8 + wid;
+    if (b >= A.n || lane >= 8) return;
+    const unsigned m8 = 0xffu;
+    const uint64_t word = A.words[b];
+    const int j = lane;
+    bool nz = false;
+    double gain = 0.0;
+    for (int ci = 0; ci < A.npl; ++ci) {
+        // quantise this row's coefficients, dequantise + unmap into the rebuild buffer
+        for (int x = 0; x < 8; ++x) {
+            const int k = j * 8 + x;
+            double mc = 0.0;
+            int32_t qv = 0;
+            if ((word >> k) & 1ull) {
+                qv = deadzone_q(A.c[ci][(size_t)b * 64 + k], A.c_scale, A.step, A.lmax);
+                mc = (double)qv * A.step / 127.0 * A.c_scale;  // unmap(deadzone_dequantize)
+            }
+            nz |= qv != 0;
+            A.q[ci][(size_t)b * 64 + k] = qv;
+            t[wid][k] = mc;
+        }
+        const int32_t qa = deadzone_q(A.a[ci][b], A.a_scale, A.step, A.lmax);
+        nz |= qa != 0;
+        if (j == 0) A.qa[ci][b] = qa;
+        const double a_hat = (double)qa * A.step / 127.0 * A.a_scale;
+        __syncwarp(m8);
+        block_reconstruct_8lanes(&t[wid][0], j, kGreensEig, a_hat, m8);
+        // r*r and (r-rec)^2 of this row, then column sums down the rows in order
+        for (int x = 0; x < 8; ++x) {
+            const int k = j * 8 + x;
+            const double r = A.fb[ci][(size_t)b * 64 + k], rc = t[wid][k];
+            A.rec[ci][(size_t)b * 64 + k] = rc;
+            const double d = r - rc;
+            u[wid][k] = r * r;
+            t[wid][k] = d * d;
+        }
+        __syncwarp(m8);
+        double s1 = u[wid][j], s2 = t[wid][j];  // accumulator j: elements j, j+8, ..., j+56
+        for (int row = 1; row < 8; ++row) {
+            s1 += u[wid][row * 8 + j];
+            s2 += t[wid][row * 8 + j];
+        }
+        g[wid][j] = s1;
+        __syncwarp(m8);
+        const double S1 = ((g[wid][0] + g[wid][1]) + (g[wid][2] + g[wid][3])) +
+                          ((g[wid][4] + g[wid][5]) + (g[wid][6] + g[wid][7]));
+        __syncwarp(m8);
+        g[wid][j] = s2;
+        __syncwarp(m8);
+        const double S2 = ((g[wid][0] + g[wid][1]) + (g[wid][2] + g[wid][3])) +
+                          ((g[wid][4] + g[wid][5]) + (g[wid][6] + g[wid][7]));
+        __syncwarp(m8);
+        gain = gain + (S1 - S2);
+    }
+    nz = __any_sync(m8, nz);
+    if (j == 0) {
+        const int k = __popcll(word);
+        const double cost = (double)(8 + A.npl * (k + 1) * A.bits_per_sym);
+        A.keep[b] = nz && gain > A.lam * cost;
+    }
+}
+
+void launch_residual_keep(const KeepArgs& A, cudaStream_t s) {
+    if (A.n <= 0) return;
+    residual_keep_kernel<<<(A.n + 7) / 8, 256, 0, s>>>(A);
+    CUDA_CHECK(cudaGetLastError());
+}
+
 // ---------------------------------------------------------------- block coefficient fit (any mask layout)
 // One warp per block: the bordered (K+1)x(K+1) system [[G_KK,1],[1^T,0]] is
 // assembled in shared memory from the 64x64 Green's matrix and solved by

@@ -64,6 +64,21 @@ void launch_block_reconstruct(const double* mc, const double* a, const double* e
 void launch_block_fit(const double* f, const uint64_t* masks, int n, double* c_out, double* a_out, int* status,
                       cudaStream_t s);
 
+// codec._encode_residual's quantise + keep decision for one channel group (codec.py:181-221).
+struct KeepArgs {
+    const double* c[2];   // fitted M c per plane (n x 64, zero off the mask)
+    const double* a[2];   // fitted constants per plane (n)
+    const double* fb[2];  // residual tiles per plane (n x 64)
+    const uint64_t* words;
+    int n, npl, lmax, bits_per_sym;
+    double c_scale, a_scale, step, lam;
+    int32_t* q[2];   // out: quantised coefficient indices (n x 64, 0 off the mask)
+    int32_t* qa[2];  // out: quantised constants (n)
+    double* rec[2];  // out: rebuilt blocks (n x 64)
+    uint8_t* keep;   // out
+};
+void launch_residual_keep(const KeepArgs& A, cudaStream_t s);
+
 const double* device_default_eig();  // greens_eigenvalues_harmonic() in device memory
 
 }  // namespace hivc

@@ -88,16 +88,6 @@ class _stage:
 # ----------------------------------------------------------------------------- residual coding
 
 
-def _pairwise64(x: np.ndarray) -> np.ndarray:
-    """numpy's pairwise sum of 64 contiguous doubles (8 accumulators, tree combine),
-    over the last axis: np.sum of one 8x8 block, vectorised across blocks."""
-    x = x.reshape(*x.shape[:-1], 8, 8)
-    r = x[..., 0, :].copy()
-    for i in range(1, 8):
-        r += x[..., i, :]
-    return ((r[..., 0] + r[..., 1]) + (r[..., 2] + r[..., 3])) + ((r[..., 4] + r[..., 5]) + (r[..., 6] + r[..., 7]))
-
-
 def _plan_group(gplanes, points: int):
     """codec._plan_group (codec.py:118-137) in C++: coded tiles, their 8x8 mask words and tree bits."""
     h, w = gplanes[0].shape
@@ -114,13 +104,16 @@ def _plan_group(gplanes, points: int):
     return idx, masks[idx], tbits[idx], tnb[idx]
 
 
-def _tile_blocks(plane, idx) -> np.ndarray:
-    """Tiles `idx` of a plane embedded top-left into zero-padded 8x8 blocks (codec.py:108-115)."""
-    h, w = plane.shape
-    nby, nbx = (h + 7) // 8, (w + 7) // 8
-    pad = np.zeros((nby * 8, nbx * 8))
-    pad[:h, :w] = plane
-    return pad.reshape(nby, 8, nbx, 8).transpose(0, 2, 1, 3).reshape(-1, 8, 8)[idx]
+def _tile_blocks(arrs, idx) -> np.ndarray:
+    """Tiles `idx` of int64 planes embedded top-left into zero-padded 8x8 blocks,
+    (nplanes, n, 64) float64 (codec._tile_residuals, codec.py:108-115), in C++."""
+    h, w = arrs[0].shape
+    idx = np.ascontiguousarray(idx, dtype=np.int64)
+    out = np.empty((len(arrs), idx.size, 64))
+    pp = (C.c_void_p * len(arrs))(*[a.ctypes.data for a in arrs])
+    N.check(N.lib.hivc_gather_tiles(pp, len(arrs), h, w, idx.ctypes.data if idx.size else None, idx.size,
+                                    out.ctypes.data))
+    return out
 
 
 def _encode_residual(planes, points: int, levels: int, lam: float = 0.0) -> bytes:
@@ -130,85 +123,85 @@ def _encode_residual(planes, points: int, levels: int, lam: float = 0.0) -> byte
 
 def _encode_residual_rec(planes, points: int, levels: int, lam: float = 0.0):
     """``_encode_residual`` plus the residual planes the decoder will rebuild from
-    the payload: the kept blocks' keep-decision rebuilds are exactly the decoder's
-    (same dequantisation expression, same per-block GPU transform), so the closed
+    the payload.  Per channel group: tile plans and tile gather in C++; the
+    bordered-system fits, the dead-zone quantisation, the rebuilds and the
+    keep decision on the GPU (``hivc_block_fit``, ``hivc_residual_keep``); the
+    frame's coefficient scales (99.9th percentiles over every group and plane)
+    on the host.  The kept blocks' rebuilds are exactly the decoder's residual
+    (same dequantisation expression, same per-block transform), so the closed
     loop needs no second parse (codec._decode_residual stays the self-check)."""
+    from paper_2008_10273_b200._tensors import ptr, torch
     from paper_2008_10273_b200.entropy import encode_signed_values
-    from paper_2008_10273_b200.pseudodiff import reconstruct_blocks, solve_blocks_any_k
-    from paper_2008_10273_b200.quantize import (coefficient_scale, deadzone_dequantize, deadzone_quantize,
-                                                map_coefficients, unmap_coefficients)
+    from paper_2008_10273_b200.pseudodiff import solve_blocks_any_k
+    from paper_2008_10273_b200.quantize import coefficient_scale, deadzone_step
 
+    t = torch()
+    dev = t.device("cuda", t.cuda.current_device())
     h, w = planes[0].shape
-    ntiles = ((h + 7) // 8) * ((w + 7) // 8)
+    nby, nbx = (h + 7) // 8, (w + 7) // 8
+    ntiles = nby * nbx
     groups = [[planes[0]]] + ([[planes[1], planes[2]]] if len(planes) == 3 else [])
+    deadzone_step(levels)  # validates the level count (QuantizeError)
     plans, all_c, all_a = [], [], []
     for gplanes in groups:
+        arrs = [np.ascontiguousarray(p, dtype=np.int64) for p in gplanes]
         with _stage("res_plan"):
-            idx, words, tbits, tnb = _plan_group(gplanes, points)
+            idx, words, tbits, tnb = _plan_group(arrs, points)
+        n = idx.size
         bitmask = ((words[:, None] >> np.arange(64, dtype=np.uint64)) & np.uint64(1)).astype(bool)  # (n, 64)
-        fb = np.stack([_tile_blocks(p, idx) for p in gplanes])  # (np, n, 8, 8)
-        per_plane = []
-        t_fit = time.perf_counter()
-        for ci in range(len(gplanes)):
-            if idx.size:
-                c_sc, a = solve_blocks_any_k(fb[ci], words)  # GPU bordered-system fits
-                c = c_sc.reshape(-1, 64).cpu().numpy()[bitmask]  # block by block, raster mask order
-                a = a.cpu().numpy()
-            else:
-                c, a = np.zeros(0), np.zeros(0)
-            per_plane.append((c, a))
-            all_c.append(c)
-            all_a.append(a)
-        plans.append((idx, words, bitmask, tbits, tnb, per_plane, fb))
-        if _stage_times is not None:
-            _stage_times["res_fit"] = _stage_times.get("res_fit", 0.0) + time.perf_counter() - t_fit
+        fits = []
+        with _stage("res_fit"):
+            fb = t.from_numpy(_tile_blocks(arrs, idx)).to(dev) if n else None  # (npl, n, 64)
+            wd = t.from_numpy(words.view(np.int64)).to(dev) if n else None
+            for ci in range(len(arrs)):
+                if n:
+                    c_sc, a = solve_blocks_any_k(fb[ci].view(n, 8, 8), words)  # GPU bordered-system fits
+                    c_sc = c_sc.view(n, 64)
+                    fits.append((c_sc, a))
+                    all_c.append(c_sc.cpu().numpy()[bitmask])  # block by block, raster mask order
+                    all_a.append(a.cpu().numpy())
+        plans.append((idx, words, bitmask, tbits, tnb, fits, fb, wd, len(arrs)))
 
-    c_flat, a_flat = np.concatenate(all_c), np.concatenate(all_a)
+    c_flat = np.concatenate(all_c) if all_c else np.zeros(0)
+    a_flat = np.concatenate(all_a) if all_a else np.zeros(0)
     c_scale = coefficient_scale(c_flat) if c_flat.size else 1.0
     a_scale = coefficient_scale(a_flat) if a_flat.size else 1.0
     c_fp = min(int(round(c_scale * _SCALE_FP)), 0xFFFFFFFF) or 1
     a_fp = min(int(round(a_scale * _SCALE_FP)), 0xFFFFFFFF) or 1
     c_scale, a_scale = c_fp / _SCALE_FP, a_fp / _SCALE_FP
     bits_per_sym = max(1, int(np.ceil(np.log2(levels))))
+    ctx = N.context(dev.index)
 
     kept_total = 0
     out = bytearray(struct.pack("<II", c_fp, a_fp))
-    nby, nbx = (h + 7) // 8, (w + 7) // 8
     rec_planes = []
-    for idx, words, bitmask, tbits, tnb, per_plane, fb in plans:
-        n, npl = idx.size, len(per_plane)
-        k = bitmask.sum(axis=1)
-        qc = [deadzone_quantize(map_coefficients(c, c_scale), levels) if c.size else np.zeros(0, np.int64)
-              for c, _ in per_plane]
-        qa = [deadzone_quantize(map_coefficients(a, a_scale), levels) if a.size else np.zeros(0, np.int64)
-              for _, a in per_plane]
+    for idx, words, bitmask, tbits, tnb, fits, fb, wd, npl in plans:
+        n = idx.size
         keep = np.zeros(0, dtype=np.int64)
+        q = qa = rec = None
         if n:
-            nz = np.zeros(n, dtype=bool)
-            mc = np.zeros((npl, n, 64))
-            for ci in range(npl):
-                q64 = np.zeros((n, 64), dtype=np.int64)
-                q64[bitmask] = qc[ci]
-                nz |= (q64 != 0).any(axis=1) | (qa[ci] != 0)
-                mc[ci][bitmask] = unmap_coefficients(deadzone_dequantize(qc[ci], levels), c_scale)
-            a_hat = np.stack([unmap_coefficients(deadzone_dequantize(q, levels), a_scale) for q in qa])
-            # keep a block only when its error drop pays for its bits (codec.py:203-221)
+            q = t.empty((npl, n, 64), dtype=t.int32, device=dev)
+            qa = t.empty((npl, n), dtype=t.int32, device=dev)
+            rec = t.empty((npl, n, 64), dtype=t.float64, device=dev)
+            kp = t.empty(n, dtype=t.uint8, device=dev)
+            arr = lambda xs: (C.c_void_p * npl)(*[ptr(x) for x in xs])  # noqa: E731
             with _stage("res_keep_rebuild"):
-                rec = np.asarray(reconstruct_blocks(mc.reshape(-1, 8, 8), a_hat.reshape(-1))).reshape(npl, n, 64)
-            r = fb.reshape(npl, n, 64)
-            gain = np.zeros(n)
-            for ci in range(npl):
-                d = r[ci] - rec[ci]
-                gain = gain + (_pairwise64(r[ci] * r[ci]) - _pairwise64(d * d))
-            cost = 8 + npl * (k + 1) * bits_per_sym
-            keep = np.flatnonzero(nz & (gain > lam * cost))
+                t.cuda.current_stream(dev).synchronize()
+                N.check(N.lib.hivc_residual_keep(ctx.handle, npl, arr([f[0] for f in fits]), arr([f[1] for f in fits]),
+                                                 arr([fb[ci] for ci in range(npl)]), ptr(wd), n, levels, bits_per_sym,
+                                                 c_scale, a_scale, float(lam), arr([q[ci] for ci in range(npl)]),
+                                                 arr([qa[ci] for ci in range(npl)]),
+                                                 arr([rec[ci] for ci in range(npl)]), ptr(kp)))
+                keep = np.flatnonzero(kp.cpu().numpy())
         kept_total += keep.size
+        # decoded residual planes: kept blocks' rebuilds placed on the tile grid (GPU scatter)
         for ci in range(npl):
-            pad = np.zeros((nby, nbx, 8, 8))
+            full = t.zeros((ntiles, 64), dtype=t.float64, device=dev)
             if keep.size:
-                t = idx[keep]
-                pad[t // nbx, t % nbx] = rec[ci][keep].reshape(-1, 8, 8)
-            rec_planes.append(pad.transpose(0, 2, 1, 3).reshape(nby * 8, nbx * 8)[:h, :w])
+                kd = t.from_numpy(keep).to(dev)
+                full[t.from_numpy(idx[keep]).to(dev)] = rec[ci].index_select(0, kd)
+            rec_planes.append(full.view(nby, nbx, 8, 8).permute(0, 2, 1, 3).reshape(nby * 8, nbx * 8)[:h, :w]
+                              .cpu().numpy())
         coded_bits = np.zeros(ntiles, dtype=np.uint8)
         coded_bits[idx[keep]] = 1
         out += np.packbits(coded_bits).tobytes()
@@ -217,12 +210,14 @@ def _encode_residual_rec(planes, points: int, levels: int, lam: float = 0.0):
         out += np.packbits(tb).tobytes()
         # plane-major: every kept block's coefficients of plane 0, then plane 1 (codec.py:232-241)
         c_sym, a_sym = [], []
-        for ci in range(npl):
-            if n:
-                q64 = np.zeros((n, 64), dtype=np.int64)
-                q64[bitmask] = qc[ci]
-                c_sym.append(q64[keep][bitmask[keep]])
-                a_sym.append(qa[ci][keep])
+        if keep.size:
+            kd = t.from_numpy(keep).to(dev)
+            qk = q.index_select(1, kd).cpu().numpy()  # (npl, nk, 64)
+            qak = qa.index_select(1, kd).cpu().numpy()
+            mk = bitmask[keep]
+            for ci in range(npl):
+                c_sym.append(qk[ci][mk].astype(np.int64))
+                a_sym.append(qak[ci].astype(np.int64))
         with _stage("res_entropy"):
             out += encode_signed_values(np.concatenate(c_sym) if c_sym else np.zeros(0, np.int64))
             out += encode_signed_values(np.concatenate(a_sym) if a_sym else np.zeros(0, np.int64))
