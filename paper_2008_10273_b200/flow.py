@@ -207,4 +207,10 @@ def compress_flow(flow: FlowField, points_budget: int, quant_levels: int) -> byt
     """Encode u and v independently: tree bits + quantized leaf averages (flow.py:359-365)."""
     if points_budget < 1:
         raise FlowError("points budget must be >= 1")
-    return _compress_plane(flow.u, points_budget, quant_levels) + _compress_plane(flow.v, points_budget, quant_levels)
+    # the two components are independent: subdivide them on two host threads
+    from concurrent.futures import ThreadPoolExecutor
+
+    with ThreadPoolExecutor(2) as ex:
+        pu = ex.submit(_compress_plane, flow.u, points_budget, quant_levels)
+        pv = ex.submit(_compress_plane, flow.v, points_budget, quant_levels)
+        return pu.result() + pv.result()
