@@ -260,7 +260,8 @@ def _estimate_flow(y_t, y_prev, method: str):
 
 def _encode_gop(frames_planes, cfg: EncoderConfig, colorspace: str, flows_raw):
     """One group: I-frame, then P-frames against the previous reconstruction (codec.py:375-400)."""
-    from paper_2008_10273_b200.flow import compress_flow, decompress_flow
+    from paper_2008_10273_b200._tensors import torch
+    from paper_2008_10273_b200.flow import FlowField, _decompress_plane_device, compress_flow
     from paper_2008_10273_b200.prediction import decode_intra, encode_intra, predict_inter
 
     h, w = frames_planes[0][0].shape
@@ -278,8 +279,12 @@ def _encode_gop(frames_planes, cfg: EncoderConfig, colorspace: str, flows_raw):
             with _stage("flow_compress"):
                 pred_payload = compress_flow(flows_raw[i - 1], cfg.flow_points, cfg.flow_levels)
             with _stage("inter_predict"):
-                flow_dec, consumed = decompress_flow(pred_payload, 0, (h, w), cfg.flow_levels)
-                pred = predict_inter(recons[-1], flow_dec)
+                # decompress_flow + predict_inter with the dense flow painted and warped on the device
+                dev = torch().device("cuda", torch().cuda.current_device())
+                u, pos = _decompress_plane_device(pred_payload, 0, (h, w), cfg.flow_levels, dev)
+                v, consumed = _decompress_plane_device(pred_payload, pos, (h, w), cfg.flow_levels, dev)
+                prev = [torch().from_numpy(np.ascontiguousarray(p)).to(dev).double() for p in recons[-1]]
+                pred = [q.cpu().numpy() for q in predict_inter(prev, FlowField(u, v))]
             ftype = 1
         if consumed != len(pred_payload):
             raise CodecError("prediction payload not consumed exactly")

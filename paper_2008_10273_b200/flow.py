@@ -180,6 +180,32 @@ def _decompress_plane(data: bytes, pos: int, shape, levels: int):
     return out, pos
 
 
+def _decompress_plane_device(data: bytes, pos: int, shape, levels: int, device):
+    """_decompress_plane painting the leaf values on the GPU (the encoder's closed
+    loop keeps the dense flow on the device for the warp)."""
+    if pos + 12 > len(data):
+        raise TruncatedStream("flow payload truncated")
+    lo, hi, nbits = struct.unpack_from("<ffI", data, pos)
+    pos += 12
+    nbytes = (nbits + 7) // 8
+    if pos + nbytes > len(data):
+        raise TruncatedStream("flow payload truncated")
+    leaves = _tree_leaves(data, pos, nbits, shape[1], shape[0])
+    pos += nbytes
+    idx, pos = _decode_symbols(data, pos)
+    lo, hi = float(lo), float(hi)
+    if not lo < hi:
+        raise QuantizeError("need lo < hi")
+    vals = lo + idx.astype(np.float64) * ((hi - lo) / (levels - 1))
+    if len(vals) != len(leaves):
+        raise SubdivisionError("leaf value count mismatch")
+    t = torch()
+    out = t.empty(shape, dtype=t.float64, device=device)
+    for (x, y, w, h), val in zip(leaves.tolist(), vals.tolist()):
+        out[y : y + h, x : x + w] = val
+    return out, pos
+
+
 def decompress_flow(data: bytes, pos: int, shape, quant_levels: int):
     """Decode a compressed flow payload; returns (FlowField, next position) (flow.py:368-372)."""
     u, pos = _decompress_plane(data, pos, shape, quant_levels)

@@ -74,8 +74,12 @@ def decode_intra(data: bytes, pos: int, shape, channels: int, levels: int):
 
 
 def predict_inter(prev_planes, flow):
-    """Motion-compensated prediction: previous reconstruction sampled at (x+u, y+v)."""
-    return warp_planes([np.asarray(p, dtype=np.float64) for p in prev_planes], flow.u, flow.v)
+    """Motion-compensated prediction: previous reconstruction sampled at (x+u, y+v)
+    (numpy planes -> numpy, CUDA tensors -> CUDA tensors)."""
+    from paper_2008_10273_b200._tensors import is_cuda_tensor
+
+    return warp_planes([p if is_cuda_tensor(p) else np.asarray(p, dtype=np.float64) for p in prev_planes],
+                       flow.u, flow.v)
 
 
 # ----------------------------------------------------------------------------- tonal optimisation (encoder)
