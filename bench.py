@@ -8,7 +8,10 @@ A "frame" is one 4:2:0 picture (all three planes).
 Multi-GPU (one process per GPU, torchrun): weak scaling by GOP sharding.  The
 video is the config-3 GOP sequence tiled N times (5N GOPs per plane); rank r
 decodes GOPs [5r, 5r+5) of every plane — 60 frames per GPU — and the decoded
-frames are gathered to rank 0 over NCCL (the only collective).
+frames land in rank 0's GPU memory (the only exchange): each
+finished frame is copied over NVLink into rank 0's CUDA-IPC-mapped frame
+buffer by the decoder's copy streams while later frames decode
+(HIVC_GATHER=nccl: one NCCL gather after the decode instead).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
@@ -247,7 +250,22 @@ def main():
     host_out = [torch.empty(s, dtype=torch.uint8, pin_memory=True) for s in shapes]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     per_rank_bytes = sum(int(np.prod(s)) for s in shapes)
-    gather_buf = torch.empty(per_rank_bytes, dtype=torch.uint8, device="cuda")
+    # N > 1: decoded frames reach rank 0's GPU.  Default: fused into the decode
+    # (every finished frame is copied over NVLink into rank 0's CUDA-IPC-mapped
+    # frame buffer while the next frames decode); HIVC_GATHER=nccl: one NCCL
+    # gather after the decode.
+    gather_mode = os.environ.get("HIVC_GATHER", "peer") if world > 1 else "none"
+    peer = peer_addrs = None
+    if gather_mode == "peer":
+        from paper_2008_10273_b200.shard import PeerFrames
+
+        peer = PeerFrames(world * per_rank_bytes, world, rank, local)
+        off = rank * per_rank_bytes
+        peer_addrs = []
+        for s_ in shapes:
+            peer_addrs.append(peer.base + off)
+            off += int(np.prod(s_))
+    gather_buf = torch.empty(per_rank_bytes if gather_mode == "nccl" else 0, dtype=torch.uint8, device="cuda")
 
     def pack_for_gather():
         off = 0
@@ -259,10 +277,15 @@ def main():
     def step(outs, timed_events):
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record()
-        span = codec.decode_streams(video, outs, gop_ranges=ranges, ctx=ctx, timings=timed_events)
-        if world > 1 and outs is dev_out:
-            pack_for_gather()
-            gather_frames(gather_buf, world, rank)  # decoded GOPs -> rank 0 over NCCL
+        if outs is dev_out and gather_mode == "peer":
+            span = codec.decode_streams(video, peer_addrs, gop_ranges=ranges, ctx=ctx, timings=timed_events,
+                                        peer=True)
+            dist.barrier()  # every rank's frames are in rank 0's buffer
+        else:
+            span = codec.decode_streams(video, outs, gop_ranges=ranges, ctx=ctx, timings=timed_events)
+            if outs is dev_out and gather_mode == "nccl":
+                pack_for_gather()
+                gather_frames(gather_buf, world, rank)  # decoded GOPs -> rank 0 over NCCL
         ev1.record()
         torch.cuda.synchronize()
         return ev0.elapsed_time(ev1) / 1e3, span
@@ -375,7 +398,9 @@ def main():
                 "workload": WORKLOAD,
                 "frames_per_rank": frames_per_rank,
                 "gops_per_rank": gops_per_rank,
-                "parallelism": f"gop-shard x{world}" + (" + nccl gather to rank 0" if world > 1 else ""),
+                "parallelism": f"gop-shard x{world}" + ({"peer": " + frames copied into rank 0's IPC-mapped buffer over "
+                                                           "NVLink during the decode",
+                                                           "nccl": " + nccl gather to rank 0"}.get(gather_mode, "")),
                 "input": "bitstream bytes in host RAM (parsed by host threads), frames written to HBM",
                 "l2": "flushed between timed steps (256 MiB device write)",
             },

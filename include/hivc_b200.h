@@ -211,9 +211,12 @@ int hivc_horn_schunck(hivc_ctx* ctx, const double* frame_t, const double* frame_
 /* ------------------------------------------------------------------ stream decode
  * Replaces codec.decode (codec.py:484-563) for the GOP range [gop_begin, gop_end):
  * frames are written as uint8 planes, layout [frame][channel][h][w] (gray: the
- * Y plane; colour: R, G, B after rct_inverse, frame.py:84-93).  `out` is a host
- * pointer when out_on_device == 0 (pinned memory recommended) else a device
- * pointer.  stage_seconds (nullable, 8 doubles) receives the reference timing
+ * Y plane; colour: R, G, B after rct_inverse, frame.py:84-93).  out_on_device:
+ * 0 = `out` is host memory (pinned recommended; each frame is copied out as it
+ * completes), 1 = device memory written directly, 2 = device memory reached
+ * through per-frame device-to-device copies on a copy stream (a peer GPU's
+ * buffer, e.g. CUDA-IPC-mapped: the multi-GPU gather fused into the decode).
+ * stage_seconds (nullable, 8 doubles) receives the reference timing
  * keys: intra_solve, flow_parse, warp, residual_parse, residual_transform,
  * finalize, total (codec.py:509-562), then the device-side span of the call
  * measured with CUDA events (first lane start -> last lane's final copy).
@@ -227,6 +230,16 @@ int hivc_decode(hivc_ctx* ctx, const uint8_t* data, size_t len, int32_t gop_begi
 int hivc_decode_multi(hivc_ctx* ctx, int32_t nstreams, const uint8_t* const* data, const size_t* len,
                       const int32_t* gop_begin, const int32_t* gop_end, uint8_t* const* out,
                       int32_t out_on_device, double* stage_seconds);
+/* Peer frame buffers for the fused multi-GPU gather: rank 0 allocates the whole
+ * job's frame buffer and exports a 64-byte CUDA IPC handle; every other rank
+ * maps it for its own device and decodes with out_on_device = 2 into its slice
+ * (each finished frame is copied over NVLink while the next ones decode). */
+int hivc_peer_alloc(int32_t device, size_t bytes, void** ptr, uint8_t* ipc_handle);
+int hivc_peer_open(int32_t device, const uint8_t* ipc_handle, void** ptr);
+int hivc_peer_close(void* ptr);
+int hivc_peer_free(void* ptr);
+/* Synchronous copy between any two (host / device / peer) addresses. */
+int hivc_memcpy(void* dst, const void* src, size_t bytes);
 /* Host<->device bytes moved by this context's decodes so far. */
 int hivc_ctx_bytes(hivc_ctx* ctx, int64_t* h2d, int64_t* d2h);
 /* Accumulated statistics of timed decodes (stage timing on), 10 doubles:

@@ -73,6 +73,11 @@ _proto("hivc_decode", C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_int32, C.
        c_dbl_p)
 _proto("hivc_decode_multi", C.c_int, C.c_void_p, C.c_int32, C.POINTER(C.c_void_p), c_size_p, c_int_p, c_int_p,
        C.POINTER(C.c_void_p), C.c_int32, c_dbl_p)
+_proto("hivc_peer_alloc", C.c_int, C.c_int32, C.c_size_t, C.POINTER(C.c_void_p), C.c_void_p)
+_proto("hivc_peer_open", C.c_int, C.c_int32, C.c_void_p, C.POINTER(C.c_void_p))
+_proto("hivc_peer_close", C.c_int, C.c_void_p)
+_proto("hivc_peer_free", C.c_int, C.c_void_p)
+_proto("hivc_memcpy", C.c_int, C.c_void_p, C.c_void_p, C.c_size_t)
 _proto("hivc_ctx_bytes", C.c_int, C.c_void_p, c_i64_p, c_i64_p)
 _proto("hivc_encode_symbols", C.c_int, C.c_void_p, C.c_size_t, C.c_int32, C.c_void_p, C.c_size_t, c_size_p)
 _proto("hivc_normalize_counts", C.c_int, C.c_void_p, C.c_size_t, C.c_int32, C.c_void_p)

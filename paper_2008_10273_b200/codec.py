@@ -74,26 +74,33 @@ def decode_frames(data: bytes, out=None, gop_begin: int = 0, gop_end: int | None
     return out
 
 
-def decode_streams(streams, outs, gop_ranges=None, ctx=None, timings: dict | None = None) -> float:
+def decode_streams(streams, outs, gop_ranges=None, ctx=None, timings: dict | None = None,
+                   peer: bool = False) -> float:
     """Decode several streams (e.g. the Y/Cb/Cr gray streams of a 4:2:0 video)
     in ONE native call sharing the decode lanes.  ``outs[k]``: uint8 buffer of
     ``frames_shape(streams[k], *gop_ranges[k])`` (all on the device or all on
-    the host).  Returns the device-side span in seconds (CUDA events)."""
+    the host).  ``peer=True``: ``outs`` are device addresses (ints) of a peer
+    GPU's frame buffer (``shard.PeerFrames``); every frame is copied there over
+    NVLink as it completes (``ctx`` required).  Returns the device-side span in
+    seconds (CUDA events)."""
     t = torch()
     n = len(streams)
     datas = [np.frombuffer(bytes(s), dtype=np.uint8) for s in streams]
-    on_dev = bool(getattr(outs[0], "is_cuda", False))
+    on_dev = peer or bool(getattr(outs[0], "is_cuda", False))
+    if peer and ctx is None:
+        raise ValueError("peer output needs the decoding GPU's context")
     if ctx is None:
         ctx = N.context(outs[0].device.index if on_dev else None)
     dptr = (C.c_void_p * n)(*[d.ctypes.data for d in datas])
     lens = (C.c_size_t * n)(*[len(d) for d in datas])
     gb = (C.c_int32 * n)(*[(r[0] if gop_ranges else 0) for r in (gop_ranges or [None] * n)])
     ge = (C.c_int32 * n)(*[(r[1] if gop_ranges and r[1] is not None else -1) for r in (gop_ranges or [None] * n)])
-    optr = (C.c_void_p * n)(*[(o.data_ptr() if hasattr(o, "data_ptr") else o.ctypes.data) for o in outs])
+    optr = (C.c_void_p * n)(*[(int(o) if peer else o.data_ptr() if hasattr(o, "data_ptr") else o.ctypes.data)
+                              for o in outs])
     stage = (C.c_double * 8)()
-    if on_dev:
+    if on_dev and not peer:
         t.cuda.current_stream(outs[0].device).synchronize()
-    N.check(N.lib.hivc_decode_multi(ctx.handle, n, dptr, lens, gb, ge, optr, int(on_dev), stage))
+    N.check(N.lib.hivc_decode_multi(ctx.handle, n, dptr, lens, gb, ge, optr, 2 if peer else int(on_dev), stage))
     if timings is not None:
         for k, v in zip(STAGES + ("device_span",), stage):
             timings[k] = timings.get(k, 0.0) + float(v)

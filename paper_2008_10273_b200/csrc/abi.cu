@@ -436,13 +436,51 @@ int hivc_horn_schunck(hivc_ctx* ctx, const double* frame_t, const double* frame_
     });
 }
 
+// ---------------------------------------------------------------- peer frame buffers (multi-GPU gather)
+
+int hivc_peer_alloc(int32_t device, size_t bytes, void** ptr, uint8_t* ipc_handle) {
+    return guarded([&] {
+        CUDA_CHECK(cudaSetDevice(device));
+        CUDA_CHECK(cudaMalloc(ptr, std::max<size_t>(bytes, 1)));
+        cudaIpcMemHandle_t h;
+        CUDA_CHECK(cudaIpcGetMemHandle(&h, *ptr));
+        std::memcpy(ipc_handle, &h, sizeof(h));
+    });
+}
+
+int hivc_peer_open(int32_t device, const uint8_t* ipc_handle, void** ptr) {
+    return guarded([&] {
+        CUDA_CHECK(cudaSetDevice(device));
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, ipc_handle, sizeof(h));
+        CUDA_CHECK(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    });
+}
+
+int hivc_peer_close(void* ptr) {
+    return guarded([&] { CUDA_CHECK(cudaIpcCloseMemHandle(ptr)); });
+}
+
+int hivc_peer_free(void* ptr) {
+    return guarded([&] { CUDA_CHECK(cudaFree(ptr)); });
+}
+
+int hivc_memcpy(void* dst, const void* src, size_t bytes) {
+    return guarded([&] { CUDA_CHECK(cudaMemcpy(dst, src, bytes, cudaMemcpyDefault)); });
+}
+
+static int out_mode_of(int32_t v) {
+    if (v < 0 || v > 2) hivc::fail(HIVC_E_ARGUMENT, "out_on_device must be 0 (host), 1 (device) or 2 (staged device)");
+    return v;
+}
+
 int hivc_decode(hivc_ctx* ctx, const uint8_t* data, size_t len, int32_t gop_begin, int32_t gop_end, uint8_t* out,
                 int32_t out_on_device, double* stage_seconds) {
     return guarded([&] {
         if (!ctx) hivc::fail(HIVC_E_ARGUMENT, "null context");
         CUDA_CHECK(cudaSetDevice(ctx->c.device));
         int gb = gop_begin, ge = gop_end;
-        hivc::decode_streams(ctx->c, 1, &data, &len, &gb, &ge, &out, out_on_device != 0, stage_seconds);
+        hivc::decode_streams(ctx->c, 1, &data, &len, &gb, &ge, &out, out_mode_of(out_on_device), stage_seconds);
     });
 }
 
@@ -453,7 +491,8 @@ int hivc_decode_multi(hivc_ctx* ctx, int32_t nstreams, const uint8_t* const* dat
         if (!ctx) hivc::fail(HIVC_E_ARGUMENT, "null context");
         if (nstreams < 1) hivc::fail(HIVC_E_ARGUMENT, "no streams");
         CUDA_CHECK(cudaSetDevice(ctx->c.device));
-        hivc::decode_streams(ctx->c, nstreams, data, len, gop_begin, gop_end, out, out_on_device != 0, stage_seconds);
+        hivc::decode_streams(ctx->c, nstreams, data, len, gop_begin, gop_end, out, out_mode_of(out_on_device),
+                             stage_seconds);
     });
 }
 

@@ -506,19 +506,26 @@ struct CallState {
     std::vector<Item>& items;
     std::deque<Group>& groups;
     Shared& sh;
-    bool out_on_device, timed;
+    bool out_on_device;  // frames written straight into `out` (out_mode 1)
+    bool timed;
     cudaEvent_t origin;
-    double t0;  // host clock at the origin event
+    double t0;     // host clock at the origin event
+    int out_mode;  // 0 host, 1 device, 2 device through per-frame staged copies (peer / IPC destinations)
 };
 
+// A finished frame leaves the slot's GOP buffer on the copy stream while the
+// next frames decode: D2H into host frames (out_mode 0), or device-to-device
+// into a peer GPU's frame buffer over NVLink (out_mode 2: the multi-GPU
+// gather fused into the decode, frame by frame).
 void copy_out(CallState& cs, Slot& L, Item& it, size_t fi, size_t frame_bytes) {
     if (cs.out_on_device) return;
     cudaEvent_t fe = L.frame_ev[L.frame_ev_next++ % Slot::kFrameEv];
     CUDA_CHECK(cudaEventRecord(fe, L.stream));
     CUDA_CHECK(cudaStreamWaitEvent(L.copy, fe, 0));
+    const bool d2d = cs.out_mode == 2;
     CUDA_CHECK(cudaMemcpyAsync(it.gop_host + fi * frame_bytes, it.gop_dev + fi * frame_bytes, frame_bytes,
-                               cudaMemcpyDeviceToHost, L.copy));
-    it.d2h += (int64_t)frame_bytes;
+                               d2d ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, L.copy));
+    if (!d2d) it.d2h += (int64_t)frame_bytes;
 }
 
 // Solve the staged I-frames of items idx (same shape): pyramid + cluster
@@ -741,7 +748,8 @@ void inter_phase(CallState& cs, Item& it) {
 }  // namespace
 
 void decode_streams(Context& ctx, int nstreams, const uint8_t* const* data, const size_t* len, const int* gop_begin,
-                    const int* gop_end, uint8_t* const* out, bool out_on_device, double* stage_seconds) {
+                    const int* gop_end, uint8_t* const* out, int out_mode, double* stage_seconds) {
+    const bool out_on_device = out_mode == 1;
     double t_all = now_s();
     std::vector<StreamJob> streams(nstreams);
     std::vector<Item> items;
@@ -823,7 +831,7 @@ void decode_streams(Context& ctx, int nstreams, const uint8_t* const* data, cons
     CUDA_CHECK(cudaStreamWaitEvent(ctx.solver, origin, 0));
     for (cudaStream_t p : ctx.pre) CUDA_CHECK(cudaStreamWaitEvent(p, origin, 0));
     Shared sh;
-    CallState cs{ctx, streams, items, groups, sh, out_on_device, timed, origin, now_s()};
+    CallState cs{ctx, streams, items, groups, sh, out_on_device, timed, origin, now_s(), out_mode};
     // task queue: every item's intra phase, then the inter phases, both in
     // batch-issue order.  A pool thread that reaches the inter phases drops
     // its scheduling priority: P-frame parsing has slack (its GPU work queues

@@ -101,7 +101,7 @@ struct Context {
 // GOP), parsed by a pool of host threads; I-frame solves batched per shape).  stage_seconds (nullable, 8 doubles): the 7
 // reference timing keys + the device-side span (first lane start -> last lane end).
 void decode_streams(Context& ctx, int nstreams, const uint8_t* const* data, const size_t* len, const int* gop_begin,
-                    const int* gop_end, uint8_t* const* out, bool out_on_device, double* stage_seconds);
+                    const int* gop_end, uint8_t* const* out, int out_mode, double* stage_seconds);
 
 // Host-only parse of every frame record (8 int64 per frame, see decode.cu).
 void parse_stream_stats(const uint8_t* data, size_t len, std::vector<int64_t>& stats, double* seconds);

@@ -105,3 +105,57 @@ def encode_sharded(frames, cfg=None, world: int = 1, rank: int = 0, _flows=None,
     from paper_2008_10273_b200.bitstream import write_stream
 
     return write_stream(header, allp)
+
+
+class PeerFrames:
+    """The job's decoded-frame buffer on rank ``owner``'s GPU, mapped into every
+    rank's address space through CUDA IPC (``hivc_peer_alloc`` / ``hivc_peer_open``).
+
+    Ranks decode with ``codec.decode_streams(..., peer=True)`` into their slice:
+    each finished frame is copied device-to-device over NVLink by the decoder's
+    copy streams while later frames decode, so the gather to rank 0 is fused
+    into the decode instead of following it (an NCCL gather of 186 MB per rank
+    and step would serialise after the last frame).  The handle travels over
+    ``torch.distributed`` (any backend); one process per GPU.
+    """
+
+    def __init__(self, nbytes: int, world: int, rank: int, device: int, owner: int = 0):
+        import ctypes as C
+
+        import torch.distributed as dist
+
+        from paper_2008_10273_b200 import _native as N
+
+        self.nbytes, self.rank, self.owner, self.device = int(nbytes), rank, owner, device
+        self._N = N
+        self.ptr = C.c_void_p()
+        handle = (C.c_uint8 * 64)()
+        if rank == owner:
+            N.check(N.lib.hivc_peer_alloc(device, self.nbytes, C.byref(self.ptr), handle))
+        box = [bytes(handle) if rank == owner else None]
+        if world > 1:
+            dist.broadcast_object_list(box, src=owner)
+        if rank != owner:
+            h = (C.c_uint8 * 64).from_buffer_copy(box[0])
+            N.check(N.lib.hivc_peer_open(device, h, C.byref(self.ptr)))
+
+    @property
+    def base(self) -> int:
+        return int(self.ptr.value)
+
+    def to_host(self, offset: int = 0, nbytes: int | None = None):
+        """Copy (part of) the buffer into a numpy uint8 array (synchronous)."""
+        import numpy as np
+
+        n = self.nbytes - offset if nbytes is None else nbytes
+        out = np.empty(n, dtype=np.uint8)
+        self._N.check(self._N.lib.hivc_memcpy(out.ctypes.data, self.base + offset, n))
+        return out
+
+    def close(self):
+        if self.ptr.value:
+            if self.rank == self.owner:
+                self._N.check(self._N.lib.hivc_peer_free(self.ptr))
+            else:
+                self._N.check(self._N.lib.hivc_peer_close(self.ptr))
+            self.ptr.value = None
