@@ -259,7 +259,17 @@ def main():
     if gather_mode == "peer":
         from paper_2008_10273_b200.shard import PeerFrames
 
-        peer = PeerFrames(world * per_rank_bytes, world, rank, local)
+        try:
+            peer = PeerFrames(world * per_rank_bytes, world, rank, local)
+        except Exception as e:  # e.g. CUDA IPC unavailable: every rank falls back to the NCCL gather
+            print(f"[bench] rank {rank}: peer frame buffer unavailable ({e}); NCCL gather", file=sys.stderr)
+        ok = torch.tensor([1 if peer is not None else 0], device="cuda")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if int(ok.item()) == 0:
+            if peer is not None:
+                peer.close()
+            peer, gather_mode = None, "nccl"
+    if gather_mode == "peer":
         off = rank * per_rank_bytes
         peer_addrs = []
         for s_ in shapes:

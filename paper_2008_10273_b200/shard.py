@@ -130,11 +130,14 @@ class PeerFrames:
         self._N = N
         self.ptr = C.c_void_p()
         handle = (C.c_uint8 * 64)()
+        ok = True
         if rank == owner:
-            N.check(N.lib.hivc_peer_alloc(device, self.nbytes, C.byref(self.ptr), handle))
-        box = [bytes(handle) if rank == owner else None]
+            ok = N.lib.hivc_peer_alloc(device, self.nbytes, C.byref(self.ptr), handle) == 0
+        box = [bytes(handle) if rank == owner and ok else None]
         if world > 1:
-            dist.broadcast_object_list(box, src=owner)
+            dist.broadcast_object_list(box, src=owner)  # every rank takes part, even on failure
+        if box[0] is None:
+            raise RuntimeError("peer frame buffer allocation failed on the owner rank")
         if rank != owner:
             h = (C.c_uint8 * 64).from_buffer_copy(box[0])
             N.check(N.lib.hivc_peer_open(device, h, C.byref(self.ptr)))
