@@ -229,10 +229,18 @@ def main():
     import torch
     import torch.distributed as dist
 
+    # HIVC_BENCH_DEVICE / HIVC_DIST_BACKEND: functional check of the N > 1 code
+    # path with all ranks on one GPU over gloo (NCCL refuses duplicate GPUs);
+    # such a run's timings are meaningless and it is never a bench result.
+    local = int(os.environ.get("HIVC_BENCH_DEVICE", local))
     torch.cuda.set_device(local)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("HIVC_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     import ctypes as C
 
     from paper_2008_10273_b200 import _native as N
@@ -318,6 +326,19 @@ def main():
             spans.append(span)
     launches = ctx.launches - launches0
     clocks = clk.summary()
+
+    # N > 1, outside the timed region: rank 0's buffer must hold every rank's frames
+    gather_verified = None
+    if world > 1 and gather_mode == "peer":
+        codec.decode_streams(video, dev_out, gop_ranges=ranges, ctx=ctx)
+        mine = torch.cat([o.view(-1) for o in dev_out]).cpu().numpy()
+        sums = [None] * world
+        dist.all_gather_object(sums, int(np.sum(mine.astype(np.int64) * (1 + np.arange(mine.size) % 251))))
+        if rank == 0:
+            buf = peer.to_host()
+            got = [int(np.sum(buf[r * per_rank_bytes : (r + 1) * per_rank_bytes].astype(np.int64)
+                              * (1 + np.arange(per_rank_bytes) % 251))) for r in range(world)]
+            gather_verified = got == sums
 
     # instrumented steps (not timed): per-stage times, the CG level launches'
     # in-kernel spans and iteration counts for the roofline, P-kernel times
@@ -421,6 +442,7 @@ def main():
                 "d2h_bytes_per_step": int(d2h),
             },
             "gpu_launches": int(launches),
+            **({"gather_verified": gather_verified} if gather_verified is not None else {}),
             "device_span_ms": 1e3 * statistics.median(spans),
             "stages_ms_per_step": {k: round(1e3 * v / n_instr, 3) for k, v in timings.items()},
             "stages_note": f"from {n_instr} separate instrumented (CUDA-event) steps, not the timed ones",
