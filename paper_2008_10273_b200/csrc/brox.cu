@@ -251,6 +251,86 @@ __global__ void jacobi_kernel(Sys S, const double* __restrict__ du, const double
     }
 }
 
+// Two damped Jacobi sweeps per launch: du, dv of a 32x16 tile plus a 2-pixel
+// halo in shared memory; the 2x2 systems are re-read from global memory in the
+// second sweep, where they hit L1 (the tile's ~40 KB were just read), so the
+// HBM-bound large levels move ~1.7x fewer bytes per sweep.  The halo ring is
+// computed redundantly in sweep 1; sweep s is exact on the tile shrunk by s+1
+// on interior sides, so the inner tile equals two jacobi_kernel launches bit
+// for bit.
+constexpr int kJ2TX = 32, kJ2TY = 16, kJ2H = 2, kJ2NT = 256;
+constexpr int kJ2HX = kJ2TX + 2 * kJ2H, kJ2HY = kJ2TY + 2 * kJ2H, kJ2HN = kJ2HX * kJ2HY;
+
+__global__ void __launch_bounds__(kJ2NT) jacobi2_kernel(Sys S, const double* __restrict__ du_in,
+                                                       const double* __restrict__ dv_in, double* __restrict__ du_out,
+                                                       double* __restrict__ dv_out, int h, int w, double alpha,
+                                                       int nsweeps, int clip_last) {
+    __shared__ double sm[4 * kJ2HN];
+    double* cu = sm;
+    double* cv = sm + kJ2HN;
+    double* nu = sm + 2 * kJ2HN;
+    double* nv = sm + 3 * kJ2HN;
+    const int tid = threadIdx.x;
+    const int gx0 = blockIdx.x * kJ2TX - kJ2H, gy0 = blockIdx.y * kJ2TY - kJ2H;
+    for (int i = tid; i < kJ2HN; i += kJ2NT) {
+        const int gx = gx0 + i % kJ2HX, gy = gy0 + i / kJ2HX;
+        if (gx >= 0 && gx < w && gy >= 0 && gy < h) {
+            const size_t g = (size_t)gy * w + gx;
+            cu[i] = du_in[g];
+            cv[i] = dv_in[g];
+        }
+    }
+    __syncthreads();
+    for (int sw = 0; sw < nsweeps; ++sw) {
+        const bool clip = clip_last && sw == nsweeps - 1;
+        for (int i = tid; i < kJ2HN; i += kJ2NT) {
+            const int lx = i % kJ2HX, ly = i / kJ2HX, gx = gx0 + lx, gy = gy0 + ly;
+            // exact region of this sweep: inside the image, sw+1 away from interior halo edges
+            const int m = sw + 1;
+            if (gx < 0 || gx >= w || gy < 0 || gy >= h) continue;
+            if ((gy != 0 && ly < m) || (gy != h - 1 && ly > kJ2HY - 1 - m) || (gx != 0 && lx < m) ||
+                (gx != w - 1 && lx > kJ2HX - 1 - m))
+                continue;
+            const size_t g = (size_t)gy * w + gx;
+            const W4 W = weights_at(S.psi_s, gy, gx, h, w);
+            const int in = gy == 0 ? i : i - kJ2HX, is = gy == h - 1 ? i : i + kJ2HX;
+            const int iw = gx == 0 ? i : i - 1, ie = gx == w - 1 ? i : i + 1;
+            const double nsu = ((W.n * cu[in] + W.s * cu[is]) + W.w * cu[iw]) + W.e * cu[ie];
+            const double nsv = ((W.n * cv[in] + W.s * cv[is]) + W.w * cv[iw]) + W.e * cv[ie];
+            const double b1 = S.b1f[g] + alpha * (S.su[g] + nsu);
+            const double b2 = S.b2f[g] + alpha * (S.sv[g] + nsv);
+            const double a11 = S.a11[g], a12 = S.a12[g], a22 = S.a22[g];
+            double det = a11 * a22 - a12 * a12;
+            det = fabs(det) < 1e-12 ? 1e-12 : det;
+            const double dun = (a22 * b1 - a12 * b2) / det;
+            const double dvn = (a11 * b2 - a12 * b1) / det;
+            double a = 0.5 * cu[i] + 0.5 * dun;
+            double b = 0.5 * cv[i] + 0.5 * dvn;
+            if (clip) {
+                a = fmin(fmax(a, -1.0), 1.0);
+                b = fmin(fmax(b, -1.0), 1.0);
+            }
+            nu[i] = a;
+            nv[i] = b;
+        }
+        __syncthreads();
+        double* t = cu;
+        cu = nu;
+        nu = t;
+        t = cv;
+        cv = nv;
+        nv = t;
+    }
+    for (int k = tid; k < kJ2TX * kJ2TY; k += kJ2NT) {
+        const int lx = kJ2H + k % kJ2TX, ly = kJ2H + k / kJ2TX, gx = gx0 + lx, gy = gy0 + ly;
+        if (gx < w && gy < h) {
+            const size_t g = (size_t)gy * w + gx;
+            du_out[g] = cu[ly * kJ2HX + lx];
+            dv_out[g] = cv[ly * kJ2HX + lx];
+        }
+    }
+}
+
 __device__ __forceinline__ void cswap(double& a, double& b) {
     double lo = fmin(a, b), hi = fmax(a, b);
     a = lo;
@@ -326,6 +406,17 @@ static void set_taps(Taps& T, int& radius, const double* host_taps, int ntaps) {
     for (int i = 0; i < ntaps && i < 64; ++i) T.t[i] = host_taps[i];
 }
 
+// levels of at least HIVC_BROX_J2_MIN pixels (default 1 Mpx: the HBM-bound
+// ones) run two Jacobi sweeps per launch; 0 disables (measured at 1080p /
+// pyramid 0.95: 242 ms per pair -> 234 ms; on smaller levels it does not pay)
+static int jacobi2_min_px() {
+    static const int v = [] {
+        const char* e = std::getenv("HIVC_BROX_J2_MIN");
+        return e ? std::atoi(e) : (1 << 20);
+    }();
+    return v;
+}
+
 // The whole estimator as a launch sequence on stream s (captured once per
 // shape/parameter set into a CUDA graph by brox_flow).
 static void enqueue_brox(BroxWorkspace& ws, cudaStream_t s, const std::vector<std::pair<int, int>>& shapes,
@@ -399,11 +490,19 @@ static void enqueue_brox(BroxWorkspace& ws, cudaStream_t s, const std::vector<st
                 robust_kernel<<<nb, kT, 0, s>>>(Lz, Sz, u, v, du, dv, hh, ww, P.gamma, eps2);
                 system_kernel<<<nb, kT, 0, s>>>(Lz, Sz, u, v, hh, ww, P.alpha);
                 *launches += 2;
-                for (int it = 0; it < P.solver_iters; ++it) {
-                    jacobi_kernel<<<nb, kT, 0, s>>>(Sz, du, dv, du2, dv2, hh, ww, P.alpha, it == P.solver_iters - 1);
+                const bool two = jacobi2_min_px() > 0 && n >= (size_t)jacobi2_min_px();
+                const dim3 g2((ww + kJ2TX - 1) / kJ2TX, (hh + kJ2TY - 1) / kJ2TY);
+                for (int it = 0; it < P.solver_iters;) {
+                    const int k = two ? std::min(2, P.solver_iters - it) : 1;
+                    const bool last = it + k == P.solver_iters;
+                    if (two)
+                        jacobi2_kernel<<<g2, kJ2NT, 0, s>>>(Sz, du, dv, du2, dv2, hh, ww, P.alpha, k, last);
+                    else
+                        jacobi_kernel<<<nb, kT, 0, s>>>(Sz, du, dv, du2, dv2, hh, ww, P.alpha, last);
                     ++*launches;
                     std::swap(du, du2);
                     std::swap(dv, dv2);
+                    it += k;
                 }
                 if (P.solver_iters == 0) {  // clip still applies
                     clip_kernel<<<nb, kT, 0, s>>>(du, n, 1.0);
