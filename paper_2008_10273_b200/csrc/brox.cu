@@ -14,6 +14,7 @@
 // sweeps are 30 launches of one small kernel).  The whole launch sequence
 // (~500 kernels per pyramid level) is captured once per shape / parameter set
 // into a CUDA graph and replayed (HIVC_BROX_GRAPH=0: direct launches).
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -331,6 +332,173 @@ __global__ void __launch_bounds__(kJ2NT) jacobi2_kernel(Sys S, const double* __r
     }
 }
 
+// All sweeps of a small level (<= kJCMaxPx px) in ONE launch: one thread-block
+// cluster of up to 16 CTAs, CTA c owning a band of rows.  Each thread keeps
+// the 2x2 systems of its kJCPx pixels in registers (a11, a12, a22, the clamped
+// determinant, b1f, b2f, su, sv) and their half-point weights in shared
+// memory; du, dv live in shared memory (two buffers), and the band's halo
+// rows are copied from the neighbouring CTAs' buffers over DSMEM at the start
+// of every sweep, one cluster barrier per sweep.  Replaces 30 launches that
+// are launch-latency bound below ~128 kpx; every expression is jacobi_kernel's,
+// so the result is bit-identical.
+constexpr int kJCNT = 512, kJCPx = 4, kJCMaxCtas = 16;
+constexpr int kJCBand = kJCNT * kJCPx;  // px per CTA
+
+__global__ void __launch_bounds__(kJCNT, 1) jacobi_cluster_kernel(Sys S, const double* __restrict__ du_in,
+                                                                 const double* __restrict__ dv_in,
+                                                                 double* __restrict__ du_out,
+                                                                 double* __restrict__ dv_out, int h, int w, int rpc,
+                                                                 double alpha, int iters, int clip_last) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    extern __shared__ double jsm[];
+    const int rank = (int)cluster.block_rank(), nct = (int)cluster.num_blocks();
+    const int y0 = rank * rpc, rows = min(rpc, h - y0), np = rows * w;
+    const int H = (rpc + 2) * w;  // band + halo rows
+    double* Wn = jsm;             // [kJCBand] x 4 weights
+    double* Ws = Wn + kJCBand;
+    double* Ww = Ws + kJCBand;
+    double* We = Ww + kJCBand;
+    double* buf = We + kJCBand;  // [2][du, dv][H]
+    const int tid = threadIdx.x;
+    double a11[kJCPx], a12[kJCPx], a22[kJCPx], det[kJCPx], b1f[kJCPx], b2f[kJCPx], su[kJCPx], sv[kJCPx];
+#pragma unroll
+    for (int j = 0; j < kJCPx; ++j) {
+        const int q = tid + j * kJCNT;
+        if (q < np) {
+            const int y = y0 + q / w, x = q % w;
+            const size_t g = (size_t)y * w + x;
+            const W4 W = weights_at(S.psi_s, y, x, h, w);
+            Wn[q] = W.n;
+            Ws[q] = W.s;
+            Ww[q] = W.w;
+            We[q] = W.e;
+            a11[j] = S.a11[g];
+            a12[j] = S.a12[g];
+            a22[j] = S.a22[g];
+            double d = a11[j] * a22[j] - a12[j] * a12[j];
+            det[j] = fabs(d) < 1e-12 ? 1e-12 : d;
+            b1f[j] = S.b1f[g];
+            b2f[j] = S.b2f[g];
+            su[j] = S.su[g];
+            sv[j] = S.sv[g];
+            buf[w + q] = du_in[g];
+            buf[H + w + q] = dv_in[g];
+        }
+    }
+    cluster.sync();
+    for (int it = 0; it < iters; ++it) {
+        double* cu = buf + (it & 1) * 2 * H;
+        double* cv = cu + H;
+        double* nu = buf + ((it + 1) & 1) * 2 * H;
+        double* nv = nu + H;
+        // halo rows: the upper CTA's last band row, the lower CTA's first
+        if (rank > 0) {
+            const double* pu = cluster.map_shared_rank(cu, rank - 1);
+            const double* pv = cluster.map_shared_rank(cv, rank - 1);
+            for (int x = tid; x < w; x += kJCNT) {
+                cu[x] = pu[rpc * w + x];
+                cv[x] = pv[rpc * w + x];
+            }
+        }
+        if (rank < nct - 1) {
+            const double* pu = cluster.map_shared_rank(cu, rank + 1);
+            const double* pv = cluster.map_shared_rank(cv, rank + 1);
+            for (int x = tid; x < w; x += kJCNT) {
+                cu[(rows + 1) * w + x] = pu[w + x];
+                cv[(rows + 1) * w + x] = pv[w + x];
+            }
+        }
+        __syncthreads();
+        const bool clip = clip_last && it == iters - 1;
+#pragma unroll
+        for (int j = 0; j < kJCPx; ++j) {
+            const int q = tid + j * kJCNT;
+            if (q < np) {
+                const int y = y0 + q / w, x = q % w;
+                const int i = w + q;
+                const int in = y == 0 ? i : i - w, is = y == h - 1 ? i : i + w;
+                const int iw = x == 0 ? i : i - 1, ie = x == w - 1 ? i : i + 1;
+                const double wn = Wn[q], ws = Ws[q], ww = Ww[q], we = We[q];
+                const double nsu = ((wn * cu[in] + ws * cu[is]) + ww * cu[iw]) + we * cu[ie];
+                const double nsv = ((wn * cv[in] + ws * cv[is]) + ww * cv[iw]) + we * cv[ie];
+                const double b1 = b1f[j] + alpha * (su[j] + nsu);
+                const double b2 = b2f[j] + alpha * (sv[j] + nsv);
+                const double dun = (a22[j] * b1 - a12[j] * b2) / det[j];
+                const double dvn = (a11[j] * b2 - a12[j] * b1) / det[j];
+                double a = 0.5 * cu[i] + 0.5 * dun;
+                double b = 0.5 * cv[i] + 0.5 * dvn;
+                if (clip) {
+                    a = fmin(fmax(a, -1.0), 1.0);
+                    b = fmin(fmax(b, -1.0), 1.0);
+                }
+                nu[i] = a;
+                nv[i] = b;
+            }
+        }
+        cluster.sync();
+    }
+    const double* fu = buf + (iters & 1) * 2 * H;
+    const double* fv = fu + H;
+#pragma unroll
+    for (int j = 0; j < kJCPx; ++j) {
+        const int q = tid + j * kJCNT;
+        if (q < np) {
+            const size_t g = (size_t)y0 * w + q;
+            du_out[g] = fu[w + q];
+            dv_out[g] = fv[w + q];
+        }
+    }
+}
+
+// Cluster layout of a level for jacobi_cluster_kernel (rows per CTA, CTAs), or
+// {0, 0} when the level does not fit (then the per-sweep launches run).
+struct JcPlan {
+    int rpc = 0, ctas = 0;
+    size_t smem = 0;
+};
+static JcPlan jc_plan(int h, int w) {
+    JcPlan p;
+    static const int max_px = [] {
+        const char* e = std::getenv("HIVC_BROX_JC_MAX");
+        return e ? std::atoi(e) : kJCMaxCtas * kJCBand;
+    }();
+    if ((long long)h * w > max_px || w > kJCBand) return p;
+    const int ctas = std::min(kJCMaxCtas, h);
+    const int rpc = (h + ctas - 1) / ctas;
+    if ((long long)rpc * w > kJCBand) return p;
+    const size_t smem = (size_t)(4 * kJCBand + 4 * (rpc + 2) * w) * sizeof(double);
+    if (smem > 200 * 1024) return p;
+    p.rpc = rpc;
+    p.ctas = (h + rpc - 1) / rpc;
+    p.smem = smem;
+    return p;
+}
+
+static void launch_jacobi_cluster(const JcPlan& jp, const Sys& S, const double* du, const double* dv, double* du2,
+                                  double* dv2, int h, int w, double alpha, int iters, cudaStream_t s) {
+    static const bool init = [] {
+        CUDA_CHECK(cudaFuncSetAttribute(jacobi_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        CUDA_CHECK(cudaFuncSetAttribute(jacobi_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        200 * 1024));
+        return true;
+    }();
+    (void)init;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(jp.ctas);
+    cfg.blockDim = dim3(kJCNT);
+    cfg.dynamicSmemBytes = jp.smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = jp.ctas;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CUDA_CHECK(cudaLaunchKernelEx(&cfg, jacobi_cluster_kernel, S, du, dv, du2, dv2, h, w, jp.rpc, alpha, iters, 1));
+}
+
 __device__ __forceinline__ void cswap(double& a, double& b) {
     double lo = fmin(a, b), hi = fmax(a, b);
     a = lo;
@@ -490,6 +658,14 @@ static void enqueue_brox(BroxWorkspace& ws, cudaStream_t s, const std::vector<st
                 robust_kernel<<<nb, kT, 0, s>>>(Lz, Sz, u, v, du, dv, hh, ww, P.gamma, eps2);
                 system_kernel<<<nb, kT, 0, s>>>(Lz, Sz, u, v, hh, ww, P.alpha);
                 *launches += 2;
+                const JcPlan jp = P.solver_iters > 0 ? jc_plan(hh, ww) : JcPlan{};
+                if (jp.ctas > 0) {  // all sweeps in one cluster launch
+                    launch_jacobi_cluster(jp, Sz, du, dv, du2, dv2, hh, ww, P.alpha, P.solver_iters, s);
+                    ++*launches;
+                    std::swap(du, du2);
+                    std::swap(dv, dv2);
+                    continue;
+                }
                 const bool two = jacobi2_min_px() > 0 && n >= (size_t)jacobi2_min_px();
                 const dim3 g2((ww + kJ2TX - 1) / kJ2TX, (hh + kJ2TY - 1) / kJ2TY);
                 for (int it = 0; it < P.solver_iters;) {

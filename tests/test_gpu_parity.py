@@ -1,6 +1,7 @@
 """CUDA path vs the oracle / reference goldens, through the C ABI.  Needs a B200."""
 
 import numpy as np
+from pathlib import Path
 import pytest
 
 pytestmark = pytest.mark.gpu
@@ -234,6 +235,32 @@ def test_flow_brox_vs_oracle_larger():
     ru, rv = brox.brox(clip[1], clip[0])
     ff = flow_brox(clip[1], clip[0])
     assert max(np.abs(ff.u - ru).max(), np.abs(ff.v - rv).max()) <= 1e-6
+
+
+def test_flow_brox_cluster_sweeps_bit_identical(tmp_path):
+    """Small levels run all Jacobi sweeps in one cluster launch; the result must equal
+    the per-sweep launches (HIVC_BROX_JC_MAX=0) bit for bit, with and without the graph."""
+    import os
+    import subprocess
+    import sys
+
+    from paper_2008_10273_b200.flow import BroxParams, flow_brox
+    from paper_2008_10273_b200.synth import synth_clip
+
+    clip = synth_clip(2, 180, 320, blobs=8, rects=3, v=3.0, seed=0)[:, 0].astype(np.float64)
+    np.save(tmp_path / "clip.npy", clip)
+    ff = flow_brox(clip[1], clip[0], BroxParams(pyramid_scale=0.95))
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, %r)\n"
+        "from paper_2008_10273_b200.flow import BroxParams, flow_brox\n"
+        "c = np.load(%r); f = flow_brox(c[1], c[0], BroxParams(pyramid_scale=0.95))\n"
+        "np.save(%r, np.stack([f.u, f.v]))\n"
+    ) % (str(Path(__file__).resolve().parent.parent), str(tmp_path / "clip.npy"), str(tmp_path / "uv.npy"))
+    for graph in ("1", "0"):
+        env = dict(os.environ, HIVC_BROX_JC_MAX="0", HIVC_BROX_GRAPH=graph)
+        subprocess.run([sys.executable, "-c", code], env=env, check=True, timeout=600)
+        uv = np.load(tmp_path / "uv.npy")
+        assert np.array_equal(uv[0], ff.u) and np.array_equal(uv[1], ff.v), graph
 
 
 def test_solve_homogeneous_repeatable_across_shapes():
