@@ -166,8 +166,57 @@ __device__ __forceinline__ void reduce(double (&v)[NV], double* sh, const CgPara
     __syncthreads();
 }
 
-// Grid-wide fixed-order sum with 3 CTA barriers: block_sum1, the grid
-// arrival/wait, and the broadcast of warp 0's sum over the CTA partials.
+// Fixed-order sum of the n CTA partials of each of the NV values (lane l
+// adds partials l, l + 32, ... in order, then warp_sum); warp k sums value k,
+// and each lane issues all its loads before the first add, so the partials
+// arrive in ONE L2 round trip (a runtime-bound loop took two or more).
+constexpr int kSumPer = 5;  // unrolled loads per lane: n <= 160 (one CTA per SM)
+template <int NV>
+__device__ __forceinline__ void sum_partials(const double* part, int n, double* bc) {
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (wid >= NV) return;
+    double s = 0.0;
+    if (n <= 32 * kSumPer) {
+        double vals[kSumPer];
+#pragma unroll
+        for (int j = 0; j < kSumPer; ++j) {
+            const int g = lane + 32 * j;
+            vals[j] = g < n ? __ldcg(part + g * 4 + wid) : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < kSumPer; ++j)
+            if (lane + 32 * j < n) s += vals[j];
+    } else {
+        for (int g = lane; g < n; g += 32) s += __ldcg(part + g * 4 + wid);
+    }
+    s = warp_sum(s);
+    if (lane == 0) bc[wid] = s;
+}
+
+// This CTA's partial of each value into part[0..NV): warp sums, one CTA
+// barrier, then lane k of warp 0 adds the warp partials of value k in warp
+// order (block_sum1's order, without every thread re-reading them).
+template <int NV>
+__device__ __forceinline__ void cta_partial(double (&v)[NV], double* sh, int& par, double* part) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    double* buf = sh + par * NV * 32;
+    par ^= 1;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) v[k] = warp_sum(v[k]);
+    if (lane == 0)
+#pragma unroll
+        for (int k = 0; k < NV; ++k) buf[k * 32 + wid] = v[k];
+    __syncthreads();
+    if (threadIdx.x < NV) {
+        double s = 0.0;
+        for (int i = 0; i < nw; ++i) s += buf[threadIdx.x * 32 + i];
+        part[threadIdx.x] = s;
+    }
+    if (threadIdx.x < 32) __syncwarp();  // lanes 1..NV-1's stores before lane 0's arrival (release)
+}
+
+// Grid-wide fixed-order sum with 3 CTA barriers: cta_partial, the grid
+// arrival/wait, and the broadcast of the sums over the CTA partials.
 // sh: 2*4*32 (block_sum1 buffers) + 2*4 (broadcast buffers) doubles.
 struct RedState {
     unsigned int epoch = 0;
@@ -178,24 +227,12 @@ struct RedState {
 template <int NV>
 __device__ __forceinline__ void grid_reduce(double (&v)[NV], double* sh, const CgParams& P, RedState& st, int idx,
                                             int n) {
-    block_sum1<NV>(v, sh, st.par);
     double* part = P.partials + ((st.epoch + 1) & 1) * kPartialBank;
-    if (threadIdx.x == 0)
-#pragma unroll
-        for (int k = 0; k < NV; ++k) part[idx * 4 + k] = v[k];
+    cta_partial<NV>(v, sh, st.par, part + idx * 4);
     grid_arrive_wait(P.bar, n, st.epoch);
     double* bc = sh + 2 * 4 * 32 + st.bpar * 4;
     st.bpar ^= 1;
-    if (threadIdx.x < 32) {
-        const int lane = threadIdx.x;
-#pragma unroll
-        for (int k = 0; k < NV; ++k) {
-            double s = 0.0;
-            for (int g = lane; g < n; g += 32) s += __ldcg(part + g * 4 + k);
-            s = warp_sum(s);
-            if (lane == 0) bc[k] = s;
-        }
-    }
+    sum_partials<NV>(part, n, bc);
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < NV; ++k) v[k] = bc[k];
@@ -204,11 +241,8 @@ __device__ __forceinline__ void grid_reduce(double (&v)[NV], double* sh, const C
 template <int NV>
 __device__ __forceinline__ void grid_reduce_arrive(double (&v)[NV], double* sh, const CgParams& P, RedState& st,
                                                    int idx) {
-    block_sum1<NV>(v, sh, st.par);
     double* part = P.partials + ((st.epoch + 1) & 1) * kPartialBank;
-    if (threadIdx.x == 0)
-#pragma unroll
-        for (int k = 0; k < NV; ++k) part[idx * 4 + k] = v[k];
+    cta_partial<NV>(v, sh, st.par, part + idx * 4);
     grid_arrive(P.bar, st.epoch);
 }
 template <int NV>
@@ -218,16 +252,7 @@ __device__ __forceinline__ void grid_reduce_finish(double (&v)[NV], double* sh, 
     const double* part = P.partials + (st.epoch & 1) * kPartialBank;
     double* bc = sh + 2 * 4 * 32 + st.bpar * 4;
     st.bpar ^= 1;
-    if (threadIdx.x < 32) {
-        const int lane = threadIdx.x;
-#pragma unroll
-        for (int k = 0; k < NV; ++k) {
-            double s = 0.0;
-            for (int g = lane; g < n; g += 32) s += __ldcg(part + g * 4 + k);
-            s = warp_sum(s);
-            if (lane == 0) bc[k] = s;
-        }
-    }
+    sum_partials<NV>(part, n, bc);
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < NV; ++k) v[k] = bc[k];
