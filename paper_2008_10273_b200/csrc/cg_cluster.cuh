@@ -57,9 +57,20 @@ __global__ void __launch_bounds__(kClThreads, 1) cg_cluster_kernel(const __grid_
 
     // fixed-order cluster-wide sum of NV values (identical in every CTA)
     auto creduce = [&](double* v, int nv) {
-        block_sum1<4>(*reinterpret_cast<double(*)[4]>(v), sh, par);
-        if (tid == 0)
-            for (int k = 0; k < nv; ++k) red[rpar][k] = v[k];
+        {  // this CTA's sums: warp sums, then lane k of warp 0 adds value k's warp sums in warp order
+            const int lane = tid & 31, wid = tid >> 5, nw = kClThreads >> 5;
+            double* buf = sh + par * 4 * 32;
+            par ^= 1;
+            for (int k = 0; k < nv; ++k) v[k] = warp_sum(v[k]);
+            if (lane == 0)
+                for (int k = 0; k < nv; ++k) buf[k * 32 + wid] = v[k];
+            __syncthreads();
+            if (tid < nv) {
+                double s = 0.0;
+                for (int i = 0; i < nw; ++i) s += buf[tid * 32 + i];
+                red[rpar][tid] = s;
+            }
+        }
         cluster.sync();
         if (tid < 32) {
             double s[4] = {0, 0, 0, 0};
