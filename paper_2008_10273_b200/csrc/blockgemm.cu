@@ -72,9 +72,9 @@ __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__flo
 }  // namespace
 
 // rec[b] = R f[b] for every 8x8 block b of the plane (f32 in/out), 3xTF32 on tcgen05.
-__global__ void __launch_bounds__(kThreadsG, 1)
+__global__ void __launch_bounds__(kThreadsG, 2)
     block_operator_tc_kernel(const float* __restrict__ plane, float* __restrict__ out, int h, int w,
-                             const float* __restrict__ r_hi, const float* __restrict__ r_lo, int nblocks) {
+                             const float* __restrict__ r_hi, const float* __restrict__ r_lo, int nblocks, int vec) {
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* a_hi = smem;                        // 128 x 64 f32 = 32 KB
     uint8_t* a_lo = smem + 32768;                // 32 KB
@@ -86,11 +86,21 @@ __global__ void __launch_bounds__(kThreadsG, 1)
     const int nbx = (w + 7) >> 3;
     const int ntiles = (nblocks + kTileM - 1) / kTileM;
 
-    // operator halves, K-major (row n of R = output pixel n, k = input pixel)
-    for (int e = tid; e < kN * kK; e += kThreadsG) {
-        int n = e / kK, k = e % kK;
-        *reinterpret_cast<float*>(b_hi + kmajor_off(n, k)) = r_hi[e];
-        *reinterpret_cast<float*>(b_lo + kmajor_off(n, k)) = r_lo[e];
+    // operator halves, K-major (row n of R = output pixel n, k = input pixel):
+    // every thread issues its 16 float4 loads before the first store (one round trip)
+    {
+        float4 vh[8], vl[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            vh[i] = __ldg(reinterpret_cast<const float4*>(r_hi) + tid + kThreadsG * i);
+            vl[i] = __ldg(reinterpret_cast<const float4*>(r_lo) + tid + kThreadsG * i);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int e = 4 * (tid + kThreadsG * i), n = e / kK, k = e % kK;
+            *reinterpret_cast<float4*>(b_hi + kmajor_off(n, k)) = vh[i];
+            *reinterpret_cast<float4*>(b_lo + kmajor_off(n, k)) = vl[i];
+        }
     }
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
@@ -108,19 +118,40 @@ __global__ void __launch_bounds__(kThreadsG, 1)
     uint32_t phase = 0;
 
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        // ---- stage the tile's blocks: A = f (block-major rows, 64 samples each), split hi/lo
-        for (int e = tid; e < kTileM * kK; e += kThreadsG) {
-            int m = e / kK, k = e % kK;
-            int b = tile * kTileM + m;
-            float v = 0.f;
+        // ---- stage the tile's blocks: A = f (row m = block tile*128 + m, 64 samples), split hi/lo.
+        // Thread m loads its own block (8 rows x 2 float4, all issued before use).
+        {
+            const int b = tile * kTileM + tid;
+            const int by = b / nbx, bx = b % nbx, y0 = by * 8, x0 = bx * 8;
+            float4 v[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] = make_float4(0.f, 0.f, 0.f, 0.f);
             if (b < nblocks) {
-                int by = b / nbx, bx = b % nbx;
-                int y = by * 8 + (k >> 3), x = bx * 8 + (k & 7);
-                if (y < h && x < w) v = __ldg(plane + (size_t)y * w + x);
+                if (vec && y0 + 8 <= h && x0 + 8 <= w) {
+#pragma unroll
+                    for (int r = 0; r < 8; ++r) {
+                        const float4* src = reinterpret_cast<const float4*>(plane + (size_t)(y0 + r) * w + x0);
+                        v[2 * r] = __ldg(src);
+                        v[2 * r + 1] = __ldg(src + 1);
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const int y = y0 + (j >> 1), x = x0 + (j & 1) * 4;
+                        float t[4] = {0.f, 0.f, 0.f, 0.f};
+                        for (int q = 0; q < 4; ++q)
+                            if (y < h && x + q < w) t[q] = __ldg(plane + (size_t)y * w + x + q);
+                        v[j] = make_float4(t[0], t[1], t[2], t[3]);
+                    }
+                }
             }
-            float hi = tf32_hi(v);
-            *reinterpret_cast<float*>(a_hi + kmajor_off(m, k)) = hi;
-            *reinterpret_cast<float*>(a_lo + kmajor_off(m, k)) = v - hi;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {  // samples k = 4j .. 4j+3 (row j/2 of the block)
+                const float4 hv = make_float4(tf32_hi(v[j].x), tf32_hi(v[j].y), tf32_hi(v[j].z), tf32_hi(v[j].w));
+                const float4 lv = make_float4(v[j].x - hv.x, v[j].y - hv.y, v[j].z - hv.z, v[j].w - hv.w);
+                *reinterpret_cast<float4*>(a_hi + kmajor_off(tid, 4 * j)) = hv;
+                *reinterpret_cast<float4*>(a_lo + kmajor_off(tid, 4 * j)) = lv;
+            }
         }
         asm volatile("fence.proxy.async.shared::cta;");  // generic-proxy smem writes -> tensor core
         __syncthreads();
@@ -168,11 +199,21 @@ __global__ void __launch_bounds__(kThreadsG, 1)
                 : "r"(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0));
             asm volatile("tcgen05.wait::ld.sync.aligned;");
             if (b < nblocks) {
+                if (vec && by * 8 + 8 <= h && bx * 8 + 8 <= w) {  // two block rows, 4 float4 stores
 #pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    int n = c0 + j;
-                    int y = by * 8 + (n >> 3), x = bx * 8 + (n & 7);
-                    if (y < h && x < w) out[(size_t)y * w + x] = __uint_as_float(v[j]);
+                    for (int j = 0; j < 16; j += 4) {
+                        const int n = c0 + j;
+                        float4* dst = reinterpret_cast<float4*>(out + (size_t)(by * 8 + (n >> 3)) * w + bx * 8 + (n & 7));
+                        *dst = make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]), __uint_as_float(v[j + 2]),
+                                           __uint_as_float(v[j + 3]));
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        int n = c0 + j;
+                        int y = by * 8 + (n >> 3), x = bx * 8 + (n & 7);
+                        if (y < h && x < w) out[(size_t)y * w + x] = __uint_as_float(v[j]);
+                    }
                 }
             }
         }
@@ -318,7 +359,11 @@ void launch_block_operator_tc(const float* plane, float* out, int h, int w, cons
         CUDA_CHECK(cudaFuncSetAttribute(block_operator_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
-    block_operator_tc_kernel<<<std::min(ntiles, num_sms), kThreadsG, smem, s>>>(plane, out, h, w, r_hi, r_lo, nblocks);
+    const int vec = (w % 4 == 0) && ((uintptr_t)plane % 16 == 0) && ((uintptr_t)out % 16 == 0);
+    // two CTAs per SM (96 KB smem, 64 TMEM columns each): one tile per CTA at 1080p, loads of one
+    // CTA overlap the MMA / epilogue of the other
+    block_operator_tc_kernel<<<std::min(ntiles, 2 * num_sms), kThreadsG, smem, s>>>(plane, out, h, w, r_hi, r_lo, nblocks,
+                                                                             vec);
     CUDA_CHECK(cudaGetLastError());
 }
 
