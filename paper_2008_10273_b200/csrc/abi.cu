@@ -386,6 +386,13 @@ int hivc_block_perblock(hivc_ctx* ctx, const float* plane, int32_t h, int32_t w,
         int st = 0;
         CUDA_CHECK(cudaMemcpyAsync(&st, C.d_status, sizeof(int), cudaMemcpyDeviceToHost, C.stream));
         CUDA_CHECK(cudaStreamSynchronize(C.stream));
+        if (st == 4) {  // a block has more than 16 points: the wide-system variant for all blocks
+            CUDA_CHECK(cudaMemsetAsync(C.d_status, 0, sizeof(int), C.stream));
+            hivc::launch_block_perblock(plane, out, h, w, masks, C.d_status, C.stream, true);
+            C.launches += 1;
+            CUDA_CHECK(cudaMemcpyAsync(&st, C.d_status, sizeof(int), cudaMemcpyDeviceToHost, C.stream));
+            CUDA_CHECK(cudaStreamSynchronize(C.stream));
+        }
         if (st == 1) hivc::fail(HIVC_E_PSEUDODIFF, "block mask needs at least one point");
         if (st == 2) hivc::fail(HIVC_E_PSEUDODIFF, "singular coefficient system");
     });

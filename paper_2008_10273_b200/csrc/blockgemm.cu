@@ -228,8 +228,12 @@ __global__ void __launch_bounds__(kThreadsG, 2)
 // (b) per-block masks: bordered solve in shared memory (float64), then
 // rec = G[:, pos] c + a (pseudodiff.py:218-240, 266-272), one warp per block.
 constexpr int kPbWarps = 4;
-constexpr int kPbLd = 66;
 
+// LD: row stride of the bordered system (K <= LD - 2).  The LD = 18 variant
+// (K <= 16: every block of a 5 % mask in practice) needs ~10 KB of shared
+// memory per CTA instead of ~140 KB, so 16 CTAs per SM run instead of one; a
+// block with more points flags status 4 and the host reruns with LD = 66.
+template <int LD>
 __global__ void __launch_bounds__(kPbWarps * 32)
     block_perblock_kernel(const float* __restrict__ plane, float* __restrict__ out, int h, int w,
                           const uint64_t* __restrict__ masks, int nblocks, int* status) {
@@ -237,9 +241,9 @@ __global__ void __launch_bounds__(kPbWarps * 32)
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int b = blockIdx.x * kPbWarps + wid;
     if (b >= nblocks) return;
-    double* M = sm + (size_t)wid * 65 * kPbLd;
-    double* fb = sm + (size_t)kPbWarps * 65 * kPbLd + wid * 64;
-    int* pos = reinterpret_cast<int*>(sm + (size_t)kPbWarps * (65 * kPbLd + 64)) + wid * 64;
+    double* M = sm + (size_t)wid * (LD - 1) * LD;
+    double* fb = sm + (size_t)kPbWarps * (LD - 1) * LD + wid * 64;
+    int* pos = reinterpret_cast<int*>(sm + (size_t)kPbWarps * ((LD - 1) * LD + 64)) + wid * 64;
     const int nbx = (w + 7) >> 3;
     const int by = b / nbx, bx = b % nbx;
     for (int k = lane; k < 64; k += 32) {
@@ -252,21 +256,25 @@ __global__ void __launch_bounds__(kPbWarps * 32)
         if (lane == 0) atomicExch(status, 1);
         return;
     }
+    if (K > LD - 2) {  // does not fit this variant
+        if (lane == 0) atomicExch(status, 4);
+        return;
+    }
     for (int j = lane; j < 64; j += 32)
         if ((mask >> j) & 1ull) pos[__popcll(mask & ((1ull << j) - 1ull))] = j;
     __syncwarp();
     const int N = K + 1;
     for (int e = lane; e < N * N; e += 32) {
         int i = e / N, j = e % N;
-        M[i * kPbLd + j] = (i < K && j < K) ? kGreens64[pos[i] * 64 + pos[j]] : ((i == K && j == K) ? 0.0 : 1.0);
+        M[i * LD + j] = (i < K && j < K) ? kGreens64[pos[i] * 64 + pos[j]] : ((i == K && j == K) ? 0.0 : 1.0);
     }
-    for (int i = lane; i < N; i += 32) M[i * kPbLd + N] = i < K ? fb[pos[i]] : 0.0;
+    for (int i = lane; i < N; i += 32) M[i * LD + N] = i < K ? fb[pos[i]] : 0.0;
     __syncwarp();
     for (int col = 0; col < N; ++col) {
         int piv = col;
         double best = -1.0;
         for (int i = col; i < N; ++i) {
-            double v = fabs(M[i * kPbLd + col]);
+            double v = fabs(M[i * LD + col]);
             if (v > best) {
                 best = v;
                 piv = i;
@@ -278,29 +286,29 @@ __global__ void __launch_bounds__(kPbWarps * 32)
         }
         if (piv != col)
             for (int j = lane; j <= N; j += 32) {
-                double t = M[col * kPbLd + j];
-                M[col * kPbLd + j] = M[piv * kPbLd + j];
-                M[piv * kPbLd + j] = t;
+                double t = M[col * LD + j];
+                M[col * LD + j] = M[piv * LD + j];
+                M[piv * LD + j] = t;
             }
         __syncwarp();
-        const double d = M[col * kPbLd + col];
+        const double d = M[col * LD + col];
         for (int i = col + 1; i < N; ++i) {
-            const double l = M[i * kPbLd + col] / d;
-            for (int j = col + 1 + lane; j <= N; j += 32) M[i * kPbLd + j] = M[i * kPbLd + j] - l * M[col * kPbLd + j];
+            const double l = M[i * LD + col] / d;
+            for (int j = col + 1 + lane; j <= N; j += 32) M[i * LD + j] = M[i * LD + j] - l * M[col * LD + j];
             __syncwarp();
         }
     }
     if (lane == 0)
         for (int i = N - 1; i >= 0; --i) {
-            double s = M[i * kPbLd + N];
-            for (int j = i + 1; j < N; ++j) s = s - M[i * kPbLd + j] * M[j * kPbLd + N];
-            M[i * kPbLd + N] = s / M[i * kPbLd + i];
+            double s = M[i * LD + N];
+            for (int j = i + 1; j < N; ++j) s = s - M[i * LD + j] * M[j * LD + N];
+            M[i * LD + N] = s / M[i * LD + i];
         }
     __syncwarp();
-    const double a = M[K * kPbLd + N];
+    const double a = M[K * LD + N];
     for (int n = lane; n < 64; n += 32) {
         double acc = 0.0;
-        for (int i = 0; i < K; ++i) acc = acc + kGreens64[n * 64 + pos[i]] * M[i * kPbLd + N];
+        for (int i = 0; i < K; ++i) acc = acc + kGreens64[n * 64 + pos[i]] * M[i * LD + N];
         int y = by * 8 + (n >> 3), x = bx * 8 + (n & 7);
         if (y < h && x < w) out[(size_t)y * w + x] = (float)(acc + a);
     }
@@ -368,16 +376,19 @@ void launch_block_operator_tc(const float* plane, float* out, int h, int w, cons
 }
 
 void launch_block_perblock(const float* plane, float* out, int h, int w, const uint64_t* masks, int* status,
-                           cudaStream_t s) {
+                           cudaStream_t s, bool wide) {
     const int nblocks = ((h + 7) / 8) * ((w + 7) / 8);
-    const size_t smem = (size_t)kPbWarps * (65 * kPbLd + 64) * sizeof(double) + kPbWarps * 64 * sizeof(int);
-    static bool attr = false;
-    if (!attr) {
-        CUDA_CHECK(cudaFuncSetAttribute(block_perblock_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
-    block_perblock_kernel<<<(nblocks + kPbWarps - 1) / kPbWarps, kPbWarps * 32, smem, s>>>(plane, out, h, w, masks,
-                                                                                              nblocks, status);
+    auto go = [&](auto kernel, int ld) {
+        const size_t smem =
+            (size_t)kPbWarps * ((ld - 1) * ld + 64) * sizeof(double) + kPbWarps * 64 * sizeof(int);
+        CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        kernel<<<(nblocks + kPbWarps - 1) / kPbWarps, kPbWarps * 32, smem, s>>>(plane, out, h, w, masks, nblocks,
+                                                                                  status);
+    };
+    if (wide)
+        go(block_perblock_kernel<66>, 66);
+    else
+        go(block_perblock_kernel<18>, 18);
     CUDA_CHECK(cudaGetLastError());
 }
 

@@ -17,6 +17,6 @@ void launch_block_operator_tc(const float* plane, float* out, int h, int w, cons
 
 // (b) per-block masks (device uint64 per block), float64 shared-memory solves.
 void launch_block_perblock(const float* plane, float* out, int h, int w, const uint64_t* masks, int* status,
-                           cudaStream_t s);
+                           cudaStream_t s, bool wide = false);
 
 }  // namespace hivc

@@ -75,3 +75,21 @@ def test_shared_mask_rejects_points_outside_edge_tiles():
 
     with pytest.raises(PseudodiffError):
         reconstruct_plane_shared_mask(np.zeros((20, 16), np.float32), FLAT_BLOCK_MASK)
+
+
+def test_per_block_masks_dense_blocks_use_wide_systems():
+    """Blocks with more than 16 points take the wide-system kernel variant."""
+    from paper_2008_10273_b200.pseudodiff import reconstruct_plane_masks
+
+    plane = _residual(32, 48, 4)
+    rng = np.random.default_rng(7)
+    tiles = 4 * 6
+    masks = rng.uniform(size=(tiles, 8, 8)) < 0.05
+    masks[3] = rng.uniform(size=(8, 8)) < 0.5  # ~32 points
+    masks[10] = rng.uniform(size=(8, 8)) < 0.35  # ~22 points
+    for i in range(tiles):
+        if not masks[i].any():
+            masks[i, rng.integers(0, 8), rng.integers(0, 8)] = True
+    ref = _oracle_plane(plane.astype(np.float64), masks)
+    got = reconstruct_plane_masks(plane, masks)
+    assert np.abs(got.astype(np.float64) - ref).max() < 1e-3
