@@ -112,44 +112,77 @@ class ClockSampler:
 # ----------------------------------------------------------------------------- CPU leg
 
 
-def gop_payloads(data):
-    from oracle import parse
-
-    return parse.read_container(data)[1]
+REF_DIR = REPO / "baseline" / "_ref"  # the unmodified reference, pip-installed by build() (git-ignored, travels)
 
 
-def _oracle_job(args):
-    data, gop = args
-    os.environ["OMP_NUM_THREADS"] = "1"
-    from oracle import decoder
-
-    # decode one GOP of one plane: rebuild a one-GOP stream (header frame count adjusted)
-    pay = gop_payloads(data)[gop]
+def one_gop_stream(data, gop):
+    """A valid one-GOP container holding GOP `gop` of `data` (header frame count adjusted)."""
+    off = 22  # header `<4sBHHIHHBBBBB`, frame_count at byte 9 (bitstream.py:58-129)
+    for _ in range(gop):
+        (ln,) = struct.unpack_from("<I", data, off)
+        off += 4 + ln
+    (ln,) = struct.unpack_from("<I", data, off)
+    pay = data[off + 4 : off + 4 + ln]
     (nf,) = struct.unpack_from("<H", pay, 0)
     head = bytearray(data[:22])
     struct.pack_into("<I", head, 9, nf)
-    one = bytes(head) + struct.pack("<I", len(pay)) + pay
+    return bytes(head) + struct.pack("<I", len(pay)) + pay
+
+
+def gop_count(data):
+    n, off = 0, 22
+    while off < len(data):
+        off += 4 + struct.unpack_from("<I", data, off)[0]
+        n += 1
+    return n
+
+
+def _reference_job(one):
+    """The unmodified reference decoder (hivc.codec.decode, codec.py:484-563) on one GOP."""
+    if str(REF_DIR) not in sys.path:
+        sys.path.insert(0, str(REF_DIR))
+    from hivc import codec as ref_codec
+
+    t0 = time.perf_counter()
+    frames = ref_codec.decode(one)
+    return time.perf_counter() - t0, len(frames)
+
+
+def _oracle_job(one):
+    """The oracle/ port (test infrastructure) on one GOP — reported beside the reference."""
+    from oracle import decoder
+
     t0 = time.perf_counter()
     frames = decoder.decode_stream(one)
     return time.perf_counter() - t0, len(frames)
 
 
+def reference_available():
+    return (REF_DIR / "hivc" / "codec.py").exists()
+
+
 def cpu_sample(streams, procs: int):
-    """The oracle port decoding GOP 0 of Y, Cb and Cr (12 frames), `procs` processes."""
-    jobs = [(s, 0) for s in streams]
+    """GOP 0 of Y, Cb and Cr (12 frames) on the host: the unmodified reference
+    decoder when baseline/_ref holds it, else the oracle port."""
+    kind = "reference" if reference_available() else "port"
+    job = _reference_job if kind == "reference" else _oracle_job
+    jobs = [one_gop_stream(s, 0) for s in streams]
+    _worker_init()
     t0 = time.perf_counter()
     if procs <= 1:
-        res = [_oracle_job(j) for j in jobs]
+        res = [job(j) for j in jobs]
     else:
         from multiprocessing import get_context
 
-        with get_context("fork").Pool(min(procs, len(jobs))) as pool:
-            res = pool.map(_oracle_job, jobs)
+        with get_context("fork").Pool(min(procs, len(jobs)), initializer=_worker_init) as pool:
+            res = pool.map(job, jobs)
     wall = time.perf_counter() - t0
-    return 12 / wall, wall, res
+    return 12 / wall, wall, res, kind
 
 
 def _worker_init():
+    os.environ["OMP_NUM_THREADS"] = "1"
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
     try:  # one BLAS thread per process: the pool itself supplies the parallelism
         from threadpoolctl import threadpool_limits
 
@@ -159,33 +192,45 @@ def _worker_init():
 
 
 def reference_arm(args, rank):
-    """The reference's CPU path (the oracle port, pinned to the reference decoder)
-    on this box's host cores: every step decodes the whole config-3 workload —
-    all 5 GOPs of the Y, Cb and Cr streams — as 15 independent (plane, GOP)
-    jobs on one process per core."""
+    """The reference's own CPU decoder on this box's host cores: every step
+    decodes the whole config-3 workload — all 5 GOPs of the Y, Cb and Cr
+    streams — as 15 independent (plane, GOP) one-GOP streams through the
+    UNMODIFIED reference package (`hivc.codec.decode`, pip-installed into
+    baseline/_ref by build()), one process per core.  The oracle port's time
+    for the same jobs is reported beside it (`port_value`)."""
     if rank != 0:
         return
     streams = load_streams()
     cores = os.cpu_count() or 1
-    ngops = len(gop_payloads(streams[0]))
-    jobs = [(s, g) for g in range(ngops) for s in streams]
+    jobs = [one_gop_stream(s, g) for g in range(gop_count(streams[0])) for s in streams]
     procs = max(1, min(cores, len(jobs)))
+    kind = "reference" if reference_available() else "port"
+    job = _reference_job if kind == "reference" else _oracle_job
     from multiprocessing import get_context
 
-    frames_per_step = 0
-    times = []
-    with get_context("fork").Pool(procs, initializer=_worker_init) as pool:
-        for i in range(args.warmup + args.steps):
-            t0 = time.perf_counter()
-            res = pool.map(_oracle_job, jobs, chunksize=1)
-            dt = time.perf_counter() - t0
-            frames_per_step = sum(n for _, n in res) // len(streams)  # 4:2:0 frames (Y+Cb+Cr)
-            if i >= args.warmup:
-                times.append(dt)
+    def run(fn, nsteps, warm):
+        times, frames = [], 0
+        with get_context("fork").Pool(procs, initializer=_worker_init) as pool:
+            for i in range(warm + nsteps):
+                t0 = time.perf_counter()
+                res = pool.map(fn, jobs, chunksize=1)
+                dt = time.perf_counter() - t0
+                frames = sum(n for _, n in res) // len(streams)  # 4:2:0 frames (Y+Cb+Cr)
+                if i >= warm:
+                    times.append(dt)
+        return frames, times
+
+    frames_per_step, times = run(job, args.steps, args.warmup)
     ms = 1e3 * statistics.median(times)
     value = frames_per_step / (ms / 1e3)
-    sample = (f"oracle/ numpy port of the reference decoder; the whole workload per step: {len(jobs)} (plane, GOP) "
-              f"jobs, {frames_per_step} frames, on {procs} processes ({cores} host cores)")
+    port = None
+    if kind == "reference" and not args.no_cpu:
+        pf, pt = run(_oracle_job, 1, 0)
+        port = pf / statistics.median(pt)
+    what = ("the unmodified reference decoder (hivc.codec.decode from baseline/_ref)" if kind == "reference"
+            else "oracle/ numpy port of the reference decoder (baseline/_ref missing)")
+    sample = (f"{what}; the whole workload per step: {len(jobs)} (plane, GOP) one-GOP streams, "
+              f"{frames_per_step} frames, on {procs} processes ({cores} host cores), 1 BLAS thread each")
     line = {
         "impl": "reference",
         "metric": METRIC,
@@ -201,9 +246,12 @@ def reference_arm(args, rank):
         "dtype": "f64",
         "data": "synthetic (seeded, SURVEY §8(d) recipe), reference-encoded bitstreams",
         "config": {"workload": WORKLOAD, "sample": sample},
-        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": procs, "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": procs, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if port is not None:
+        line["port_value"] = port
+        line["port_note"] = "oracle/ numpy port on the same jobs and processes (1 step), for comparison only"
     print(json.dumps(line), flush=True)
 
 
@@ -403,14 +451,16 @@ def main():
             traffic = json.loads(tf.read_text()).get("dram_bytes_per_launch")
         cpu = None
         if world == 1 and not args.no_cpu:
-            fps, wall, _ = cpu_sample(base, 1)
+            fps, wall, _, kind = cpu_sample(base, 1)
+            what = ("the unmodified reference decoder (hivc.codec.decode, baseline/_ref)" if kind == "reference"
+                    else "oracle/ numpy port of the reference decoder")
             cpu = {
                 "value": fps,
                 "unit": "frames/s",
                 "cores": 1,
-                "kind": "port",
-                "sample": f"oracle/ numpy port of the reference decoder, 1 process: GOP 0 (12 frames) of the Y, Cb "
-                          f"and Cr streams decoded sequentially in {wall:.1f} s",
+                "kind": kind,
+                "sample": f"{what}, 1 process, 1 BLAS thread: GOP 0 (12 frames) of the Y, Cb and Cr streams decoded "
+                          f"sequentially in {wall:.1f} s",
             }
         line = {
             "metric": METRIC,

@@ -206,9 +206,8 @@ def test_decode_config3_matches_reference_checksums(plane):
         dc = np.abs(a.sum(axis=0).astype(np.int64) - ref["col_sums"][i])
         assert dr.max() <= a.shape[1] and dc.max() <= a.shape[0]
         assert dr.sum() <= 64, f"frame {i}: {dr.sum()} grey levels of drift"
-    # all 60 frames of every plane are bit-identical today (tools/cfg3_exact.py); the
-    # tolerance (<= 1 grey level, north star) leaves room for dot-product order only
-    assert exact >= out.shape[0] - 3
+    # every frame of every plane is bit-identical to the reference decoder
+    assert exact == out.shape[0]
 
 
 # ---------------------------------------------------------------- Brox flow (encoder side)

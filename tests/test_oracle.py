@@ -141,3 +141,21 @@ def test_oracle_decodes_edge_size_streams():
         ref = g[f"{name}_frames"].astype(np.int32)
         got = np.stack([np.stack(f) for f in decoder.decode_stream(g[f"{name}_stream"].tobytes())])
         assert np.array_equal(got, ref), name
+
+
+def test_oracle_config1_channel0_matches_reference():
+    """Config 1 at its full size (1080p, 2 % mask, tol 1e-6, strict), channel 0:
+    the oracle against the reference's iterations and solution (make_bench_pins.py)."""
+    from conftest import GOLDEN
+
+    g = np.load(GOLDEN / "pin_cfg1.npz")
+    h, w = (int(x) for x in g["shape"])
+    f = np.zeros(h * w)
+    f[g["mask_idx"]] = g["vals0"].astype(np.float64)
+    m = np.zeros(h * w, bool)
+    m[g["mask_idx"]] = True
+    st = {}
+    u = inpaint.solve(f.reshape(h, w), m.reshape(h, w), tol=1e-6, max_iter=10000, strict=True, stats=st)
+    assert np.array_equal(np.array(st["level_iterations"]), g["iters0"])
+    assert np.abs(u[::8, ::4] - g["u0_grid"]).max() <= 1e-9
+    assert np.abs(u.sum(axis=1) - g["u0_rows"]).max() <= 1e-9 * w
