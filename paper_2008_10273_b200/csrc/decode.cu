@@ -11,7 +11,6 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
-#include <condition_variable>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -102,6 +101,41 @@ void parse_gop(const uint8_t* p, size_t n, const StreamHeader& hd, int gi, std::
     jobs.resize(cur.nframes);
     for (int fi = 0; fi < cur.nframes; ++fi) cur.parse(jobs[fi], ht, bits);
     cur.finish();
+}
+
+// Frame-record layout of one GOP payload (codec.py:494-556; record =
+// [u8 type][u32 pred_len][pred][u32 res_len][res]), found from the length
+// fields alone: rec[i] = start of record i for every record that fits, plus
+// the start of the first one that does not.  `complete` records fit
+// structurally (<= the u16 frame count); `end` follows the last of them.
+// Output buffers are sized by `complete`, never by the unchecked count, and
+// the records can be parsed in parallel (each from its own start).
+struct GopLayout {
+    int nframes = 0, complete = 0;
+    size_t end = 2;
+    std::vector<size_t> rec;
+};
+
+void scan_gop(const uint8_t* p, size_t n, GopLayout& L) {
+    L.rec.clear();
+    L.nframes = L.complete = 0;
+    L.end = 2;
+    if (n < 2) return;
+    uint16_t nf;
+    std::memcpy(&nf, p, 2);
+    L.nframes = nf;
+    size_t pos = 2;
+    for (int fi = 0; fi < nf; ++fi) {
+        L.rec.push_back(pos);
+        if (pos + 5 > n) break;
+        const uint64_t q = (uint64_t)pos + 5 + rd_u32(p + pos + 1);
+        if (q + 4 > n) break;
+        const uint64_t e = q + 4 + rd_u32(p + q);
+        if (e > n) break;
+        pos = (size_t)e;
+        L.complete = fi + 1;
+        L.end = pos;
+    }
 }
 
 // Bump allocator over the pinned staging buffer.
@@ -318,11 +352,13 @@ void gop_frame_counts(const uint8_t* data, size_t len, std::vector<int32_t>& cou
     std::vector<std::pair<size_t, size_t>> gops;
     split_gops(data, len, hd, gops);
     counts.resize(gops.size());
+    GopLayout lay;
     for (size_t g = 0; g < gops.size(); ++g) {
         if (gops[g].second < 2) fail(HIVC_E_TRUNCATED, "group " + std::to_string(g) + " payload too small");
-        uint16_t nf;
-        std::memcpy(&nf, data + gops[g].first, 2);
-        counts[g] = nf;
+        // frames whose records fit (= the u16 count on a valid stream): a corrupt
+        // count cannot size the output beyond the frames the payload can hold
+        scan_gop(data + gops[g].first, gops[g].second, lay);
+        counts[g] = lay.complete;
     }
 }
 
@@ -368,12 +404,21 @@ double drain(EvPairs& v, cudaEvent_t origin, char kind, int lane, std::string* t
     return t;
 }
 
-// One (stream, GOP) of a decode call.
+// One (stream, GOP) of a decode call.  Its frame records are parsed by any
+// pool thread (frame 0 in the intra phase, every later record as its own
+// task); frames are launched on the item's stream strictly in order by
+// whichever thread completes the parsed prefix (try_launch, under `mu`).
 struct Item {
     int stream = 0, gop = 0, group = 0;
     Slot* slot = nullptr;
-    std::unique_ptr<GopCursor> cur;
+    GopLayout lay;
     int nf = 0;
+    std::unique_ptr<std::mutex> mu;  // launch state, errors, host times
+    std::vector<uint8_t> parsed;     // per frame: record parsed (under mu)
+    int next_launch = 1;             // next P frame to launch (under mu)
+    bool head_done = false;          // I-frame finalize + frame 0 copy queued (under mu)
+    bool finished = false;           // every frame launched, `done` recorded (under mu)
+    int err_frame = 1 << 30;         // frame of the recorded error (the earliest wins)
     const double* qtab = nullptr;  // device dequantisation table (ResDev::qtab), shipped with frame 0
     FrameArgs a0;  // I-frame finalize (frame 0)
     uint8_t* gop_dev = nullptr;
@@ -385,7 +430,7 @@ struct Item {
     int64_t h2d = 0, d2h = 0, inter_frames = 0, intra_frames = 0;
     EvPairs ev_inter, ev_intra, ev_ifin;
     cudaEvent_t done = nullptr;
-    bool issued = false;  // its batch is queued (under Shared::mu)
+    bool issued = false;  // its I-frame solve is queued (under mu)
     double h_i0 = 0, h_i1 = 0, h_issue = 0, h_p0 = 0, h_p1 = 0;  // host timeline (HIVC_TIMELINE)
 };
 
@@ -401,15 +446,14 @@ struct Group {
     std::vector<int> ready;  // parsed, not yet issued (under mu)
 };
 
-struct Shared {
-    std::mutex mu;
-    std::condition_variable cv;
-};
-
-void fail_item(Item& it, int code, const std::string& msg) {
-    if (it.code == HIVC_OK) {
+// Record an error of frame fi; the reference decodes in order, so the
+// earliest failing frame's error is the one it raises.
+void fail_item(Item& it, int code, const std::string& msg, int fi = 0) {
+    std::lock_guard<std::mutex> lk(*it.mu);
+    if (it.code == HIVC_OK || fi < it.err_frame) {
         it.code = code;
         it.msg = msg;
+        it.err_frame = fi;
     }
 }
 
@@ -505,7 +549,6 @@ struct CallState {
     std::vector<StreamJob>& streams;
     std::vector<Item>& items;
     std::deque<Group>& groups;
-    Shared& sh;
     bool out_on_device;  // frames written straight into `out` (out_mode 1)
     bool timed;
     cudaEvent_t origin;
@@ -588,6 +631,90 @@ void finalize_intra(CallState& cs, Item& it, const FrameArgs& A, int frame) {
     }
 }
 
+// The item's last frame is queued: its device span ends there (and, with
+// host output, with its last D2H copy).  Callers hold it.mu or run alone.
+void finish_item(CallState& cs, Item& it) {
+    Slot& L = *it.slot;
+    if (!cs.out_on_device) {
+        cudaEventRecord(L.out_free, L.copy);
+        cudaStreamWaitEvent(L.stream, L.out_free, 0);
+    }
+    cudaEventRecord(it.done, L.stream);
+    it.finished = true;
+    it.h_p1 = now_s() - cs.t0;
+}
+
+// Queue everything of the item that can go now, in frame order: the I-frame
+// finalize once its solve is issued, then every parsed P frame of the
+// unbroken prefix (one staged upload, kernel and copy-out each).
+void try_launch(CallState& cs, Item& it) {
+    std::lock_guard<std::mutex> lk(*it.mu);
+    if (!it.issued || it.finished) return;
+    const StreamHeader& hd = cs.streams[it.stream].hd;
+    Slot& L = *it.slot;
+    const size_t frame_bytes = (size_t)hd.height * hd.width * hd.channels;
+    int fi = 0;
+    try {
+        CUDA_CHECK(cudaSetDevice(L.device));
+        if (it.nf > 0 && it.err_frame > 0 && !it.head_done) {
+            finalize_intra(cs, it, it.a0, 0);
+            copy_out(cs, L, it, 0, frame_bytes);
+            it.head_done = true;
+        }
+        while (it.next_launch < it.nf && it.parsed[it.next_launch] && it.next_launch < it.err_frame) {
+            fi = it.next_launch;
+            FrameOffsets o[1];
+            const uint8_t* dev = stage_chunk(L, it, (size_t)fi, 1, o);
+            const FrameJob& J = L.jobs[fi];
+            FrameArgs A = frame_args(L, hd, it, (size_t)fi, o[0], dev);
+            EvRec e;
+            e.stream = it.stream;
+            e.gop = it.gop;
+            e.frame = fi;
+            if (cs.timed) {
+                CUDA_CHECK(cudaEventCreate(&e.first));
+                CUDA_CHECK(cudaEventCreate(&e.second));
+                CUDA_CHECK(cudaEventRecord(e.first, L.stream));
+            }
+            if (J.type == 0) {
+                // an intra frame inside the GOP: solved alone on the solver stream
+                scatter_intra(cs.ctx, L, hd, J, o[0], dev);
+                CUDA_CHECK(cudaEventRecord(L.intra_ready, L.stream));
+                {
+                    std::lock_guard<std::mutex> sl(cs.ctx.solver_mu);
+                    issue_solves(cs, std::vector<int>{(int)(&it - cs.items.data())}, hd);
+                }
+                finalize_intra(cs, it, A, fi);
+                it.intra_frames += 1;
+            } else {
+                launch_frame(A, true, L.stream);
+                cs.ctx.launches += 1;
+                it.inter_frames += 1;
+            }
+            if (cs.timed) {
+                CUDA_CHECK(cudaEventRecord(e.second, L.stream));
+                it.ev_inter.push_back(e);
+            }
+            copy_out(cs, L, it, (size_t)fi, frame_bytes);
+            ++it.next_launch;
+        }
+        if (it.next_launch >= it.nf && it.code == HIVC_OK) finish_item(cs, it);
+    } catch (const Error& e) {
+        if (it.code == HIVC_OK || fi < it.err_frame) it.code = e.code, it.msg = e.what(), it.err_frame = fi;
+    } catch (const std::exception& e) {
+        if (it.code == HIVC_OK || fi < it.err_frame) it.code = HIVC_E_ARGUMENT, it.msg = e.what(), it.err_frame = fi;
+    }
+}
+
+// A cursor over the item's GOP payload positioned at record fi.
+GopCursor cursor_at(CallState& cs, const Item& it, int fi) {
+    const StreamJob& S = cs.streams[it.stream];
+    GopCursor cur(S.data + S.gops[it.gop].first, S.gops[it.gop].second, S.hd, it.gop);
+    cur.pos = it.lay.rec[fi];
+    cur.next = fi;
+    return cur;
+}
+
 // Phase 1 of an item: parse + ship its I-frame, scatter the mask values; the
 // last item of a shape group issues the group's batched solves.
 void intra_phase(CallState& cs, Item& it) {
@@ -605,12 +732,14 @@ void intra_phase(CallState& cs, Item& it) {
         it.gop_dev = cs.out_on_device ? S.out + S.frame_base[it.gop] * frame_bytes : L.gop_out;
         it.gop_host = cs.out_on_device ? nullptr : S.out + S.frame_base[it.gop] * frame_bytes;
         if (!cs.out_on_device) CUDA_CHECK(cudaStreamWaitEvent(L.stream, L.out_free, 0));  // last call's copies
-        it.cur = std::make_unique<GopCursor>(S.data + S.gops[it.gop].first, S.gops[it.gop].second, hd, it.gop);
-        it.nf = it.cur->nframes;
-        if ((int)it.slot->jobs.size() < it.nf) it.slot->jobs.resize(it.nf);
+        if (S.gops[it.gop].second < 2) fail(HIVC_E_TRUNCATED, "group " + std::to_string(it.gop) + " payload too small");
         if (it.nf > 0) {
-            it.cur->parse(it.slot->jobs[0], it.ht, bits);  // frame 0 must be intra (codec.py:503)
-            if (it.nf == 1) it.cur->finish();
+            GopCursor cur = cursor_at(cs, it, 0);
+            HostTimes ht;
+            cur.parse(L.jobs[0], ht, bits);  // frame 0 must be intra (codec.py:503)
+            if (it.nf == 1) cur.finish();
+            it.ht.intra_parse += ht.intra_parse;
+            it.ht.residual_parse += ht.residual_parse;
             FrameOffsets o[1];
             std::vector<double> qt(255);  // s * dz_step / 127 for |s| <= 127 (quantize.py:43-47, codec.py:316-321)
             const double dz = 127.0 / (double)((hd.residual_levels - 1) / 2);
@@ -618,26 +747,25 @@ void intra_phase(CallState& cs, Item& it) {
             size_t qoff = 0;
             const uint8_t* dev = stage_chunk(L, it, 0, 1, o, &qt, &qoff);
             it.qtab = reinterpret_cast<const double*>(dev + qoff);
-            scatter_intra(cs.ctx, L, hd, it.slot->jobs[0], o[0], dev);
+            scatter_intra(cs.ctx, L, hd, L.jobs[0], o[0], dev);
             CUDA_CHECK(cudaEventRecord(L.intra_ready, L.stream));
             it.a0 = frame_args(L, hd, it, 0, o[0], dev);
             it.intra_frames += 1;
             it.solve0 = true;
         } else {
-            it.cur->finish();
+            GopCursor(S.data + S.gops[it.gop].first, S.gops[it.gop].second, hd, it.gop).finish();
         }
     } catch (const Error& e) {
-        fail_item(it, e.code, e.what());
+        fail_item(it, e.code, e.what(), 0);
     } catch (const std::exception& e) {
-        fail_item(it, HIVC_E_ARGUMENT, e.what());
+        fail_item(it, HIVC_E_ARGUMENT, e.what(), 0);
     }
     it.h_i1 = now_s() - cs.t0;
     Group& g = cs.groups[it.group];
-    std::vector<int> batch, done_items;
+    std::vector<int> batch;
     {
         std::lock_guard<std::mutex> lk(g.mu);
         const int self = (int)(&it - cs.items.data());
-        done_items.push_back(self);
         if (it.code == HIVC_OK && it.solve0) g.ready.push_back(self);
         --g.pending;
         static const int min_batch = [] {
@@ -655,94 +783,57 @@ void intra_phase(CallState& cs, Item& it) {
             CUDA_CHECK(cudaSetDevice(cs.ctx.device));
             issue_solves(cs, batch, hd);
         } catch (const Error& e) {
-            for (int i : batch) fail_item(cs.items[i], e.code, e.what());
+            for (int i : batch) fail_item(cs.items[i], e.code, e.what(), 0);
         } catch (const std::exception& e) {
-            for (int i : batch) fail_item(cs.items[i], HIVC_E_ARGUMENT, e.what());
+            for (int i : batch) fail_item(cs.items[i], HIVC_E_ARGUMENT, e.what(), 0);
         }
     }
-    {  // the failed / empty item itself and the batch are now final for their inter phases
-        std::lock_guard<std::mutex> lk(cs.sh.mu);
-        for (int i : batch) cs.items[i].issued = true;
-        if (!(it.code == HIVC_OK && it.solve0) || it.nf == 0) it.issued = true;
+    // the batch (and a failed / empty item itself) may now launch their frames
+    auto release = [&](Item& x) {
+        {
+            std::lock_guard<std::mutex> lk(*x.mu);
+            x.issued = true;
+        }
+        try_launch(cs, x);
+    };
+    for (int i : batch) release(cs.items[i]);
+    bool solo;  // not waiting for a solve (failed, or no frames)
+    {
+        std::lock_guard<std::mutex> lk(*it.mu);
+        solo = !(it.err_frame > 0 && it.solve0) || it.nf == 0;
     }
-    cs.sh.cv.notify_all();
+    if (solo) release(it);
 }
 
-// Phase 2 of an item: after its group's solves are queued, parse and run the
-// P frames (chunks of kChunk) on the slot stream; host output copies each
-// finished frame out on the copy stream.
-void inter_phase(CallState& cs, Item& it) {
-    std::vector<uint64_t>& bits = it.slot->bits;
-    const StreamJob& S = cs.streams[it.stream];
-    const StreamHeader& hd = S.hd;
-    Slot& L = *it.slot;
-    const size_t frame_bytes = (size_t)hd.height * hd.width * hd.channels;
+// Phase 2, one task per later frame record: parse it (bit-exact host C++),
+// then launch whatever prefix of the item is ready.
+void frame_task(CallState& cs, Item& it, int fi) {
     {
-        std::unique_lock<std::mutex> lk(cs.sh.mu);
-        cs.sh.cv.wait(lk, [&] { return it.issued; });
+        std::lock_guard<std::mutex> lk(*it.mu);
+        if (it.code != HIVC_OK && it.err_frame <= fi) return;  // an earlier frame failed: the reference stops there
+        if (it.h_p0 == 0) it.h_p0 = now_s() - cs.t0;
     }
-    it.h_p0 = now_s() - cs.t0;
+    HostTimes ht;
     try {
-        CUDA_CHECK(cudaSetDevice(L.device));
-        if (it.code != HIVC_OK) throw Error(it.code, it.msg);
-        if (it.nf > 0) {
-            finalize_intra(cs, it, it.a0, 0);
-            copy_out(cs, L, it, 0, frame_bytes);
-        }
-        constexpr int kChunk = 2;
-        FrameOffsets offs[kChunk];
-        size_t fi = 1;
-        while ((int)fi < it.nf) {
-            const int cnt = std::min(kChunk, it.nf - (int)fi);
-            for (int k = 0; k < cnt; ++k) it.cur->parse(it.slot->jobs[fi + k], it.ht, bits);
-            if ((int)fi + cnt == it.nf) it.cur->finish();
-            const uint8_t* dev = stage_chunk(L, it, fi, cnt, offs);
-            for (int k = 0; k < cnt; ++k, ++fi) {
-                const FrameJob& J = it.slot->jobs[fi];
-                FrameArgs A = frame_args(L, hd, it, fi, offs[k], dev);
-                EvRec e;
-                e.stream = it.stream;
-                e.gop = it.gop;
-                e.frame = (int)fi;
-                if (cs.timed) {
-                    CUDA_CHECK(cudaEventCreate(&e.first));
-                    CUDA_CHECK(cudaEventCreate(&e.second));
-                    CUDA_CHECK(cudaEventRecord(e.first, L.stream));
-                }
-                if (J.type == 0) {
-                    // an intra frame inside the GOP: solve it alone on the solver stream
-                    scatter_intra(cs.ctx, L, hd, J, offs[k], dev);
-                    CUDA_CHECK(cudaEventRecord(L.intra_ready, L.stream));
-                    {
-                        std::lock_guard<std::mutex> lk(cs.ctx.solver_mu);
-                        issue_solves(cs, std::vector<int>{(int)(&it - cs.items.data())}, hd);
-                    }
-                    finalize_intra(cs, it, A, (int)fi);
-                    it.intra_frames += 1;
-                } else {
-                    launch_frame(A, true, L.stream);
-                    cs.ctx.launches += 1;
-                    it.inter_frames += 1;
-                }
-                if (cs.timed) {
-                    CUDA_CHECK(cudaEventRecord(e.second, L.stream));
-                    it.ev_inter.push_back(e);
-                }
-                copy_out(cs, L, it, fi, frame_bytes);
-            }
-        }
+        GopCursor cur = cursor_at(cs, it, fi);
+        std::vector<uint64_t> bits;  // (an intra record inside the GOP)
+        cur.parse(it.slot->jobs[fi], ht, bits);
+        if (fi == it.nf - 1) cur.finish();
     } catch (const Error& e) {
-        fail_item(it, e.code, e.what());
+        fail_item(it, e.code, e.what(), fi);
+        return;
     } catch (const std::exception& e) {
-        fail_item(it, HIVC_E_ARGUMENT, e.what());
+        fail_item(it, HIVC_E_ARGUMENT, e.what(), fi);
+        return;
     }
-    // the item's device span ends with its last frame (and its last D2H copy)
-    if (!cs.out_on_device) {
-        cudaEventRecord(L.out_free, L.copy);
-        cudaStreamWaitEvent(L.stream, L.out_free, 0);
+    {
+        std::lock_guard<std::mutex> lk(*it.mu);
+        it.parsed[fi] = 1;
+        it.ht.intra_parse += ht.intra_parse;
+        it.ht.flow_parse += ht.flow_parse;
+        it.ht.residual_parse += ht.residual_parse;
     }
-    cudaEventRecord(it.done, L.stream);
-    it.h_p1 = now_s() - cs.t0;
+    try_launch(cs, it);
 }
 
 }  // namespace
@@ -771,13 +862,16 @@ void decode_streams(Context& ctx, int nstreams, const uint8_t* const* data, cons
         const size_t frame_bytes = (size_t)S.hd.height * S.hd.width * S.hd.channels;
         for (int g = S.gop_begin; g < S.gop_end; ++g) {
             S.frame_base[g] = acc;
-            uint16_t nf = 0;
-            if (S.gops[g].second >= 2) std::memcpy(&nf, S.data + S.gops[g].first, 2);
-            acc += nf;
-            max_gop_bytes = std::max(max_gop_bytes, nf * frame_bytes);
             Item it;
             it.stream = k;
             it.gop = g;
+            scan_gop(S.data + S.gops[g].first, S.gops[g].second, it.lay);
+            it.nf = it.lay.nframes;
+            // outputs hold the frames whose records fit (gop_frame_counts): a
+            // corrupt count fails in stream order instead of sizing buffers
+            acc += (size_t)it.lay.complete;
+            max_gop_bytes = std::max(max_gop_bytes, (size_t)it.lay.complete * frame_bytes);
+            it.mu = std::make_unique<std::mutex>();
             items.push_back(std::move(it));
         }
         max_h = std::max(max_h, S.hd.height);
@@ -823,6 +917,9 @@ void decode_streams(Context& ctx, int nstreams, const uint8_t* const* data, cons
         L.stage_begin_call((size_t)4 * max_h * max_w * max_c + 65536);
         items[i].slot = &L;
         CUDA_CHECK(cudaEventCreate(&items[i].done));
+        const size_t nrec = items[i].lay.rec.size();
+        if (L.jobs.size() < nrec) L.jobs.resize(nrec);
+        items[i].parsed.assign(std::max<size_t>(nrec, 1), 0);
     }
     const bool timed = (stage_seconds != nullptr && ctx.stage_events) || std::getenv("HIVC_TIMELINE");
     cudaEvent_t origin;
@@ -830,25 +927,35 @@ void decode_streams(Context& ctx, int nstreams, const uint8_t* const* data, cons
     CUDA_CHECK(cudaEventRecord(origin, ctx.stream));
     CUDA_CHECK(cudaStreamWaitEvent(ctx.solver, origin, 0));
     for (cudaStream_t p : ctx.pre) CUDA_CHECK(cudaStreamWaitEvent(p, origin, 0));
-    Shared sh;
-    CallState cs{ctx, streams, items, groups, sh, out_on_device, timed, origin, now_s(), out_mode};
-    // task queue: every item's intra phase, then the inter phases, both in
-    // batch-issue order.  A pool thread that reaches the inter phases drops
-    // its scheduling priority: P-frame parsing has slack (its GPU work queues
-    // behind the batched solves) while the large I-frames being parsed on the
-    // other threads gate the next batch.
+    CallState cs{ctx, streams, items, groups, out_on_device, timed, origin, now_s(), out_mode};
+    // task list: every item's intra phase (in batch-issue order), then one task
+    // per later frame record, item by item.  Frame records parse independently
+    // (each from its own start, GopLayout), so a GOP's P frames are parsed by
+    // several threads and are all ready when its I-frame solve completes; a
+    // pool thread that reaches the frame tasks drops its scheduling priority
+    // (the large I-frames still being parsed gate the next solve batch).
+    std::vector<std::pair<int, int>> tasks;
+    for (int i = 0; i < n; ++i) tasks.push_back({i, 0});
+    for (int i = 0; i < n; ++i) {
+        // records 1..complete-1 fit; record `complete` (when short of nf) is parsed
+        // too, so the error is the one its own parse meets first
+        const int last = std::min(items[i].nf - 1, items[i].lay.complete);
+        for (int fi = 1; fi <= last; ++fi) tasks.push_back({i, fi});
+    }
+    const int ntasks = (int)tasks.size();
     std::atomic<int> next_task{0};
     auto worker = [&](bool pool) {
         bool low = false;
-        for (int t; (t = next_task.fetch_add(1)) < 2 * n;) {
-            if (t < n) {
-                intra_phase(cs, items[t]);
+        for (int t; (t = next_task.fetch_add(1)) < ntasks;) {
+            const auto [i, fi] = tasks[t];
+            if (fi == 0) {
+                intra_phase(cs, items[i]);
             } else {
                 if (pool && !low) {
                     setpriority(PRIO_PROCESS, (id_t)syscall(SYS_gettid), 10);
                     low = true;
                 }
-                inter_phase(cs, items[t - n]);
+                frame_task(cs, items[i], fi);
             }
         }
     };
@@ -859,7 +966,7 @@ void decode_streams(Context& ctx, int nstreams, const uint8_t* const* data, cons
         // and value helper threads (measured on 16 cores: 8 workers beat 16 by 3 %)
         return e ? std::max(1, std::min(64, std::atoi(e))) : std::max(2, std::min(hw / 2, 32));
     }();
-    const int nworkers = std::max(1, std::min(n, kMaxWorkers));
+    const int nworkers = std::max(1, std::min(ntasks, kMaxWorkers));
     if (nworkers == 1 || n == 0) {
         worker(false);
     } else {
@@ -867,6 +974,9 @@ void decode_streams(Context& ctx, int nstreams, const uint8_t* const* data, cons
         for (int l = 0; l < nworkers; ++l) th.emplace_back(worker, true);
         for (auto& t : th) t.join();
     }
+    // items that stopped early (an error) end here
+    for (auto& it : items)
+        if (!it.finished) finish_item(cs, it);
     double span = 0;
     for (auto& it : items) {
         cudaStreamSynchronize(it.slot->stream);

@@ -64,21 +64,60 @@ void FseTable::build(const std::vector<uint64_t>& counts, int tl) {  // entropy.
     }
     if (total != size) fail(HIVC_E_ENTROPY, "normalized counts must sum to table size");
     const uint32_t step = (size >> 1) + (size >> 3) + 3;
-    sym.assign(size, 0);
-    x.assign(size, 0);
-    nb.assign(size, 0);
+    std::vector<uint16_t> sym(size, 0);
     uint32_t k = 0;
     for (size_t s = 0; s < counts.size(); ++s)
         for (uint64_t j = 0; j < counts[s]; ++j) sym[(k++ * step) & (size - 1)] = (uint16_t)s;
     std::vector<uint32_t> next(counts.size());
     for (size_t s = 0; s < counts.size(); ++s) next[s] = (uint32_t)counts[s];
+    dec.resize(size);
     for (uint32_t slot = 0; slot < size; ++slot) {
-        uint32_t xv = next[sym[slot]]++;
-        x[slot] = xv;
-        int bl = 32 - __builtin_clz(xv);  // xv >= 1
-        nb[slot] = (uint8_t)(tl + 1 - bl);
+        const uint32_t xv = next[sym[slot]]++;
+        const int bl = 32 - __builtin_clz(xv);  // xv >= 1
+        const int nb = tl + 1 - bl;             // 0 <= nb <= tl
+        dec[slot] = {xv << nb, sym[slot], (uint8_t)nb};
     }
 }
+
+namespace {
+// MSB-first reader for the hot entropy loops: a 64-bit window refilled eight
+// bytes at a time, no per-read limit check (reads past the data see zeros);
+// the caller compares the consumed bit count with the limit once, which
+// raises the same error a bit-by-bit reader would (fse_decode's loop has no
+// other failure, entropy.py:175-211).
+struct FastBits {
+    const uint8_t* d;
+    size_t nbytes, next = 0;
+    uint64_t buf = 0;
+    int avail = 0;
+    FastBits(const uint8_t* p, size_t n) : d(p), nbytes(n) { refill(); }
+    inline void refill() {
+        if (avail > 56) return;
+        if (next + 8 <= nbytes) {
+            uint64_t v;
+            std::memcpy(&v, d + next, 8);
+            v = __builtin_bswap64(v);
+            buf |= v >> avail;  // the partial byte below the whole ones is re-ORed identically next time
+            const int nb = (63 - avail) >> 3;
+            next += (size_t)nb;
+            avail += nb * 8;
+        } else {
+            while (avail <= 56) {
+                const uint64_t b = next < nbytes ? d[next] : 0;
+                buf |= b << (56 - avail);
+                ++next;
+                avail += 8;
+            }
+        }
+    }
+    inline uint32_t take(int n) {  // 0 <= n <= 32, avail >= n
+        const uint32_t v = n ? (uint32_t)(buf >> (64 - n)) : 0u;
+        buf <<= n;
+        avail -= n;
+        return v;
+    }
+};
+}  // namespace
 
 size_t decode_symbols(const uint8_t* d, size_t len, size_t pos, std::vector<int32_t>& out) {
     // header: entropy.py:227-240
@@ -104,48 +143,99 @@ size_t decode_symbols(const uint8_t* d, size_t len, size_t pos, std::vector<int3
     if (count) {  // fse_decode, entropy.py:175-211
         const uint32_t size = 1u << tl;
         if (state < size || state >= 2 * size) fail(HIVC_E_ENTROPY, "corrupt stream: initial state out of range");
-        BitReader rd(d + pos, nbytes, bit_len);
-        const uint16_t* sym = t.sym.data();
-        const uint32_t* xs = t.x.data();
-        const uint8_t* nbs = t.nb.data();
+        FastBits rd(d + pos, nbytes);
+        const FseTable::Entry* tab = t.dec.data();
+        int32_t* o = out.data();
+        uint64_t used = 0;
         for (uint32_t i = 0; i < count; ++i) {
-            uint32_t slot = state - size;
-            out[i] = sym[slot];
-            int nb = nbs[slot];
-            state = nb ? ((xs[slot] << nb) | rd.take(nb)) : xs[slot];
+            const FseTable::Entry e = tab[state - size];
+            o[i] = e.sym;
+            if (rd.avail < 12) rd.refill();  // nb <= table_log <= 12
+            state = e.base + rd.take(e.nb);
+            used += e.nb;
         }
+        if (used > bit_len) fail(HIVC_E_TRUNCATED_STREAM, "bit stream exhausted");
         if (state != size) fail(HIVC_E_ENTROPY, "corrupt stream: final state mismatch");
     }
     return pos + nbytes;
 }
 
 size_t decode_signed_values(const uint8_t* d, size_t len, size_t pos, std::vector<int32_t>& out) {
-    std::vector<int32_t> cats;  // entropy.py:311-338
-    pos = decode_symbols(d, len, pos, cats);
+    // entropy.py:311-338: the category symbols, then the raw extra bits
+    pos = decode_symbols(d, len, pos, out);
     if (pos + 4 > len) fail(HIVC_E_TRUNCATED_STREAM, "entropy payload truncated");
     uint32_t bit_len = rd_u32(d + pos);
     pos += 4;
     size_t nbytes = ((size_t)bit_len + 7) / 8;
     if (pos + nbytes > len) fail(HIVC_E_TRUNCATED_STREAM, "entropy payload truncated");
     uint64_t sum = 0;
-    for (int32_t c : cats) {
-        if (c > 16) fail(HIVC_E_ENTROPY, "bad category in stream");
+    bool bad = false;
+    for (int32_t c : out) {
+        bad |= c > 16;
         sum += (uint64_t)c;
     }
+    if (bad) fail(HIVC_E_ENTROPY, "bad category in stream");
     if (sum != bit_len) fail(HIVC_E_ENTROPY, "extra-bits length mismatch");
-    BitReader rd(d + pos, nbytes, bit_len);
-    out.resize(cats.size());
-    for (size_t i = 0; i < cats.size(); ++i) {
-        int k = cats[i];
-        if (!k) {
-            out[i] = 0;
-            continue;
-        }
-        int32_t e = (int32_t)rd.take(k);
-        out[i] = e >= (1 << (k - 1)) ? e : e - (1 << k) + 1;  // from_category, entropy.py:52-60
+    FastBits rd(d + pos, nbytes);
+    for (int32_t& v : out) {  // category -> value in place (from_category, entropy.py:52-60)
+        const int k = v;
+        if (rd.avail < 16) rd.refill();
+        const int32_t e = (int32_t)rd.take(k);
+        v = k == 0 ? 0 : (e >= (1 << (k - 1)) ? e : e - (1 << k) + 1);
     }
     return pos + nbytes;
 }
+
+// Residual block trees of full 8x8 tiles (codec.py:300-303, subdivision.py:
+// 198-222) decoded by table: for every 12-bit look-ahead, the mask of the tree
+// it starts with and the tree's bit count, when the tree ends within those 12
+// bits and never splits a single pixel (nbits 0 otherwise: the bit-by-bit walk
+// handles it, and raises the reference's error when there is one).  A K = 4
+// tree is 7 bits.
+static const struct BlockTreeLut {
+    uint64_t mask[4096];
+    uint8_t nbits[4096];
+    BlockTreeLut() {
+        for (uint32_t v = 0; v < 4096; ++v) {
+            int32_t st[4 * 32];
+            int sp = 1, used = 0;
+            st[0] = 0, st[1] = 0, st[2] = 8, st[3] = 8;
+            uint64_t m = 0;
+            bool ok = true;
+            while (sp && ok) {
+                --sp;
+                const int32_t x = st[4 * sp], y = st[4 * sp + 1], rw = st[4 * sp + 2], rh = st[4 * sp + 3];
+                if (used == 12) {
+                    ok = false;
+                    break;
+                }
+                const int b = (v >> (11 - used)) & 1;
+                ++used;
+                if (b) {
+                    if (rw == 1 && rh == 1) {
+                        ok = false;
+                        break;
+                    }
+                    int32_t* a = st + 4 * sp;
+                    if (rh > rw) {
+                        const int32_t t = (rh + 1) / 2;
+                        a[0] = x, a[1] = y + t, a[2] = rw, a[3] = rh - t;
+                        a[4] = x, a[5] = y, a[6] = rw, a[7] = t;
+                    } else {
+                        const int32_t t = (rw + 1) / 2;
+                        a[0] = x + t, a[1] = y, a[2] = rw - t, a[3] = rh;
+                        a[4] = x, a[5] = y, a[6] = t, a[7] = rh;
+                    }
+                    sp += 2;
+                } else {
+                    m |= 1ull << ((y + rh / 2) * 8 + (x + rw / 2));
+                }
+            }
+            mask[v] = ok ? m : 0;
+            nbits[v] = ok ? (uint8_t)used : 0;
+        }
+    }
+} kBlockTree;
 
 void parse_tree_leaves(BitReader& rd, int32_t w, int32_t h, std::vector<Rect>& leaves) {
     walk_tree(rd, w, h, [&](int32_t x, int32_t y, int32_t rw, int32_t rh) { leaves.push_back({x, y, rw, rh}); });
@@ -197,47 +287,57 @@ void parse_flow_tree(BitReader& rd, int32_t w, int32_t h, std::vector<int32_t>& 
 // Tile -> covering leaf map.  A tile inside one leaf gets the leaf's value
 // index (< 0x8000); a tile straddling leaves gets 0x8000 + the deepest node
 // whose rectangle contains the whole tile (the device walks from there), or
-// 0xFFFF (walk from the root) when the indices do not fit 15 bits.
-static void flow_tile_map(const std::vector<Rect>& leaves, const std::vector<int32_t>& nodes, int32_t w, int32_t h,
+// 0xFFFF (walk from the root) when the indices do not fit 15 bits.  One
+// preorder descent hands each node the block of tiles lying wholly inside
+// it: a split passes its children the tiles wholly on their side and keeps
+// the (at most one) row or column of tiles its split line crosses; a leaf
+// takes all of its block.  Tiles are clipped to the plane (edge tiles).
+static void flow_tile_map(const std::vector<int32_t>& nodes, int32_t nleaves, int32_t w, int32_t h,
                           std::vector<uint16_t>& tiles) {
     const int nbx = (w + 7) / 8, nby = (h + 7) / 8;
     tiles.assign((size_t)nbx * nby, 0xFFFF);
-    if (leaves.size() >= 0x8000) return;  // all: per-pixel walk from the root
-    for (size_t li = 0; li < leaves.size(); ++li) {
-        const Rect& r = leaves[li];
-        // tiles entirely inside the leaf (edge tiles are clipped to the plane)
-        const int tx0 = (r.x + 7) / 8, ty0 = (r.y + 7) / 8;
-        for (int ty = ty0; ty < nby; ++ty) {
-            const int y0 = ty * 8, y1 = std::min(h, y0 + 8);
-            if (y1 > r.y + r.h) break;
-            for (int tx = tx0; tx < nbx; ++tx) {
-                const int x0 = tx * 8, x1 = std::min(w, x0 + 8);
-                if (x1 > r.x + r.w) break;
-                tiles[(size_t)ty * nbx + tx] = (uint16_t)li;
-            }
+    if (nleaves >= 0x8000) return;  // all: per-pixel walk from the root
+    struct Blk {
+        int32_t node, tx0, tx1, ty0, ty1;
+    };
+    std::vector<Blk> st;
+    st.push_back({0, 0, nbx, 0, nby});
+    auto fill = [&](int32_t tx0, int32_t tx1, int32_t ty0, int32_t ty1, uint16_t v) {
+        for (int32_t ty = ty0; ty < ty1; ++ty)
+            std::fill(tiles.begin() + (size_t)ty * nbx + tx0, tiles.begin() + (size_t)ty * nbx + tx1, v);
+    };
+    while (!st.empty()) {
+        const Blk b = st.back();
+        st.pop_back();
+        if (b.tx0 >= b.tx1 || b.ty0 >= b.ty1) continue;
+        const int32_t a = nodes[2 * (size_t)b.node];
+        const int code = a & 3, c = a >> 2;
+        if (code == 0) {
+            fill(b.tx0, b.tx1, b.ty0, b.ty1, (uint16_t)nodes[2 * (size_t)b.node + 1]);
+            continue;
+        }
+        const uint16_t here = b.node < 0x7FFF ? (uint16_t)(0x8000 + b.node) : (uint16_t)0xFFFF;
+        const int32_t left = b.node + 1, right = nodes[2 * (size_t)b.node + 1];
+        if (code == 1) {  // x split: tiles with min(w, 8tx + 8) <= c go left, 8tx >= c right
+            int32_t lo = std::min(c / 8, b.tx1), hi = std::max(std::min((c + 7) / 8, b.tx1), b.tx0);
+            if (lo < b.tx0) lo = b.tx0;
+            if (std::min(w, 8 * lo + 8) <= c) ++lo;  // (only when c is a multiple of 8 or at the clipped edge)
+            lo = std::min(lo, b.tx1);
+            hi = std::max(hi, lo);
+            st.push_back({right, hi, b.tx1, b.ty0, b.ty1});
+            st.push_back({left, b.tx0, lo, b.ty0, b.ty1});
+            fill(lo, hi, b.ty0, b.ty1, here);
+        } else {  // y split
+            int32_t lo = std::min(c / 8, b.ty1), hi = std::max(std::min((c + 7) / 8, b.ty1), b.ty0);
+            if (lo < b.ty0) lo = b.ty0;
+            if (std::min(h, 8 * lo + 8) <= c) ++lo;
+            lo = std::min(lo, b.ty1);
+            hi = std::max(hi, lo);
+            st.push_back({right, b.tx0, b.tx1, hi, b.ty1});
+            st.push_back({left, b.tx0, b.tx1, b.ty0, lo});
+            fill(b.tx0, b.tx1, lo, hi, here);
         }
     }
-    if (nodes.size() / 2 >= 0x7FFF) return;
-    for (int ty = 0; ty < nby; ++ty)
-        for (int tx = 0; tx < nbx; ++tx) {
-            uint16_t& t = tiles[(size_t)ty * nbx + tx];
-            if (t != 0xFFFF) continue;
-            const int x0 = tx * 8, x1 = std::min(w, x0 + 8), y0 = ty * 8, y1 = std::min(h, y0 + 8);
-            int i = 0;
-            for (;;) {  // descend while one child holds the whole tile (parse.h node layout)
-                const int32_t a = nodes[2 * (size_t)i];
-                const int code = a & 3, c = a >> 2;
-                if (code == 0) break;  // (a leaf would have been mapped above)
-                const int lo = code == 1 ? x0 : y0, hi = code == 1 ? x1 : y1;
-                if (hi <= c)
-                    i = i + 1;
-                else if (lo >= c)
-                    i = nodes[2 * (size_t)i + 1];
-                else
-                    break;
-            }
-            t = (uint16_t)(0x8000 + i);
-        }
 }
 
 StreamHeader parse_header(const uint8_t* d, size_t len) {  // bitstream.py:102-121, 80-91
@@ -696,9 +796,8 @@ size_t parse_flow(const uint8_t* d, size_t len, size_t pos, int32_t h, int32_t w
         if (pos + nbytes > len) fail(HIVC_E_TRUNCATED_STREAM, "flow payload truncated");
         BitReader rd(d + pos, nbytes, nbits);
         int32_t nleaves = 0;
-        std::vector<Rect> leaves;
-        parse_flow_tree(rd, w, h, job.nodes[c], nleaves, &leaves);
-        flow_tile_map(leaves, job.nodes[c], w, h, job.tiles[c]);
+        parse_flow_tree(rd, w, h, job.nodes[c], nleaves, nullptr);
+        flow_tile_map(job.nodes[c], nleaves, w, h, job.tiles[c]);
         pos += nbytes;
         std::vector<int32_t> idx;
         pos = decode_symbols(d, len, pos, idx);
@@ -779,9 +878,20 @@ size_t parse_residual(const uint8_t* d, size_t len, size_t pos, int32_t h, int32
                 int32_t ty = (int32_t)(t / nbx), tx = (int32_t)(t % nbx);
                 int32_t bh = std::min(8, h - ty * 8), bw = std::min(8, w - tx * 8);
                 uint64_t m = 0;  // parse_mask per coded tile (codec.py:300-303)
-                walk_tree(rd, bw, bh, [&](int32_t x, int32_t y, int32_t rw, int32_t rh) {
-                    m |= 1ull << ((y + rh / 2) * 8 + (x + rw / 2));
-                });
+                bool done = false;
+                if (bw == 8 && bh == 8) {
+                    const uint32_t v = rd.peek12();
+                    const int nb = kBlockTree.nbits[v];
+                    if (nb && rd.pos + (uint64_t)nb <= rd.limit) {
+                        m = kBlockTree.mask[v];
+                        rd.skip(nb);
+                        done = true;
+                    }
+                }
+                if (!done)
+                    walk_tree(rd, bw, bh, [&](int32_t x, int32_t y, int32_t rw, int32_t rh) {
+                        m |= 1ull << ((y + rh / 2) * 8 + (x + rw / 2));
+                    });
                 g.block_mask[b] = m;
                 g.block_off[b] = npts;
                 npts += __builtin_popcountll(m);

@@ -55,6 +55,17 @@ struct BitReader {
         ++pos;
         return b;
     }
+    // the next 12 bits without consuming them (zeros past the data)
+    inline uint32_t peek12() {
+        if (avail < 12) refill();
+        return (uint32_t)(buf >> 52);
+    }
+    // consume n <= 12 bits known to lie inside the limit (after peek12)
+    inline void skip(int n) {
+        buf <<= n;
+        avail -= n;
+        pos += (uint64_t)n;
+    }
     inline uint32_t take(int n) {  // n <= 32
         if (n == 0) return 0;
         if (pos + (uint64_t)n > limit) fail(HIVC_E_TRUNCATED_STREAM, "bit stream exhausted");
@@ -106,11 +117,16 @@ inline void walk_tree(BitReader& rd, int32_t w, int32_t h, F&& on_leaf) {
 uint64_t read_uvarint(const uint8_t* d, size_t len, size_t& pos);
 
 // tANS decode tables for one normalised distribution (entropy.py:108-130).
+// Entry: symbol, bit count nb and base = x << nb, so the next state is
+// base | the next nb bits (fse_decode, entropy.py:175-211).
 struct FseTable {
+    struct Entry {
+        uint32_t base;
+        uint16_t sym;
+        uint8_t nb;
+    };
     int table_log = 0;
-    std::vector<uint16_t> sym;
-    std::vector<uint32_t> x;
-    std::vector<uint8_t> nb;
+    std::vector<Entry> dec;
     void build(const std::vector<uint64_t>& counts, int table_log);
 };
 

@@ -43,8 +43,8 @@ __global__ void __launch_bounds__(1024) k_smem(double* out) {
     for (int i = 0; i < kSmemIters; i += 2) {
         double x0, x1, y0, y1;
         unsigned p0 = base + ((idx) & mask) * 16, p1 = base + ((idx + 1024) & mask) * 16;
-        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x0), "=d"(x1) : "r"(p0));
-        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(y0), "=d"(y1) : "r"(p1));
+        asm volatile("ld.volatile.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x0), "=d"(x1) : "r"(p0) : "memory");
+        asm volatile("ld.volatile.shared.v2.f64 {%0, %1}, [%2];" : "=d"(y0), "=d"(y1) : "r"(p1) : "memory");
         a0 += x0;
         a1 += x1;
         b0 += y0;
@@ -103,13 +103,122 @@ __global__ void k_gridbar(unsigned* bar, int rounds) {
         __syncthreads();
         ++epoch;
         if (threadIdx.x == 0) {
-            unsigned old;
-            asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(bar) : "memory");
+            asm volatile("red.add.release.gpu.global.u32 [%0], 1;" : : "l"(bar) : "memory");
             while (ld_acq(bar) < epoch * gridDim.x) {
             }
         }
         __syncthreads();
     }
+}
+// two-level barrier: cluster barrier, then one arrival per cluster on the grid counter
+__global__ void k_gridbar2(unsigned* bar, int rounds) {
+    cg::cluster_group cl = cg::this_cluster();
+    const unsigned ncl = gridDim.x / cl.num_blocks();
+    const bool leader = cl.block_rank() == 0;
+    unsigned epoch = 0;
+    for (int r = 0; r < rounds; ++r) {
+        cl.sync();
+        ++epoch;
+        if (threadIdx.x == 0) {
+            if (leader) asm volatile("red.add.release.gpu.global.u32 [%0], 1;" : : "l"(bar) : "memory");
+            while (ld_acq(bar) < epoch * ncl) {
+            }
+        }
+        __syncthreads();
+    }
+}
+// A full fixed-order grid sum of one double per thread, as the CG level kernel
+// does it twice per iteration.  v1: every CTA publishes its partial and arrives
+// on one counter, then a warp loads all CTA partials.  v2: CTA partials are
+// summed per cluster over DSMEM, the cluster leader publishes and arrives, then
+// a warp loads the cluster partials.
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__global__ void __launch_bounds__(512) k_gridred1(unsigned* bar, double* part, int rounds, double* out) {
+    __shared__ double buf[2][16];
+    __shared__ double bc[2];
+    unsigned epoch = 0;
+    double v = threadIdx.x * 1e-3, acc = 0;
+    for (int r = 0; r < rounds; ++r) {
+        const int pb = r & 1;
+        double s = warp_sum(v + acc * 1e-300);
+        if ((threadIdx.x & 31) == 0) buf[pb][threadIdx.x >> 5] = s;
+        __syncthreads();
+        double* pp = part + pb * 2048;
+        if (threadIdx.x == 0) {
+            double t = 0;
+            for (int i = 0; i < 16; ++i) t += buf[pb][i];
+            pp[blockIdx.x] = t;
+            ++epoch;
+            asm volatile("red.add.release.gpu.global.u32 [%0], 1;" : : "l"(bar) : "memory");
+            while (ld_acq(bar) < epoch * gridDim.x) {
+            }
+        } else {
+            ++epoch;
+        }
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            double vals[5], t = 0;
+#pragma unroll
+            for (int j = 0; j < 5; ++j) {
+                const int g = threadIdx.x + 32 * j;
+                vals[j] = g < (int)gridDim.x ? __ldcg(pp + g) : 0.0;
+            }
+#pragma unroll
+            for (int j = 0; j < 5; ++j) t += vals[j];
+            t = warp_sum(t);
+            if (threadIdx.x == 0) bc[pb] = t;
+        }
+        __syncthreads();
+        acc += bc[pb];
+    }
+    if (acc == -1.0) out[0] = acc;
+}
+__global__ void __launch_bounds__(512) k_gridred2(unsigned* bar, double* part, int rounds, double* out) {
+    __shared__ double buf[2][16];
+    __shared__ double cpart[2];
+    __shared__ double bc[2];
+    cg::cluster_group cl = cg::this_cluster();
+    const unsigned csz = cl.num_blocks(), ncl = gridDim.x / csz, crank = cl.block_rank();
+    unsigned epoch = 0;
+    double v = threadIdx.x * 1e-3, acc = 0;
+    for (int r = 0; r < rounds; ++r) {
+        const int pb = r & 1;
+        double s = warp_sum(v + acc * 1e-300);
+        if ((threadIdx.x & 31) == 0) buf[pb][threadIdx.x >> 5] = s;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0;
+            for (int i = 0; i < 16; ++i) t += buf[pb][i];
+            cpart[pb] = t;
+        }
+        cl.sync();
+        double* pp = part + pb * 2048;
+        ++epoch;
+        if (crank == 0 && threadIdx.x < 32) {
+            double t = (unsigned)threadIdx.x < csz ? *cl.map_shared_rank(&cpart[pb], threadIdx.x) : 0.0;
+            t = warp_sum(t);
+            if (threadIdx.x == 0) {
+                pp[blockIdx.x / csz] = t;
+                asm volatile("red.add.release.gpu.global.u32 [%0], 1;" : : "l"(bar) : "memory");
+            }
+        }
+        if (threadIdx.x == 0)
+            while (ld_acq(bar) < epoch * ncl) {
+            }
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            double t = (unsigned)threadIdx.x < ncl ? __ldcg(pp + threadIdx.x) : 0.0;
+            t = warp_sum(t);
+            if (threadIdx.x == 0) bc[pb] = t;
+        }
+        __syncthreads();
+        acc += bc[pb];
+    }
+    if (acc == -1.0) out[0] = acc;
 }
 __global__ void k_clusterbar(int rounds, double* out) {
     cg::cluster_group cl = cg::this_cluster();
@@ -219,8 +328,83 @@ int main() {
         }
         cudaGetLastError();
     }
+    double bar2_us[2] = {-1, -1};
+    CK(cudaFuncSetAttribute(k_gridbar2, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    for (int v = 0; v < 2; ++v) {
+        const int csz = v == 0 ? 16 : 8;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(nb);
+        cfg.blockDim = dim3(512);
+        cudaLaunchAttribute attr[2];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = csz;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        attr[1].id = cudaLaunchAttributeCooperative;
+        attr[1].val.cooperative = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 2;
+        float b = 1e30f;
+        for (int rep = 0; rep < 5; ++rep) {
+            cudaMemset(bar, 0, 64);
+            cudaEventRecord(e0);
+            if (cudaLaunchKernelEx(&cfg, k_gridbar2, bar, rounds) != cudaSuccess) break;
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+            b = std::min(b, time_ms(e0, e1));
+        }
+        if (b < 1e29f) bar2_us[v] = b * 1e3 / rounds;
+        cudaGetLastError();
+    }
+    double red_us[3] = {-1, -1, -1};
+    double* part;
+    CK(cudaMalloc(&part, 4096 * sizeof(double)));
+    {
+        float b = 1e30f;
+        for (int rep = 0; rep < 5; ++rep) {
+            cudaMemset(bar, 0, 64);
+            void* args[] = {&bar, &part, (void*)&rounds, &out};
+            cudaEventRecord(e0);
+            CK(cudaLaunchCooperativeKernel((const void*)k_gridred1, dim3(nb), dim3(512), args, 0, 0));
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+            b = std::min(b, time_ms(e0, e1));
+        }
+        red_us[0] = b * 1e3 / rounds;
+    }
+    CK(cudaFuncSetAttribute(k_gridred2, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    for (int v = 0; v < 2; ++v) {
+        const int csz = v == 0 ? 16 : 8;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(nb);
+        cfg.blockDim = dim3(512);
+        cudaLaunchAttribute attr[2];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = csz;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        attr[1].id = cudaLaunchAttributeCooperative;
+        attr[1].val.cooperative = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 2;
+        float b = 1e30f;
+        for (int rep = 0; rep < 5; ++rep) {
+            cudaMemset(bar, 0, 64);
+            cudaEventRecord(e0);
+            if (cudaLaunchKernelEx(&cfg, k_gridred2, bar, part, rounds, out) != cudaSuccess) break;
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+            b = std::min(b, time_ms(e0, e1));
+        }
+        if (b < 1e29f) red_us[1 + v] = b * 1e3 / rounds;
+        cudaGetLastError();
+    }
+    std::printf("{\"grid_sum_1level_us\": %.3f, \"grid_sum_2level_c16_us\": %.3f, \"grid_sum_2level_c8_us\": %.3f, ",
+                red_us[0], red_us[1], red_us[2]);
     std::printf(
-        "{\"sms\": %d, \"clock_mhz_attr\": %.0f, \"l2_bytes\": %d, \"smem_per_sm_bytes\": %zu, "
+        "\"grid_barrier_2level_c16_us\": %.3f, \"grid_barrier_2level_c8_us\": %.3f, ", bar2_us[0], bar2_us[1]);
+    std::printf(
+        "\"sms\": %d, \"clock_mhz_attr\": %.0f, \"l2_bytes\": %d, \"smem_per_sm_bytes\": %zu, "
         "\"smem_load_GBps\": %.1f, \"l2_read_GBps\": %.1f, \"l2_probe_bytes\": %zu, \"hbm_read_GBps\": %.1f, "
         "\"dadd_TFLOPs\": %.3f, \"dmul_TFLOPs\": %.3f, \"grid_barrier_us\": %.3f, \"grid_barrier_ctas\": %d, "
         "\"cluster16_barrier_us\": %.3f}\n",
