@@ -39,15 +39,21 @@ sys.path.insert(0, str(REPO))
 STREAMS = REPO / "tests" / "golden" / "streams"
 PLANES = ("Y", "Cb", "Cr")
 METRIC = "1080p decoded frames/sec (4:2:0, Y+Cb+Cr per frame)"
-WORKLOAD = "config3: 60-frame 1080p YCbCr 4:2:0 synthetic video, GOP 12, reference-encoded, 3 gray streams"
+WORKLOADS = {
+    "config3": "config3: 60-frame 1080p YCbCr 4:2:0 synthetic video, GOP 12, reference-encoded, 3 gray streams",
+    "config4": "config4: 480-frame 1080p YCbCr 4:2:0 synthetic video (seed 4), 40 GOPs of 12, Brox 0.95 flows, "
+               "3 gray streams (tools/config4_full.py); strong scaling: the 40 GOPs split over the ranks",
+}
+CFG4_DIR = REPO / "baseline" / "_cfg4"  # git-ignored, travels with the tree (tools/config4_full.py --out)
 
 
-def load_streams():
+def load_streams(workload="config3"):
     out = []
     for p in PLANES:
-        path = STREAMS / f"cfg3_{p}.hivc"
+        path = STREAMS / f"cfg3_{p}.hivc" if workload == "config3" else CFG4_DIR / f"cfg4_{p}.hivc"
         if not path.exists():
-            raise SystemExit(f"missing {path}: run tests/golden/make_streams.py cfg3 in the build container")
+            raise SystemExit(f"missing {path}: run tests/golden/make_streams.py cfg3 in the build container"
+                             if workload == "config3" else f"missing {path}: run tools/config4_full.py --out {CFG4_DIR}")
         out.append(path.read_bytes())
     return out
 
@@ -200,7 +206,7 @@ def reference_arm(args, rank):
     for the same jobs is reported beside it (`port_value`)."""
     if rank != 0:
         return
-    streams = load_streams()
+    streams = load_streams(args.workload)
     cores = os.cpu_count() or 1
     jobs = [one_gop_stream(s, g) for g in range(gop_count(streams[0])) for s in streams]
     procs = max(1, min(cores, len(jobs)))
@@ -241,11 +247,11 @@ def reference_arm(args, rank):
         "warmup": args.warmup,
         "ms_per_step": ms,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "weak" if args.workload == "config3" else "strong",
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (seeded, SURVEY §8(d) recipe), reference-encoded bitstreams",
-        "config": {"workload": WORKLOAD, "sample": sample},
+        "config": {"workload": WORKLOADS[args.workload], "sample": sample},
         "cpu_baseline": {"value": value, "unit": "frames/s", "cores": procs, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -253,6 +259,104 @@ def reference_arm(args, rank):
         line["port_value"] = port
         line["port_note"] = "oracle/ numpy port on the same jobs and processes (1 step), for comparison only"
     print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- rooflines
+
+ONCHIP = REPO / "profiles" / "r02_onchip_peaks.json"     # tools/onchip_peaks.py on this pool's B200
+KMETRICS = REPO / "profiles" / "r02_kernel_metrics.json"  # ncu capture of this bench's own launches
+# shared-memory bytes per pixel per CG iteration in cg_tile_kernel (counted from the code,
+# 8-byte accesses): p = r + beta p (load + store), A p (3 loads: row below + 2 sides; the
+# rows above / here ride in registers), r -= alpha A p (3 loads again), x += alpha p (3)
+SMEM_B_PX_IT = 88
+
+
+def _kernel_row(km, pattern):
+    import re
+
+    for name, row in (km or {}).get("kernels", {}).items():
+        if re.search(pattern, name):
+            return name, row
+    return None, None
+
+
+def roofline_rows(gsec, glaunch, gpix_it, gpix, pix_it, peaks):
+    """The dominant kernel's roofline (live timing) plus one row per decode kernel
+    (ncu capture of this bench's launches).  Each row names its real limiter."""
+    onchip = json.loads(ONCHIP.read_text()) if ONCHIP.exists() else {}
+    km = json.loads(KMETRICS.read_text()) if KMETRICS.exists() else {}
+    hbm = peaks.get("hbm_gbs", 6550.0)
+    smem_peak = onchip.get("smem_load_GBps")
+    l2_peak = onchip.get("l2_read_GBps")
+    sum_us = onchip.get("grid_sum_1level_us")
+    t_launch = gsec / glaunch if glaunch else None
+    it_per_launch = gpix_it / gpix if gpix else None  # pixel-weighted mean iterations of a level launch
+    px_per_launch = gpix / glaunch if glaunch else None
+    smem_bytes = SMEM_B_PX_IT * gpix_it / glaunch if glaunch else None
+    achieved = smem_bytes / t_launch / 1e9 if t_launch else None
+    name, kt = _kernel_row(km, r"cg_tile_kernel")
+    floor = None
+    if t_launch and smem_peak and sum_us and it_per_launch:
+        floor = smem_bytes / (smem_peak * 1e9) + it_per_launch * 2 * sum_us * 1e-6
+    top = {
+        "kernel": "cg_tile_kernel (CG level on chip: 30x480 tiles, r in registers, p + ~all of x in shared memory, "
+                  "two fixed-order grid sums per iteration; float64)",
+        "bound": "smem",
+        "achieved": achieved,
+        "peak": smem_peak,
+        "unit": "GB/s",
+        "frac": achieved / smem_peak if achieved and smem_peak else None,
+        "traffic": kt["dram_bytes"] if kt else None,
+        "algorithmic": f"shared-memory bytes = {SMEM_B_PX_IT} B x pixels x iterations per level launch "
+                       f"(= {smem_bytes / 1e9:.2f} GB/launch)" if smem_bytes else None,
+        "live_timing": "in-kernel globaltimer span per launch, instrumented bench steps",
+        "avg_launch_us": 1e6 * t_launch if t_launch else None,
+        "launches": int(glaunch),
+        "iterations_per_launch": it_per_launch,
+        "pixels_per_launch": px_per_launch,
+        "grid_sum_floor_share": (it_per_launch * 2 * sum_us * 1e-6 / t_launch) if t_launch and sum_us else None,
+        "floor_us": 1e6 * floor if floor else None,
+        "frac_of_floor": floor / t_launch if floor else None,
+        "floor_note": "smem bytes at the measured LDS peak + 2 grid sums per iteration at the measured 1.82 us "
+                      "(profiles/r02_onchip_peaks.json); the kernel is bound by both, in sequence",
+        "measured_traffic_per_launch": ({"dram_bytes": kt["dram_bytes"], "l2_bytes": kt.get("lts__t_bytes.sum"),
+                                         "smem_bytes_upper": kt["smem_bytes_upper"],
+                                         "source": KMETRICS.name} if kt else None),
+        "hbm_streaming_equiv": {
+            "achieved": (49.0 * gpix_it + 49.0 * gpix) / gsec / 1e9 if gsec else None,
+            "peak": hbm, "unit": "GB/s",
+            "note": "SURVEY 8(d) B_cg = N_l(49 it_l + 49): what a kernel streaming x, r, p through HBM would move; "
+                    "the data never leaves the SM, so this is a comparison, not the bound",
+        },
+        "peak_source": f"{ONCHIP.name} smem_load_GBps (measured)" if smem_peak else "missing",
+    }
+    rows = []
+    for label, pat, bound in [("cg_tile_kernel", r"cg_tile_kernel", "smem"),
+                              ("cg_cluster_col_kernel", r"cg_cluster_col_kernel", "smem"),
+                              ("frame_kernel P (fused warp + residual + rint/clip)", r"frame_kernel<(1|true), 1", "latency"),
+                              ("frame_kernel I (finalize)", r"frame_kernel<(0|false), 1", "latency"),
+                              ("restrict_kernel", r"restrict_kernel", "hbm")]:
+        n, r = _kernel_row(km, pat)
+        if not r:
+            continue
+        t = r.get("gpu__time_duration.sum", 0) * 1e-9
+        row = {"kernel": label, "launches_captured": r["launches"], "ncu_us": 1e6 * t,
+               "dram_GBps": r["dram_bytes"] / t / 1e9 if t else None,
+               "l2_GBps": r.get("lts__t_bytes.sum", 0) / t / 1e9 if t else None,
+               "smem_GBps_upper": r["smem_bytes_upper"] / t / 1e9 if t else None,
+               "warps_active_pct": r.get("sm__warps_active.avg.pct_of_peak_sustained_active"),
+               "bound": bound}
+        if bound == "smem" and smem_peak and t:
+            row["frac"] = r["smem_bytes_upper"] / t / 1e9 / smem_peak
+        elif bound == "hbm" and t:
+            row["frac"] = r["dram_bytes"] / t / 1e9 / hbm
+        else:
+            row["frac_of_l2"] = (r.get("lts__t_bytes.sum", 0) / t / 1e9 / l2_peak) if t and l2_peak else None
+            row["note"] = ("one CTA wave or less per frame; each warp runs a ~1500-instruction dependent chain "
+                           "(tile map -> flow value -> bilinear taps, residual AAN) at ~10 active warps/SM")
+        rows.append(row)
+    return top, rows, {"source": KMETRICS.name if km else None, "command": km.get("command"),
+                       "timing": "ncu serialised replays (cold launch, warm caches); shares, not absolutes"}
 
 
 # ----------------------------------------------------------------------------- GPU leg
@@ -265,6 +369,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--workload", default="config3", choices=sorted(WORKLOADS),
+                    help="config3 (default, BASELINE's 1-GPU metric config; weak scaling) or config4 (strong scaling)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -295,10 +401,15 @@ def main():
     from paper_2008_10273_b200 import codec
     from paper_2008_10273_b200.shard import gather_frames, gop_ranges, tile_stream
 
-    base = load_streams()
-    gops_per_rank = codec.stream_info(base[0]).gop_count
-    video = [tile_stream(s, world) for s in base]
-    ranges = [gop_ranges(gops_per_rank * world, world)[rank]] * 3
+    base = load_streams(args.workload)
+    if args.workload == "config3":  # weak scaling: the 5-GOP sequence tiled once per rank
+        gops_per_rank = codec.stream_info(base[0]).gop_count
+        video = [tile_stream(s, world) for s in base]
+        ranges = [gop_ranges(gops_per_rank * world, world)[rank]] * 3
+    else:  # strong scaling: the 40 GOPs of config 4 split over the ranks
+        video = base
+        ranges = [gop_ranges(codec.stream_info(base[0]).gop_count, world)[rank]] * 3
+        gops_per_rank = ranges[0][1] - ranges[0][0]
     shapes = [codec.frames_shape(v, *r) for v, r in zip(video, ranges)]
     frames_per_rank = shapes[0][0]
     ctx = N.Context(local)
@@ -431,24 +542,17 @@ def main():
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
     t_step = tot[0].item() / args.steps
     t_e2e = tot[1].item() / args.steps
-    total_frames = frames_per_rank * world
+    total_frames = (frames_per_rank * world if args.workload == "config3"
+                    else sum(codec.frames_shape(video[0], *r)[0] for r in gop_ranges(codec.stream_info(video[0]).gop_count, world)))
 
     if rank == 0:
         peaks = {}
         pk = REPO / "MEASURED_PEAKS.json"
         if pk.exists():
             peaks = json.loads(pk.read_text())
-        hbm = peaks.get("hbm_gbs", 6650.0)
         (solves, pix_it, pix_lv, glaunch, gsec, gpix_it, gpix, p_frames, p_sec, i_frames) = list(stats)
-        # dominant kernel: the cooperative CG level kernel; algorithmic bytes per
-        # launch = N_l * (49 * it_l + 49): float64 x, r, p read+write + the mask
-        # byte per iteration, plus the level's setup/finalise pass
-        cg_bytes = 49.0 * gpix_it + 49.0 * gpix
-        achieved = cg_bytes / gsec / 1e9 if gsec > 0 else None
-        traffic = None
-        tf = REPO / "profiles" / "cg_traffic.json"
-        if tf.exists():
-            traffic = json.loads(tf.read_text()).get("dram_bytes_per_launch")
+        roof, rows, rows_src = roofline_rows(gsec, glaunch, gpix_it, gpix, pix_it, peaks)
+        roof["share_of_step"] = gsec / sum(instr_times) if instr_times else None
         cpu = None
         if world == 1 and not args.no_cpu:
             fps, wall, _, kind = cpu_sample(base, 1)
@@ -471,12 +575,15 @@ def main():
             "warmup": args.warmup,
             "ms_per_step": t_step * 1e3,
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": "weak" if args.workload == "config3" else "strong",
             "vs_baseline": None,
             "dtype": "f64",
-            "data": "synthetic (seeded, SURVEY §8(d) recipe; no public dataset), reference-encoded bitstreams",
+            "data": "synthetic (seeded, SURVEY §8(d) recipe; no public dataset), reference-encoded bitstreams"
+                    if args.workload == "config3" else
+                    "synthetic (seeded, SURVEY §8(d) recipe; no public dataset), streams from this repo's encoder "
+                    "(GOP 0 byte-identical to the reference encoder with the same flows, tools/config4_refcheck.py)",
             "config": {
-                "workload": WORKLOAD,
+                "workload": WORKLOADS[args.workload],
                 "frames_per_rank": frames_per_rank,
                 "gops_per_rank": gops_per_rank,
                 "parallelism": f"gop-shard x{world}" + ({"peer": " + frames copied into rank 0's IPC-mapped buffer over "
@@ -496,26 +603,9 @@ def main():
             "device_span_ms": 1e3 * statistics.median(spans),
             "stages_ms_per_step": {k: round(1e3 * v / n_instr, 3) for k, v in timings.items()},
             "stages_note": f"from {n_instr} separate instrumented (CUDA-event) steps, not the timed ones",
-            "roofline": {
-                "kernel": ("cg_level_kernel<grid> (streaming CG level, float64)" if os.environ.get("HIVC_CG_BAND") == "0"
-                           else "cg_tile_kernel (on-chip CG level over 30x480 tiles, float64: r in registers, p + ~all of x in smem)"),
-                "algorithmic_bytes": "N_l*(49*it_l + 49) per level launch: float64 x, r, p read+write + mask byte "
-                                     "per iteration, plus the setup/finalise pass",
-                "bound": "hbm",
-                "achieved": achieved,
-                "peak": hbm,
-                "unit": "GB/s",
-                "frac": (achieved / hbm) if achieved else None,
-                "traffic": traffic,
-                "launches": int(glaunch),
-                "avg_launch_us": 1e6 * gsec / glaunch if glaunch else None,
-                "share_of_step": gsec / sum(instr_times) if instr_times else None,
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)" if "hbm_gbs" in peaks else "fallback",
-            },
-            "p_kernel": {
-                "frames": int(p_frames),
-                "avg_us": 1e6 * p_sec / p_frames if p_frames else None,
-            },
+            "roofline": roof,
+            "kernel_rows": rows,
+            "kernel_rows_source": rows_src,
             "clocks": clocks,
         }
         if cpu:

@@ -179,7 +179,7 @@ int hivc_homog_solve(hivc_ctx* ctx, const double* f, const uint8_t* mask, int32_
         std::vector<int> it(L);
         CUDA_CHECK(cudaMemcpyAsync(it.data(), C.ws.iters, L * sizeof(int), cudaMemcpyDeviceToHost, C.stream));
         CUDA_CHECK(cudaStreamSynchronize(C.stream));
-        if ((getenv("HIVC_CG_TRACE") || getenv("HIVC_CG_TRACE_CLUSTER")) && C.ws.trace) {
+        if ((hivc::debug_opt("cg_trace") || hivc::debug_opt("cg_trace_cluster")) && C.ws.trace) {
             // phase timing of the finest level (CTA 0, thread 0): mean ns per phase
             std::vector<unsigned long long> tr(hivc::kTraceLen);
             CUDA_CHECK(cudaMemcpy(tr.data(), C.ws.trace, tr.size() * 8, cudaMemcpyDeviceToHost));

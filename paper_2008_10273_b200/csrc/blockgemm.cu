@@ -23,6 +23,7 @@
 
 #include "aan_constants.h"
 #include "blockgemm.h"
+#include "func_attr.h"
 #include "inpaint.h"
 
 namespace hivc {
@@ -314,6 +315,147 @@ __global__ void __launch_bounds__(kPbWarps * 32)
     }
 }
 
+// One THREAD per block: the bordered system [[G_KK, 1], [1^T, 0]] [c; a] =
+// [f_K; 0] solved through its Schur complement — G_KK (a principal submatrix
+// of the positive semi-definite Green's matrix whose null space is the
+// constant block, so positive definite for K < 64) is factored
+// G_KK = L L^T, then y = G_KK^-1 f, z = G_KK^-1 1, a = 1^T y / 1^T z and
+// c = y - a z (the unique solution of the reference's system,
+// pseudodiff.py:218-263; rounding differs from LAPACK's pivoted LU at the
+// 1e-13 level); rec = G[:, pos] c + a.  The 64x64 Green's matrix is staged
+// in shared memory per CTA; each thread's packed factor lives in shared
+// memory interleaved across the CTA's threads (conflict-free); the rare block
+// with more than kSchurSmemK points factors into a per-thread local array
+// instead, up to kSchurMaxK (a block beyond that flags status 4: the host
+// reruns the warp-per-block kernel with wide systems).
+constexpr int kSchurThreads = 128;
+constexpr int kSchurSmemK = 12;
+constexpr int kSchurMaxK = 24;
+constexpr int kSchurTri = kSchurSmemK * (kSchurSmemK + 1) / 2;
+
+__global__ void __launch_bounds__(kSchurThreads) block_schur_kernel(const float* __restrict__ plane,
+                                                                    float* __restrict__ out, int h, int w,
+                                                                    const uint64_t* __restrict__ masks,
+                                                                    int nblocks, int* status) {
+    extern __shared__ double sm[];
+    double* G = sm;                    // 64 x 64
+    double* Lt = sm + 4096;            // kSchurTri x kSchurThreads, thread-interleaved
+    for (int i = threadIdx.x; i < 4096; i += kSchurThreads) G[i] = kGreens64[i];
+    __syncthreads();
+    const int b = blockIdx.x * kSchurThreads + threadIdx.x;
+    if (b >= nblocks) return;
+    const uint64_t mask = masks[b];
+    const int K = __popcll(mask);
+    if (K == 0) {
+        atomicExch(status, 1);
+        return;
+    }
+    if (K > kSchurMaxK) {
+        atomicExch(status, 4);
+        return;
+    }
+    double Lbig[kSchurMaxK * (kSchurMaxK + 1) / 2];  // (local memory; K > kSchurSmemK only)
+    const bool big = K > kSchurSmemK;
+    auto L = [&](int i, int j) -> double& {
+        return big ? Lbig[i * (i + 1) / 2 + j] : Lt[(i * (i + 1) / 2 + j) * kSchurThreads + threadIdx.x];
+    };
+    const int nbx = (w + 7) >> 3;
+    const int by = b / nbx, bx = b - by * nbx;
+    int pos[kSchurMaxK];
+    double f[kSchurMaxK];
+    {
+        uint64_t m = mask;
+#pragma unroll
+        for (int i = 0; i < kSchurMaxK; ++i) {
+            pos[i] = 0;
+            f[i] = 0.0;
+            if (i < K) {
+                const int j = __ffsll((long long)m) - 1;
+                m &= m - 1;
+                pos[i] = j;
+                const int y = by * 8 + (j >> 3), x = bx * 8 + (j & 7);
+                f[i] = (y < h && x < w) ? (double)__ldg(plane + (size_t)y * w + x) : 0.0;
+            }
+        }
+    }
+    // G_KK = L L^T (column by column)
+    for (int j = 0; j < K; ++j) {
+        double d = G[pos[j] * 64 + pos[j]];
+        for (int k = 0; k < j; ++k) d = d - L(j, k) * L(j, k);
+        if (!(d > 0.0)) {
+            atomicExch(status, 2);
+            return;
+        }
+        const double ljj = sqrt(d);
+        L(j, j) = ljj;
+        for (int i = j + 1; i < K; ++i) {
+            double v = G[pos[i] * 64 + pos[j]];
+            for (int k = 0; k < j; ++k) v = v - L(i, k) * L(j, k);
+            L(i, j) = v / ljj;
+        }
+    }
+    // y = G^-1 f, z = G^-1 1: forward then backward substitution, both at once
+    double y[kSchurMaxK], z[kSchurMaxK];
+#pragma unroll
+    for (int i = 0; i < kSchurMaxK; ++i) {
+        if (i >= K) break;
+        double sy = f[i], sz = 1.0;
+        for (int k = 0; k < i; ++k) {
+            const double l = L(i, k);
+            sy = sy - l * y[k];
+            sz = sz - l * z[k];
+        }
+        const double d = L(i, i);
+        y[i] = sy / d;
+        z[i] = sz / d;
+    }
+#pragma unroll
+    for (int i = kSchurMaxK - 1; i >= 0; --i) {
+        if (i >= K) continue;
+        double sy = y[i], sz = z[i];
+        for (int k = i + 1; k < K; ++k) {
+            const double l = L(k, i);
+            sy = sy - l * y[k];
+            sz = sz - l * z[k];
+        }
+        const double d = L(i, i);
+        y[i] = sy / d;
+        z[i] = sz / d;
+    }
+    double sy = 0.0, sz = 0.0;
+#pragma unroll
+    for (int i = 0; i < kSchurMaxK; ++i)
+        if (i < K) {
+            sy += y[i];
+            sz += z[i];
+        }
+    const double a = sy / sz;
+#pragma unroll
+    for (int i = 0; i < kSchurMaxK; ++i) y[i] = i < K ? y[i] - a * z[i] : 0.0;  // c
+    // rec = G[:, pos] c + a, one 8-pixel row at a time
+    for (int r = 0; r < 8; ++r) {
+        const int yy = by * 8 + r;
+        if (yy >= h) break;
+        float o[8];
+#pragma unroll
+        for (int xx = 0; xx < 8; ++xx) {
+            const double* g = G + (r * 8 + xx) * 64;
+            double acc = 0.0;
+#pragma unroll
+            for (int i = 0; i < kSchurMaxK; ++i)
+                if (i < K) acc = acc + g[pos[i]] * y[i];
+            o[xx] = (float)(acc + a);
+        }
+        float* dst = out + (size_t)yy * w + bx * 8;
+        if (bx * 8 + 8 <= w && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+            reinterpret_cast<float4*>(dst)[0] = make_float4(o[0], o[1], o[2], o[3]);
+            reinterpret_cast<float4*>(dst)[1] = make_float4(o[4], o[5], o[6], o[7]);
+        } else {
+            for (int xx = 0; xx < 8 && bx * 8 + xx < w; ++xx) dst[xx] = o[xx];
+        }
+    }
+}
+
 // ---------------------------------------------------------------- host
 
 // R = G[:, pos] S^-1[:K,:K] + 1 S^-1[K,:K] scattered to the mask columns (float64, Gauss-Jordan)
@@ -362,11 +504,7 @@ void launch_block_operator_tc(const float* plane, float* out, int h, int w, cons
     const int nblocks = ((h + 7) / 8) * ((w + 7) / 8);
     const int ntiles = (nblocks + kTileM - 1) / kTileM;
     const size_t smem = 65536 + 32768;
-    static bool attr = false;
-    if (!attr) {
-        CUDA_CHECK(cudaFuncSetAttribute(block_operator_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
+    ensure_func_attr((const void*)block_operator_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int vec = (w % 4 == 0) && ((uintptr_t)plane % 16 == 0) && ((uintptr_t)out % 16 == 0);
     // two CTAs per SM (96 KB smem, 64 TMEM columns each): one tile per CTA at 1080p, loads of one
     // CTA overlap the MMA / epilogue of the other
@@ -381,14 +519,18 @@ void launch_block_perblock(const float* plane, float* out, int h, int w, const u
     auto go = [&](auto kernel, int ld) {
         const size_t smem =
             (size_t)kPbWarps * ((ld - 1) * ld + 64) * sizeof(double) + kPbWarps * 64 * sizeof(int);
-        CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        ensure_func_attr((const void*)kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kernel<<<(nblocks + kPbWarps - 1) / kPbWarps, kPbWarps * 32, smem, s>>>(plane, out, h, w, masks, nblocks,
                                                                                   status);
     };
-    if (wide)
+    if (wide) {
         go(block_perblock_kernel<66>, 66);
-    else
-        go(block_perblock_kernel<18>, 18);
+    } else {
+        const size_t smem = (size_t)(4096 + kSchurTri * kSchurThreads) * sizeof(double);
+        ensure_func_attr((const void*)block_schur_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        block_schur_kernel<<<(nblocks + kSchurThreads - 1) / kSchurThreads, kSchurThreads, smem, s>>>(
+            plane, out, h, w, masks, nblocks, status);
+    }
     CUDA_CHECK(cudaGetLastError());
 }
 

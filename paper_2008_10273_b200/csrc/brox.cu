@@ -23,7 +23,12 @@
 #include <cstdlib>
 #include <vector>
 
+#include <map>
+#include <mutex>
+#include <tuple>
+
 #include "brox.h"
+#include "func_attr.h"
 #include "inpaint.h"
 
 namespace hivc {
@@ -457,10 +462,41 @@ struct JcPlan {
     int rpc = 0, ctas = 0;
     size_t smem = 0;
 };
+// Whether one cluster of `ctas` CTAs with `smem` bytes each can be resident
+// on this device (cudaOccupancyMaxActiveClusters), cached per device.
+static bool jc_cluster_fits(int ctas, size_t smem) {
+    static std::mutex mu;
+    static std::map<std::tuple<int, int, size_t>, bool> cache;
+    int dev = 0;
+    CUDA_CHECK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    const auto key = std::make_tuple(dev, ctas, smem);
+    auto f = cache.find(key);
+    if (f != cache.end()) return f->second;
+    ensure_func_attr((const void*)jacobi_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    ensure_func_attr((const void*)jacobi_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(ctas);
+    cfg.blockDim = dim3(kJCNT);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = ctas;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    const bool ok = cudaOccupancyMaxActiveClusters(&n, jacobi_cluster_kernel, &cfg) == cudaSuccess && n > 0;
+    cudaGetLastError();  // (a rejected query leaves no sticky error)
+    cache[key] = ok;
+    return ok;
+}
+
 static JcPlan jc_plan(int h, int w) {
     JcPlan p;
     static const int max_px = [] {
-        const char* e = std::getenv("HIVC_BROX_JC_MAX");
+        const char* e = debug_opt("brox_jc_max");
         return e ? std::atoi(e) : kJCMaxCtas * kJCBand;
     }();
     if ((long long)h * w > max_px || w > kJCBand) return p;
@@ -469,21 +505,18 @@ static JcPlan jc_plan(int h, int w) {
     if ((long long)rpc * w > kJCBand) return p;
     const size_t smem = (size_t)(4 * kJCBand + 4 * (rpc + 2) * w) * sizeof(double);
     if (smem > 200 * 1024) return p;
+    const int nctas = (h + rpc - 1) / rpc;
+    if (!jc_cluster_fits(nctas, smem)) return p;  // then the per-sweep launches run
     p.rpc = rpc;
-    p.ctas = (h + rpc - 1) / rpc;
+    p.ctas = nctas;
     p.smem = smem;
     return p;
 }
 
 static void launch_jacobi_cluster(const JcPlan& jp, const Sys& S, const double* du, const double* dv, double* du2,
                                   double* dv2, int h, int w, double alpha, int iters, cudaStream_t s) {
-    static const bool init = [] {
-        CUDA_CHECK(cudaFuncSetAttribute(jacobi_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        CUDA_CHECK(cudaFuncSetAttribute(jacobi_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        200 * 1024));
-        return true;
-    }();
-    (void)init;
+    ensure_func_attr((const void*)jacobi_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    ensure_func_attr((const void*)jacobi_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(jp.ctas);
     cfg.blockDim = dim3(kJCNT);
@@ -579,7 +612,7 @@ static void set_taps(Taps& T, int& radius, const double* host_taps, int ntaps) {
 // pyramid 0.95: 242 ms per pair -> 234 ms; on smaller levels it does not pay)
 static int jacobi2_min_px() {
     static const int v = [] {
-        const char* e = std::getenv("HIVC_BROX_J2_MIN");
+        const char* e = debug_opt("brox_j2_min");
         return e ? std::atoi(e) : (1 << 20);
     }();
     return v;
@@ -715,7 +748,7 @@ void brox_flow(BroxWorkspace& ws, cudaStream_t s, const double* frame_t, const d
     }
     ws.reserve(h, w, levels_px);
     static const bool use_graph = [] {
-        const char* e = std::getenv("HIVC_BROX_GRAPH");
+        const char* e = debug_opt("brox_graph");
         return !(e && e[0] == '0');
     }();
     if (!use_graph) {
@@ -738,8 +771,16 @@ void brox_flow(BroxWorkspace& ws, cudaStream_t s, const double* frame_t, const d
         int64_t n = 0;
         cudaGraph_t g;
         CUDA_CHECK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-        enqueue_brox(ws, s, shapes, lofs, levels_px, io, io + N, h, w, P, taps_pre, ntaps_pre, taps_aa, ntaps_aa,
-                     io + 2 * N, io + 3 * N, &n);
+        try {
+            enqueue_brox(ws, s, shapes, lofs, levels_px, io, io + N, h, w, P, taps_pre, ntaps_pre, taps_aa, ntaps_aa,
+                         io + 2 * N, io + 3 * N, &n);
+        } catch (...) {  // leave the stream out of capture mode before reporting the error
+            cudaGraph_t bad = nullptr;
+            cudaStreamEndCapture(s, &bad);
+            if (bad) cudaGraphDestroy(bad);
+            cudaGetLastError();
+            throw;
+        }
         CUDA_CHECK(cudaStreamEndCapture(s, &g));
         CUDA_CHECK(cudaGraphInstantiate(&ws.exec, g, 0));
         CUDA_CHECK(cudaGraphDestroy(g));

@@ -17,12 +17,13 @@
 
 constexpr int kTileRows = 32;
 constexpr int kTileThreads = 512;
+constexpr int kTileCols = kTileThreads;  // thread c owns column c of its tile
 
 struct TileBatch {
     CgParams P[kMaxBatch];
     const double* setup[kMaxBatch];
     int nt;                // tiles per solve
-    unsigned int* ticket;  // see BandBatch
+    unsigned int* ticket;  // nullable: CTAs take (solve, tile) = divmod(ticket, nt) in start order
 };
 
 __global__ void __launch_bounds__(kTileThreads, 1) cg_tile_kernel(const __grid_constant__ TileBatch B) {

@@ -39,9 +39,36 @@ inline uint32_t rd_u32(const uint8_t* p) {
 }
 
 
+// Host parse time per stage: summed seconds (every occurrence, all threads)
+// and the occurrences' intervals (absolute now_s() times) for the stage's
+// wall-clock share (codec.py:509-562 stage semantics, see decode_streams).
 struct HostTimes {
     double intra_parse = 0, flow_parse = 0, residual_parse = 0;
+    std::vector<std::pair<double, double>> iv[3];  // intra, flow, residual
+    void add(const HostTimes& o) {
+        intra_parse += o.intra_parse;
+        flow_parse += o.flow_parse;
+        residual_parse += o.residual_parse;
+        for (int k = 0; k < 3; ++k) iv[k].insert(iv[k].end(), o.iv[k].begin(), o.iv[k].end());
+    }
 };
+
+// Length of the union of intervals.
+double union_length(std::vector<std::pair<double, double>> v) {
+    std::sort(v.begin(), v.end());
+    double tot = 0, a = 0, b = -1e300;
+    for (auto& x : v) {
+        if (x.first > b) {
+            if (b > a) tot += b - a;
+            a = x.first;
+            b = x.second;
+        } else {
+            b = std::max(b, x.second);
+        }
+    }
+    if (b > a) tot += b - a;
+    return tot;
+}
 
 // Frame records of one GOP payload, parsed one at a time (codec.decode's frame
 // loop, codec.py:496-556; record layout bitstream.py:157-196).
@@ -73,11 +100,15 @@ struct GopCursor {
         J.type = ftype;
         if (ftype == 0) {
             used = parse_intra(pd, plen, 0, hd.height, hd.width, hd.channels, hd.intra_levels, J.intra, bits);
-            ht.intra_parse += now_s() - t0;
+            const double t1 = now_s();
+            ht.intra_parse += t1 - t0;
+            ht.iv[0].push_back({t0, t1});
         } else {
             if (fi == 0) fail(HIVC_E_CODEC, "group " + gs + " starts with an inter frame");
             used = parse_flow(pd, plen, 0, hd.height, hd.width, hd.flow_levels, J.flow);
-            ht.flow_parse += now_s() - t0;
+            const double t1 = now_s();
+            ht.flow_parse += t1 - t0;
+            ht.iv[1].push_back({t0, t1});
         }
         if (used != plen) fail(HIVC_E_CODEC, "prediction payload length mismatch in group " + gs);
         if (pos + 4 > n) fail(HIVC_E_TRUNCATED, "frame record cut short in group " + gs);
@@ -86,7 +117,9 @@ struct GopCursor {
         if (pos + rlen > n) fail(HIVC_E_TRUNCATED, "residual payload cut short in group " + gs);
         t0 = now_s();
         used = parse_residual(p + pos, rlen, 0, hd.height, hd.width, hd.channels, J.res);
-        ht.residual_parse += now_s() - t0;
+        const double t1 = now_s();
+        ht.residual_parse += t1 - t0;
+        ht.iv[2].push_back({t0, t1});
         if (used != rlen) fail(HIVC_E_CODEC, "residual payload length mismatch in group " + gs);
         pos += rlen;
     }
@@ -382,12 +415,19 @@ struct EvRec {
 };
 using EvPairs = std::vector<EvRec>;
 
-double drain(EvPairs& v, cudaEvent_t origin, char kind, int lane, std::string* timeline) {
+double drain(EvPairs& v, cudaEvent_t origin, char kind, int lane, std::string* timeline,
+             std::vector<std::pair<double, double>>* iv = nullptr) {
     double t = 0;
     for (auto& e : v) {
         float ms = 0;
         cudaEventElapsedTime(&ms, e.first, e.second);
         t += ms * 1e-3;
+        if (iv) {
+            float a = 0, b = 0;
+            cudaEventElapsedTime(&a, origin, e.first);
+            cudaEventElapsedTime(&b, origin, e.second);
+            iv->push_back({a * 1e-3, b * 1e-3});
+        }
         if (timeline) {
             float a = 0, b = 0;
             cudaEventElapsedTime(&a, origin, e.first);
@@ -738,8 +778,10 @@ void intra_phase(CallState& cs, Item& it) {
             HostTimes ht;
             cur.parse(L.jobs[0], ht, bits);  // frame 0 must be intra (codec.py:503)
             if (it.nf == 1) cur.finish();
-            it.ht.intra_parse += ht.intra_parse;
-            it.ht.residual_parse += ht.residual_parse;
+            {
+                std::lock_guard<std::mutex> lk0(*it.mu);
+                it.ht.add(ht);
+            }
             FrameOffsets o[1];
             std::vector<double> qt(255);  // s * dz_step / 127 for |s| <= 127 (quantize.py:43-47, codec.py:316-321)
             const double dz = 127.0 / (double)((hd.residual_levels - 1) / 2);
@@ -769,7 +811,7 @@ void intra_phase(CallState& cs, Item& it) {
         if (it.code == HIVC_OK && it.solve0) g.ready.push_back(self);
         --g.pending;
         static const int min_batch = [] {
-            const char* e = std::getenv("HIVC_MIN_BATCH");
+            const char* e = debug_opt("min_batch");
             return e ? std::max(1, std::atoi(e)) : kMinBatch;
         }();
         // (never leave a lone straggler behind a batch: its cluster levels could
@@ -829,9 +871,7 @@ void frame_task(CallState& cs, Item& it, int fi) {
     {
         std::lock_guard<std::mutex> lk(*it.mu);
         it.parsed[fi] = 1;
-        it.ht.intra_parse += ht.intra_parse;
-        it.ht.flow_parse += ht.flow_parse;
-        it.ht.residual_parse += ht.residual_parse;
+        it.ht.add(ht);
     }
     try_launch(cs, it);
 }
@@ -921,7 +961,7 @@ void decode_streams(Context& ctx, int nstreams, const uint8_t* const* data, cons
         if (L.jobs.size() < nrec) L.jobs.resize(nrec);
         items[i].parsed.assign(std::max<size_t>(nrec, 1), 0);
     }
-    const bool timed = (stage_seconds != nullptr && ctx.stage_events) || std::getenv("HIVC_TIMELINE");
+    const bool timed = (stage_seconds != nullptr && ctx.stage_events) || debug_opt("timeline");
     cudaEvent_t origin;
     CUDA_CHECK(cudaEventCreate(&origin));
     CUDA_CHECK(cudaEventRecord(origin, ctx.stream));
@@ -960,7 +1000,7 @@ void decode_streams(Context& ctx, int nstreams, const uint8_t* const* data, cons
         }
     };
     static const int kMaxWorkers = [] {
-        const char* e = std::getenv("HIVC_WORKERS");
+        const char* e = debug_opt("workers");
         const int hw = (int)std::max(2u, std::thread::hardware_concurrency());
         // half the hardware threads: each large I-frame parse also runs tree
         // and value helper threads (measured on 16 cores: 8 workers beat 16 by 3 %)
@@ -987,13 +1027,14 @@ void decode_streams(Context& ctx, int nstreams, const uint8_t* const* data, cons
     }
     cudaStreamSynchronize(ctx.solver);
     std::string timeline;
-    std::string* tl = std::getenv("HIVC_TIMELINE") ? &timeline : nullptr;
+    std::string* tl = debug_opt("timeline") ? &timeline : nullptr;
     double gpu_intra = 0, gpu_inter = 0, gpu_ifin = 0;
+    std::vector<std::pair<double, double>> dev_iv[3];  // solves, P frames, I-frame finalize (s from origin)
     for (int i = 0; i < n; ++i) {
         Item& it = items[i];
-        gpu_intra += drain(it.ev_intra, origin, 'I', i, tl);
-        gpu_inter += drain(it.ev_inter, origin, 'P', i, tl);
-        gpu_ifin += drain(it.ev_ifin, origin, 'F', i, tl);
+        gpu_intra += drain(it.ev_intra, origin, 'I', i, tl, &dev_iv[0]);
+        gpu_inter += drain(it.ev_inter, origin, 'P', i, tl, &dev_iv[1]);
+        gpu_ifin += drain(it.ev_ifin, origin, 'F', i, tl, &dev_iv[2]);
         if (tl) {  // item completion (incl. its last D2H copy in host-output mode)
             float d = 0;
             cudaEventElapsedTime(&d, origin, it.done);
@@ -1011,7 +1052,7 @@ void decode_streams(Context& ctx, int nstreams, const uint8_t* const* data, cons
     }
     cudaEventDestroy(origin);
     if (tl) {
-        if (FILE* f = std::fopen(std::getenv("HIVC_TIMELINE"), "a")) {
+        if (FILE* f = std::fopen(debug_opt("timeline"), "a")) {
             std::fputs(timeline.c_str(), f);
             std::fprintf(f, "-\n");
             std::fclose(f);
@@ -1057,14 +1098,31 @@ void decode_streams(Context& ctx, int nstreams, const uint8_t* const* data, cons
             ctx.d2h_bytes += it.d2h;
             ctx.inter_frames += it.inter_frames;
             ctx.intra_frames += it.intra_frames;
-            ht.intra_parse += it.ht.intra_parse;
-            ht.flow_parse += it.ht.flow_parse;
-            ht.residual_parse += it.ht.residual_parse;
+            ht.add(it.ht);
         }
         ctx.inter_seconds += gpu_inter;
     }
     if (stage_seconds) {
-        double s[8] = {ht.intra_parse + gpu_intra, ht.flow_parse, gpu_inter, ht.residual_parse, gpu_ifin, 0, 0, 0};
+        // The reference times its stages one after another (codec.py:509-562);
+        // here they overlap across GOPs, host threads and streams.  Each stage
+        // reports its wall-clock share: the union of its occurrences'
+        // intervals (so no stage exceeds `total`):
+        //   intra_solve        host intra-payload parse + the batched device solves
+        //   flow_parse         host flow-payload parse
+        //   warp               the fused P-frame kernels (warp + residual + rint/clip)
+        //   residual_parse     host residual-payload parse
+        //   residual_transform the I-frame finalize kernels (block rebuild + add + rint/clip)
+        //   finalize           0 here: fused into the two kernels above (codec.decode adds the
+        //                      host Frame construction)
+        auto rel = [&](const std::vector<std::pair<double, double>>& v) {
+            std::vector<std::pair<double, double>> r;
+            for (auto& x : v) r.push_back({x.first - cs.t0, x.second - cs.t0});
+            return r;
+        };
+        std::vector<std::pair<double, double>> intra = rel(ht.iv[0]);
+        intra.insert(intra.end(), dev_iv[0].begin(), dev_iv[0].end());
+        double s[8] = {union_length(intra), union_length(rel(ht.iv[1])), union_length(dev_iv[1]),
+                       union_length(rel(ht.iv[2])), union_length(dev_iv[2]), 0, 0, 0};
         s[6] = now_s() - t_all;
         s[7] = span;
         std::memcpy(stage_seconds, s, sizeof(s));

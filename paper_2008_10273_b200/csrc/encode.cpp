@@ -236,7 +236,7 @@ thread_local std::vector<double> t_buf;
 constexpr int64_t kParMin = 1 << 16;
 int enc_threads() {
     static const int n = [] {
-        const char* e = std::getenv("HIVC_ENC_THREADS");
+        const char* e = debug_opt("enc_threads");
         int v = e ? std::atoi(e) : 8;
         return std::max(1, std::min(v, (int)std::max(1u, std::thread::hardware_concurrency())));
     }();

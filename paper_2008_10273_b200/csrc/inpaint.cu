@@ -102,7 +102,7 @@ struct CgParams {
     int band_rows;
     double* ex_r;  // [nbands][2][w]: first/last owned row of r
     double* ex_p;  // [2 parity][nbands][2][w]: first/last owned row of p
-    int x_rows = 0;  // band2 / tile: leading rows whose x lives in shared memory (the rest streams)
+    int x_rows = 0;  // tile: leading rows whose x lives in shared memory (the rest streams)
     // tile kernel: tiles of band_rows x tile_cols, ntc tiles per row of tiles
     int tile_cols = 0, ntc = 1;
     unsigned long long* trace = nullptr;  // diagnostics: per-iteration phase timestamps of CTA 0
@@ -385,10 +385,8 @@ __global__ void __launch_bounds__(kThreads, 1) cg_level_kernel(CgParams P) {
     }
 }
 
-#include "cg_band.cuh"
-#include "cg_band2.cuh"
+#include "cg_setup.cuh"
 #include "cg_tile.cuh"
-#include "cg_small.cuh"
 #include "cg_cluster.cuh"
 #include "cg_cluster_col.cuh"
 
@@ -454,64 +452,39 @@ void InpaintWorkspace::reserve(int h, int w, int dev) {
     CUDA_CHECK(cudaMemset(bar, 0, 64 * sizeof(unsigned int)));
     CUDA_CHECK(cudaMalloc(&iters, 64 * sizeof(int)));
     CUDA_CHECK(cudaMalloc(&margins, 64 * sizeof(double)));
-    // band-kernel row exchange: r (nb x 2 rows) + p (2 parities x nb x 2 rows)
-    ex_cap = (size_t)6 * std::max(num_sms, 1) * w;
+    // tile-kernel edge exchange: r + 2 parities of p, every tile's perimeter
+    ex_cap = (size_t)3 * std::max(num_sms, 1) * (2 * (size_t)kTileCols + 2 * (size_t)kTileRows);
     CUDA_CHECK(cudaMalloc(&ex, ex_cap * sizeof(double)));
     cap_px = n;
     cap_w = w;
     cap_coarse = coarse;
-    const char* env = getenv("HIVC_CG_BAND");
-    band_enabled = !(env && env[0] == '0');
-    band_variant = (env && env[0] == '1') ? 1 : 2;
-    CUDA_CHECK(cudaFuncSetAttribute(cg_band2_kernel<4, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBand2Smem));
-    CUDA_CHECK(cudaFuncSetAttribute(cg_band2_kernel<8, 4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBand2Smem));
-    CUDA_CHECK(cudaFuncSetAttribute(cg_band2_kernel<kPackRows, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    kBand2Smem));
-    CUDA_CHECK(cudaFuncSetAttribute(cg_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kBand2Smem));
-    const char* env_clmax = getenv("HIVC_CL_MAXPX");
-    cluster_max_px = env_clmax ? (size_t)atoll(env_clmax) : (size_t)1 << 40;
-    const char* env_tile = getenv("HIVC_CG_TILE");
-    tile_enabled = !(env_tile && env_tile[0] == '0');
-    const char* env_pack = getenv("HIVC_CG_PACK");
-    pack_env_off = env_pack && env_pack[0] == '0';
-    if (env_pack && env_pack[0] == '2') pack_bands = true;  // experiments: throughput mode for single solves too
-    const char* env_small = getenv("HIVC_CG_SMALL");
-    small_enabled = !(env_small && env_small[0] == '0');
-    CUDA_CHECK(cudaFuncSetAttribute(cg_band_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    CUDA_CHECK(cudaFuncSetAttribute(cg_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    // 16-CTA clusters (non-portable size) for the coarse/mid levels
-    const char* env_cl = getenv("HIVC_CG_CLUSTER");
-    cluster_ok = !(env_cl && env_cl[0] == '0');
+    CUDA_CHECK(cudaFuncSetAttribute(cg_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmem));
+    // 16-CTA clusters (non-portable size) for the coarse/mid levels, when this device can host one
+    cluster_ok = cudaFuncSetAttribute(cg_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+                     cudaSuccess &&
+                 cudaFuncSetAttribute(cg_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) ==
+                     cudaSuccess;
     if (cluster_ok) {
-        cluster_ok = cudaFuncSetAttribute(cg_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
-                         cudaSuccess &&
-                     cudaFuncSetAttribute(cg_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          200 * 1024) == cudaSuccess;
-        if (cluster_ok) {
-            cudaLaunchConfig_t cfg = {};
-            cfg.gridDim = dim3(kClusterSize);
-            cfg.blockDim = dim3(kClThreads);
-            cfg.dynamicSmemBytes = 200 * 1024;
-            cudaLaunchAttribute attr[1];
-            attr[0].id = cudaLaunchAttributeClusterDimension;
-            attr[0].val.clusterDim.x = kClusterSize;
-            attr[0].val.clusterDim.y = 1;
-            attr[0].val.clusterDim.z = 1;
-            cfg.attrs = attr;
-            cfg.numAttrs = 1;
-            int nclusters = 0;
-            cluster_ok = cudaOccupancyMaxActiveClusters(&nclusters, cg_cluster_kernel, &cfg) == cudaSuccess &&
-                         nclusters > 0;
-        }
-        if (cluster_ok)
-            cluster_ok = cudaFuncSetAttribute(cg_cluster_col_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed,
-                                              1) == cudaSuccess &&
-                         cudaFuncSetAttribute(cg_cluster_col_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              200 * 1024) == cudaSuccess;
-        cudaGetLastError();  // clear a rejected attribute
-        const char* env_col = getenv("HIVC_CG_CLUSTER_COL");
-        cluster_col = !(env_col && env_col[0] == '0');
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(kClusterSize);
+        cfg.blockDim = dim3(kClThreads);
+        cfg.dynamicSmemBytes = 200 * 1024;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = kClusterSize;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int nclusters = 0;
+        cluster_ok = cudaOccupancyMaxActiveClusters(&nclusters, cg_cluster_kernel, &cfg) == cudaSuccess && nclusters > 0;
     }
+    if (cluster_ok)
+        cluster_ok = cudaFuncSetAttribute(cg_cluster_col_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+                         cudaSuccess &&
+                     cudaFuncSetAttribute(cg_cluster_col_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          200 * 1024) == cudaSuccess;
+    cudaGetLastError();  // clear a rejected attribute
 }
 
 void InpaintWorkspace::release() {
@@ -540,18 +513,6 @@ int solve_homogeneous_async(InpaintWorkspace& ws, cudaStream_t s, const double* 
 
 namespace {
 
-// band2 dynamic shared memory: padded p for a ROWS-row band, then as many x
-// rows as fit (CgParams::x_rows, set here) — those never touch global memory.
-size_t band2_smem(int rows_tpl, int band_rows, int w, CgParams* P, int K) {
-    const size_t p_bytes = (size_t)(rows_tpl + 2) * (w + 2) * sizeof(double);
-    const char* e = getenv("HIVC_CG_XRES");
-    int xr = 0;
-    if (!(e && e[0] == '0') && p_bytes < (size_t)kBand2Smem)
-        xr = (int)std::min<size_t>((size_t)band_rows, ((size_t)kBand2Smem - p_bytes) / ((size_t)w * sizeof(double)));
-    for (int j = 0; j < K; ++j) P[j].x_rows = xr;
-    return p_bytes + (size_t)xr * w * sizeof(double);
-}
-
 // 2-D tile layout of a grid level for cg_tile_kernel: at most `budget` tiles
 // of <= kTileRows rows x <= 512 columns, p + as many x rows as fit in smem.
 struct TilePlan {
@@ -569,11 +530,8 @@ TilePlan plan_tiles(int h, int w, int budget) {
     if (trows > kTileRows || trows < 1) return T;
     const int ntr = (h + trows - 1) / trows;
     const size_t p_bytes = (size_t)(trows + 2) * (tcols + 2) * sizeof(double);
-    if (p_bytes > (size_t)kBand2Smem) return T;
-    const char* e = getenv("HIVC_CG_XRES");
-    int xr = 0;
-    if (!(e && e[0] == '0'))
-        xr = (int)std::min<size_t>((size_t)trows, ((size_t)kBand2Smem - p_bytes) / ((size_t)tcols * sizeof(double)));
+    if (p_bytes > (size_t)kTileSmem) return T;
+    const int xr = (int)std::min<size_t>((size_t)trows, ((size_t)kTileSmem - p_bytes) / ((size_t)tcols * sizeof(double)));
     T.ok = true;
     T.trows = trows;
     T.tcols = tcols;
@@ -667,7 +625,7 @@ int solve_batch_async(const SolveJob* jobs, int K, int h, int w, double tol, int
             cm += nl;
         }
     }
-    const bool bt = probe && getenv("HIVC_BATCH_TRACE");
+    const bool bt = probe && debug_opt("batch_trace");
     auto mb = [&](const std::string& label, cudaStream_t st) {
         if (bt) probe->mark_begin(st, label + " K=" + std::to_string(K) + " " + std::to_string(h) + "x" + std::to_string(w));
     };
@@ -706,7 +664,6 @@ int solve_batch_async(const SolveJob* jobs, int K, int h, int w, double tol, int
             const size_t need =
                 ((size_t)(br + 2) * (ww + 2) + (size_t)br * ww + 6 * (size_t)ww) * sizeof(double) + (size_t)br * ww;
             if ((size_t)br * ww > (size_t)kClPx * kClThreads || ww > kClMaxW || need > 200 * 1024) break;
-            if ((size_t)hh * ww > ws0.cluster_max_px) break;  // larger levels go to the tile kernel
             for (int j = 0; j < K; ++j) {
                 ClusterLevels& S = CB.S[j];
                 S.h[nlev] = hh;
@@ -730,13 +687,13 @@ int solve_batch_async(const SolveJob* jobs, int K, int h, int w, double tol, int
                 S.max_iter = max_iter;
                 S.trace = nullptr;
             }
-            if (getenv("HIVC_CG_TRACE_CLUSTER") && K == 1) {
+            if (debug_opt("cg_trace_cluster") && K == 1) {
                 if (!ws0.trace) CUDA_CHECK(cudaMalloc(&ws0.trace, kTraceLen * sizeof(unsigned long long)));
                 CUDA_CHECK(cudaMemsetAsync(ws0.trace, 0, kTraceLen * sizeof(unsigned long long), sp));
                 CB.S[0].trace = ws0.trace;
             }
             // column-walk variant when every band is <= kColRows x kClThreads
-            bool col = ws0.cluster_col;
+            bool col = true;
             for (int i = 0; i < nlev && col; ++i)
                 col = CB.S[0].w[i] <= kClThreads && (CB.S[0].h[i] + kClusterSize - 1) / kClusterSize <= kColRows;
             cudaLaunchConfig_t cfg = {};
@@ -761,37 +718,6 @@ int solve_batch_async(const SolveJob* jobs, int K, int h, int w, double tol, int
             l_start = l;
         }
     }
-    if (ws0.small_enabled && l_start == L - 1) {
-        int l_end = l_start;
-        for (int j = 0; j < K; ++j) {
-            SmallLevels S{};
-            size_t smem = 0;
-            int l = L - 1;
-            while (l >= 0 && (size_t)shapes[l].first * shapes[l].second <= (size_t)kSmallMaxPx &&
-                   S.nlev < kSmallMaxLevels) {
-                const int i = S.nlev++;
-                S.h[i] = shapes[l].first;
-                S.w[i] = shapes[l].second;
-                S.f[i] = J[j].f[l];
-                S.m[i] = J[j].m[l];
-                S.u[i] = J[j].u[l];
-                S.iters[i] = jobs[j].ws->iters + (L - 1 - l);
-                const size_t n = (size_t)S.h[i] * S.w[i];
-                smem = std::max(smem, ((size_t)(S.h[i] + 2) * (S.w[i] + 2) + n) * sizeof(double) + n);
-                --l;
-            }
-            if (S.nlev > 0) {
-                S.last_is_finest = l < 0;
-                S.tol = tol;
-                S.max_iter = max_iter;
-                cg_small_kernel<<<1, kSmallThreads, smem, sp>>>(S);
-                ++*launches;
-                CUDA_CHECK(cudaGetLastError());
-            }
-            l_end = l;
-        }
-        l_start = l_end;
-    }
     if (sp != s) {  // the grid levels (and the caller's next work on s) follow the side-stream levels
         if (!ws0.pre_done) CUDA_CHECK(cudaEventCreateWithFlags(&ws0.pre_done, cudaEventDisableTiming));
         CUDA_CHECK(cudaEventRecord(ws0.pre_done, sp));
@@ -803,23 +729,16 @@ int solve_batch_async(const SolveJob* jobs, int K, int h, int w, double tol, int
         for (int j = 0; j < K; ++j) P[j] = level_params(J[j], *jobs[j].ws, shapes, l, tol, max_iter);
         const int hh = P[0].h, ww = P[0].w;
         const bool grid = !(P[0].n <= kSingleCtaMaxPx || ws0.grid_ctas == 0);
-        // on-chip band kernel when a band fits registers + shared memory
-        const int kc = (ww + kBandThreads - 1) / kBandThreads;
-        int band_rows = (hh + ws0.num_sms - 1) / std::max(ws0.num_sms, 1);
-        const bool pack = ws0.pack_bands && !ws0.pack_env_off && ws0.band_variant == 2 && kc <= 2 &&
-                          band_rows <= kPackRows;
-        if (pack) band_rows = kPackRows;
-        const int nbands = (hh + band_rows - 1) / band_rows;
-        const size_t band_smem = (size_t)(kBandRows + 2) * (ww + 2) * sizeof(double) + (size_t)kBandRows * ww;
-        const bool band = grid && ws0.band_enabled && P[0].uc != nullptr && (pack || band_rows <= kBandRows) &&
-                          ww <= kBandCols * kBandThreads && band_smem <= 220 * 1024 && nbands <= ws0.num_sms;
-        // 2-D tiles (default for band levels): packed solves share the SMs,
-        // at most 4 side by side (a lone solve gets the whole GPU)
+        // on-chip 2-D tile kernel (every level above the cluster levels of the
+        // benchmark pyramids); packed solves share the SMs, at most 4 side by
+        // side (a lone solve gets the whole GPU); other shapes: the streaming
+        // grid kernel, or one CTA for the small ones
+        const int kc = (ww + kTileCols - 1) / kTileCols;
         const int waves = (K + 3) / 4;
         const int side = (K + waves - 1) / waves;  // even waves: 5 solves -> 3 + 2, not 4 + 1
-        const bool pack_t = ws0.pack_bands && !ws0.pack_env_off && kc <= 2 && side > 1;
+        const bool pack_t = ws0.pack_bands && kc <= 2 && side > 1;
         const TilePlan TP = plan_tiles(hh, ww, pack_t ? ws0.num_sms / side : ws0.num_sms);
-        const bool tile = band && ws0.tile_enabled && TP.ok && TP.ex <= ws0.ex_cap;
+        const bool tile = grid && P[0].uc != nullptr && TP.ok && TP.ex <= ws0.ex_cap;
         CgProbe::Launch rec{};
         if (probe && grid) {
             rec.stamp_base = probe->next_stamp;
@@ -855,7 +774,7 @@ int solve_batch_async(const SolveJob* jobs, int K, int h, int w, double tol, int
                 TB.P[j] = P[j];
                 TB.setup[j] = ws.partials + 4096;
             }
-            if (getenv("HIVC_CG_TRACE") && l == 0 && K == 1) {
+            if (debug_opt("cg_trace") && l == 0 && K == 1) {
                 if (!ws0.trace) CUDA_CHECK(cudaMalloc(&ws0.trace, kTraceLen * sizeof(unsigned long long)));
                 CUDA_CHECK(cudaMemsetAsync(ws0.trace, 0, kTraceLen * sizeof(unsigned long long), s));
                 SB.P[0].trace = TB.P[0].trace = ws0.trace;
@@ -894,76 +813,6 @@ int solve_batch_async(const SolveJob* jobs, int K, int h, int w, double tol, int
                     }
                 }
             }
-        } else if (band) {
-            SetupBatch SB{};
-            BandBatch BB{};
-            for (int j = 0; j < K; ++j) {
-                InpaintWorkspace& ws = *jobs[j].ws;
-                P[j].band_rows = band_rows;
-                P[j].ex_r = ws.ex;
-                P[j].ex_p = ws.ex + (size_t)2 * nbands * ww;
-                SB.P[j] = P[j];
-                SB.partials[j] = ws.partials + 4096;
-                BB.P[j] = P[j];
-                BB.setup[j] = ws.partials + 4096;
-            }
-            if (getenv("HIVC_CG_TRACE") && l == 0 && K == 1) {
-                if (!ws0.trace) CUDA_CHECK(cudaMalloc(&ws0.trace, kTraceLen * sizeof(unsigned long long)));
-                CUDA_CHECK(cudaMemsetAsync(ws0.trace, 0, kTraceLen * sizeof(unsigned long long), s));
-                SB.P[0].trace = BB.P[0].trace = ws0.trace;
-            }
-            unsigned int* ticket = ws0.bar + 32;
-            SB.ticket = pack && K > 1 ? ticket : nullptr;  // setup resets the barrier counters + ticket
-            mb("setup l=" + std::to_string(l), s);
-            cg_setup_x_kernel<<<dim3(kSetupCtas, K), 512, 0, s>>>(SB);
-            cg_setup_kernel<<<dim3(kSetupCtas, K), 512, 0, s>>>(SB);
-            me(s);
-            *launches += 2;
-            mb(std::string(pack && K > 1 ? "band-ticket" : "band-coop") + " l=" + std::to_string(l) + " nb=" +
-                   std::to_string(nbands),
-               s);
-            rec_begin();
-            if (pack && K > 1) {
-                // several solves side by side: ticketed plain launch (see BandBatch)
-                BB.nb = nbands;
-                BB.ticket = ticket;
-                const size_t smem_b = band2_smem(kPackRows, band_rows, ww, BB.P, K);
-                cg_band2_kernel<kPackRows, 2, false><<<nbands * K, kBandThreads, smem_b, s>>>(BB);
-                ++*launches;
-            } else {
-                for (int j = 0; j < K; ++j) {
-                    if (ws0.band_variant == 2) {
-                        BandBatch one{};
-                        one.P[0] = BB.P[j];
-                        one.setup[0] = BB.setup[j];
-                        one.nb = nbands;
-                        one.ticket = nullptr;
-                        const void* fn;
-                        size_t smem_b;
-                        if (pack) {
-                            smem_b = band2_smem(kPackRows, band_rows, ww, one.P, 1);
-                            fn = (const void*)cg_band2_kernel<kPackRows, 2, false>;
-                        } else {
-                            const bool small = band_rows <= 4 && kc <= 2;
-                            smem_b = band2_smem(small ? 4 : kBandRows, band_rows, ww, one.P, 1);
-                            fn = small ? (const void*)cg_band2_kernel<4, 2, true>
-                                       : (const void*)cg_band2_kernel<8, 4, false>;
-                        }
-                        void* args[] = {&one};
-                        CUDA_CHECK(cudaLaunchCooperativeKernel(fn, dim3(nbands), dim3(kBandThreads), args, smem_b, s));
-                    } else {
-                        const double* setup = BB.setup[j];
-                        void* args[] = {&BB.P[j], &setup};
-                        CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)cg_band_kernel, dim3(nbands),
-                                                               dim3(kBandThreads), args, band_smem, s));
-                    }
-                    ++*launches;
-                    if (l == 0 && jobs[j].done) {  // this solve is complete: its consumer may start now
-                        CUDA_CHECK(cudaEventRecord(jobs[j].done, s));
-                        recorded[j] = true;
-                    }
-                }
-            }
         } else {
             rec_begin();
             for (int j = 0; j < K; ++j) {
@@ -975,7 +824,7 @@ int solve_batch_async(const SolveJob* jobs, int K, int h, int w, double tol, int
             }
         }
         CUDA_CHECK(cudaGetLastError());
-        if (band || tile) me(s);
+        if (tile) me(s);
         if (probe && grid) {
             CUDA_CHECK(cudaEventRecord(rec.stop, s));
             rec.pixels = P[0].n;

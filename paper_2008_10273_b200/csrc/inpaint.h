@@ -29,21 +29,13 @@ struct InpaintWorkspace {
     int num_sms = 0;
     int grid_ctas = 0;  // CTAs of the cooperative (grid-barrier) CG kernel
     size_t cap_px = 0, cap_coarse = 0, cap_w = 0;
-    double* ex = nullptr;       // band-kernel row exchange buffers
+    double* ex = nullptr;       // tile-kernel edge exchange buffers
     unsigned long long* trace = nullptr;  // HIVC_CG_TRACE diagnostics (finest level phase timestamps)
-    bool band_enabled = true;   // HIVC_CG_BAND=0 selects the streaming kernel
-    int band_variant = 2;       // HIVC_CG_BAND=1: row-mapped band kernel; default: column-streaming
-    bool small_enabled = true;  // HIVC_CG_SMALL=0: one single-CTA launch per coarse level instead
-    bool cluster_ok = false;    // 16-CTA cluster kernel for coarse/mid levels (HIVC_CG_CLUSTER=0 disables)
-    bool cluster_col = true;    // its column-walk variant when the bands fit (HIVC_CG_CLUSTER_COL=0 disables)
-    // throughput mode (decode lanes): band levels use the fewest CTAs whose
-    // bands still fit on chip, so solves of several lanes run side by side
-    // (HIVC_CG_PACK=0 disables); latency mode spreads a level over every SM
+    bool cluster_ok = false;    // 16-CTA cluster kernels for the coarse/mid levels (device can host one)
+    // throughput mode (decode lanes): solves of a batch run side by side on the
+    // tile kernel, sharing the SMs; latency mode spreads a level over every SM
     bool pack_bands = false;
-    bool pack_env_off = false;
-    bool tile_enabled = true;  // 2-D tile CG kernel for band levels (HIVC_CG_TILE=0: row bands)
     size_t ex_cap = 0;         // doubles in ex
-    size_t cluster_max_px = (size_t)1 << 40;  // cluster kernel only for levels up to this size
     double* dbl = nullptr;
     uint8_t* bytes = nullptr;
     double* partials = nullptr;

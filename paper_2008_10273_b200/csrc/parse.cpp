@@ -725,11 +725,11 @@ size_t parse_intra(const uint8_t* d, size_t len, size_t pos, int32_t h, int32_t 
     // (the decoder already runs one parse per GOP on its own thread: only the
     // largest planes, whose I-frame parse is on the critical path, fan out)
     static const int kTreeThreads = [] {
-        const char* e = getenv("HIVC_TREE_THREADS");
+        const char* e = debug_opt("tree_threads");
         return e ? std::max(1, atoi(e)) : 3;
     }();
     static const int kTreeThreadsSmall = [] {
-        const char* e = getenv("HIVC_TREE_THREADS_SMALL");
+        const char* e = debug_opt("tree_threads_small");
         return e ? std::max(1, atoi(e)) : 1;
     }();
     const int tree_threads = npx >= (1u << 20) ? std::min(kTreeThreads, kHw)

@@ -18,6 +18,7 @@
 #include "device.cuh"
 #include "inpaint.h"
 #include "recon.h"
+#include "func_attr.h"
 
 namespace hivc {
 
@@ -612,11 +613,7 @@ void launch_block_fit(const double* f, const uint64_t* masks, int n, double* c_o
                       cudaStream_t s) {
     if (n <= 0) return;
     size_t smem = (size_t)kFitWarps * (kFitMaxK + 1) * kFitLd * sizeof(double) + kFitWarps * 64 * sizeof(int);
-    static bool attr = false;
-    if (!attr) {
-        CUDA_CHECK(cudaFuncSetAttribute(block_fit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
+    ensure_func_attr((const void*)block_fit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     block_fit_kernel<<<(n + kFitWarps - 1) / kFitWarps, kFitWarps * 32, smem, s>>>(f, masks, n, c_out, a_out, status);
     CUDA_CHECK(cudaGetLastError());
 }

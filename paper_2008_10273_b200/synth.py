@@ -22,7 +22,7 @@ from __future__ import annotations
 import numpy as np
 
 
-def synth_clip(
+def synth_frames(
     n_frames: int,
     height: int,
     width: int,
@@ -31,8 +31,10 @@ def synth_clip(
     v: float = 3.0,
     seed: int = 0,
     channels: int = 1,
-) -> np.ndarray:
-    """Float32 clip of shape (n_frames, channels, height, width) in [0, 255]."""
+):
+    """Frames of ``synth_clip`` one at a time (same draws, same values): a
+    generator of float32 (channels, height, width) arrays, so long clips
+    (config 4: 480 frames at 1080p) never sit in memory whole."""
     rng = np.random.default_rng(seed)
     bc = np.stack([rng.uniform(0, width, blobs), rng.uniform(0, height, blobs)], axis=1)
     bs = rng.uniform(8.0, 30.0, blobs)
@@ -48,7 +50,6 @@ def synth_clip(
 
     xs = np.arange(width, dtype=np.float64) + 0.5
     ys = np.arange(height, dtype=np.float64) + 0.5
-    out = np.empty((n_frames, channels, height, width), dtype=np.float32)
     for t in range(n_frames):
         acc = np.zeros((channels, height, width))
         for i in range(blobs):
@@ -67,7 +68,23 @@ def synth_clip(
                 acc[c][ind] += rval[i, c]
         for c in range(channels):
             acc[c] += rng.normal(0.0, 2.0, (height, width))
-        out[t] = np.clip(acc, 0.0, 255.0)
+        yield np.clip(acc, 0.0, 255.0).astype(np.float32)
+
+
+def synth_clip(
+    n_frames: int,
+    height: int,
+    width: int,
+    blobs: int = 8,
+    rects: int = 3,
+    v: float = 3.0,
+    seed: int = 0,
+    channels: int = 1,
+) -> np.ndarray:
+    """Float32 clip of shape (n_frames, channels, height, width) in [0, 255]."""
+    out = np.empty((n_frames, channels, height, width), dtype=np.float32)
+    for t, f in enumerate(synth_frames(n_frames, height, width, blobs, rects, v, seed, channels)):
+        out[t] = f
     return out
 
 
@@ -82,6 +99,12 @@ def downsample2(plane: np.ndarray) -> np.ndarray:
     ph, pw = h + (h & 1), w + (w & 1)
     p = np.pad(plane.astype(np.float64), [(0, 0)] * (plane.ndim - 2) + [(0, ph - h), (0, pw - w)], mode="edge")
     return 0.25 * (p[..., 0::2, 0::2] + p[..., 1::2, 0::2] + p[..., 0::2, 1::2] + p[..., 1::2, 1::2])
+
+
+def synth_420_frames(n_frames: int, height: int, width: int, blobs: int, rects: int, v: float, seed: int):
+    """``synth_420`` one frame at a time: yields (Y, Cb, Cr) int32 planes."""
+    for f in synth_frames(n_frames, height, width, blobs, rects, v, seed, channels=3):
+        yield (to_codec_planes(f[0]), to_codec_planes(downsample2(f[1])), to_codec_planes(downsample2(f[2])))
 
 
 def synth_420(n_frames: int, height: int, width: int, blobs: int, rects: int, v: float, seed: int):

@@ -213,3 +213,17 @@ def test_420_three_stream_round_trip():
 def _psnr_arr(a, b):
     d = a.astype(np.float64) - b
     return 10 * np.log10(255.0**2 / max(np.mean(d * d), 1e-12))
+
+
+def test_corrupt_gop_frame_count_raises_reference_error(cfg0_stream):
+    """The reference decodes the 10 records, then raises Truncated("frame record
+    cut short in group 0") (codec.py:497-499); so must the GPU decode, without
+    first sizing 60000 frames of output."""
+    import struct
+
+    from paper_2008_10273_b200 import codec, errors
+
+    d = bytearray(cfg0_stream)
+    struct.pack_into("<H", d, 26, 60000)
+    with pytest.raises(errors.Truncated, match="frame record cut short in group 0"):
+        codec.decode(bytes(d))

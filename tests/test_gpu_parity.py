@@ -238,7 +238,7 @@ def test_flow_brox_vs_oracle_larger():
 
 def test_flow_brox_cluster_sweeps_bit_identical(tmp_path):
     """Small levels run all Jacobi sweeps in one cluster launch; the result must equal
-    the per-sweep launches (HIVC_BROX_JC_MAX=0) bit for bit, with and without the graph."""
+    the per-sweep launches (HIVC_DEBUG=brox_jc_max=0) bit for bit, with and without the graph."""
     import os
     import subprocess
     import sys
@@ -256,7 +256,7 @@ def test_flow_brox_cluster_sweeps_bit_identical(tmp_path):
         "np.save(%r, np.stack([f.u, f.v]))\n"
     ) % (str(Path(__file__).resolve().parent.parent), str(tmp_path / "clip.npy"), str(tmp_path / "uv.npy"))
     for graph in ("1", "0"):
-        env = dict(os.environ, HIVC_BROX_JC_MAX="0", HIVC_BROX_GRAPH=graph)
+        env = dict(os.environ, HIVC_DEBUG=f"brox_jc_max=0,brox_graph={graph}")
         subprocess.run([sys.executable, "-c", code], env=env, check=True, timeout=600)
         uv = np.load(tmp_path / "uv.npy")
         assert np.array_equal(uv[0], ff.u) and np.array_equal(uv[1], ff.v), graph

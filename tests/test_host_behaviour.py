@@ -211,3 +211,16 @@ def test_stream_header_validation_and_gop_framing():
         read_stream(s[:-1])
     with pytest.raises(LengthMismatch):
         read_stream(write_stream(h, [b"\x02\x00abc"]))
+
+
+def test_corrupt_gop_frame_count_sizes_outputs_by_records(cfg0_stream):
+    """A GOP whose u16 frame count is corrupt (60000 instead of 10) must not size
+    the output buffers: frames_shape counts the records that fit."""
+    import struct
+
+    from paper_2008_10273_b200 import codec
+
+    d = bytearray(cfg0_stream)
+    struct.pack_into("<H", d, 26, 60000)  # GOP 0's frame count (22-byte header + u32 length)
+    assert codec.frames_shape(bytes(d))[0] == 10
+    assert codec.frames_shape(cfg0_stream)[0] == 10

@@ -1,10 +1,10 @@
 """Per-phase device timing of the batched I-frame solves of one config-3 decode
-(HIVC_BATCH_TRACE=1 prints one line per phase from the CgProbe marks)."""
+(HIVC_DEBUG=batch_trace prints one line per phase from the CgProbe marks)."""
 import os
 import sys
 from pathlib import Path
 
-os.environ.setdefault("HIVC_BATCH_TRACE", "1")
+os.environ.setdefault("HIVC_DEBUG", "batch_trace")
 import torch  # noqa: E402
 
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))

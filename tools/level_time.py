@@ -1,5 +1,5 @@
 """Time one cascadic solve per plane size with the HIVC_CG_TRACE phase breakdown
-of its finest level (run under HIVC_CG_TRACE=1; HIVC_CG_PACK=2 forces the
+of its finest level (run under HIVC_DEBUG=cg_trace; packed mode is the
 packed band layout for single solves)."""
 import sys
 from pathlib import Path

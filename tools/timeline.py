@@ -1,4 +1,4 @@
-"""Summarise a HIVC_TIMELINE dump (decode.cu): per-lane I-solve windows, P-frame
+"""Summarise a HIVC_DEBUG=timeline=<path> dump (decode.cu): per-lane I-solve windows, P-frame
 busy time and the I-solve concurrency histogram of one decode call.
 
 Usage: python tools/timeline.py tl.csv [block index, default -2]

@@ -1,4 +1,4 @@
-"""Print one decode call of a HIVC_TIMELINE dump per item: host I-parse (H),
+"""Print one decode call of a HIVC_DEBUG=timeline=<path> dump per item: host I-parse (H),
 batched I-solve (I), finalize (F), host P-phase (Q), P-frame kernels (P).
 
 Usage: python tools/timeline2.py tl.csv [call index, default -2]
