@@ -97,15 +97,27 @@ __device__ __forceinline__ double clampd(double v, double lo, double hi) {
     return v > hi ? hi : v;
 }
 
-// Layout: a warp covers 4 horizontally adjacent 8x8 tiles (32 x 8 pixels);
-// lane l owns column l of that strip for all 8 rows, so every load/store row
-// is 32 consecutive pixels, each lane has 8 independent prediction chains in
-// flight (the warp is latency-bound: tile map -> flow value -> 4 gathers),
-// and the coded residual blocks of the 4 tiles are rebuilt side by side by
-// the 4 groups of 8 lanes (lanes 8g..8g+7 for tile g).  2 warps per CTA.
+// Layout: a warp covers kWarpTiles horizontally adjacent 8x8 tiles; each
+// tile gets kLanesTile lanes — lane (column gl, row half rh) owns column gl
+// of the tile for kRowsL rows (rh * kRowsL ...), so every load/store row is
+// consecutive pixels and each lane has kRowsL independent prediction chains
+// in flight (the warp is latency-bound: tile map -> flow value -> 4 gathers).
+// The coded residual blocks of the warp's tiles are rebuilt side by side by
+// the first 8 lanes of each tile's group.
+#ifndef HIVC_FRAME_ROWS
+#define HIVC_FRAME_ROWS 4
+#endif
+constexpr int kRowsL = HIVC_FRAME_ROWS;          // rows per lane (8 or 4)
+constexpr int kLanesTile = 8 * (8 / kRowsL);     // lanes per tile
+constexpr int kWarpTiles = 32 / kLanesTile;
 constexpr int kFrameWarps = 2;
-constexpr int kWarpTiles = 4;
-constexpr int kFrameMinBlocks = 12;  // 2-warp CTAs: <= 80 registers (measured best of 1/8/12/16)
+#ifndef HIVC_FRAME_MIN_BLOCKS
+#define HIVC_FRAME_MIN_BLOCKS 16
+#endif
+// 2-warp CTAs, <= 64 registers.  Measured (ncu, config-3 P frames, 1080p /
+// 540p): 8 rows per lane at <= 80 registers 24.4 / 16.5 us; 4 rows 21.2 /
+// 12.5 us; 2 rows (one tile per warp) 24.0-25.7 / 12.0 us (profiles/r02_summary.md)
+constexpr int kFrameMinBlocks = HIVC_FRAME_MIN_BLOCKS;
 
 template <bool kInter, int C, typename RT>
 __global__ void __launch_bounds__(32 * kFrameWarps, kFrameMinBlocks) frame_kernel(FrameArgs A) {
@@ -114,14 +126,15 @@ __global__ void __launch_bounds__(32 * kFrameWarps, kFrameMinBlocks) frame_kerne
     const int nbx = (w + 7) >> 3;
     const int ty = blockIdx.y;
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int grp = lane >> 3, gl = lane & 7;          // tile within the warp, column within the tile
+    const int grp = lane / kLanesTile, sub = lane % kLanesTile;
+    const int gl = sub & 7, r0 = (sub >> 3) * kRowsL;  // column within the tile, first own row
     const int tx = (blockIdx.x * kFrameWarps + wid) * kWarpTiles + grp;
     const bool tile_ok = tx < nbx;
     const int x = tx * 8 + gl;
     const bool col_ok = tile_ok && x < w;
-    const int y_base = ty * 8;
-    const int rows = min(8, h - y_base);
-    double pred[8][C];
+    const int y_base = ty * 8 + r0;
+    const int rows = min(kRowsL, h - y_base);  // (<= 0: no rows of this lane in a bottom edge tile)
+    double pred[kRowsL][C];
     // ---- prediction
     if (kInter) {
         // the host rasterised each flow tree to tiles: most tiles lie inside one
@@ -138,7 +151,7 @@ __global__ void __launch_bounds__(32 * kFrameWarps, kFrameMinBlocks) frame_kerne
         const double u_tile = mu ? 0.0 : __ldg(vals0 + lu);
         const double v_tile = mv ? 0.0 : __ldg(vals1 + lv);
 #pragma unroll
-        for (int r = 0; r < 8; ++r)
+        for (int r = 0; r < kRowsL; ++r)
 #pragma unroll
             for (int c = 0; c < C; ++c) pred[r][c] = 0.0;
         if (col_ok && !mu && !mv) {
@@ -148,10 +161,10 @@ __global__ void __launch_bounds__(32 * kFrameWarps, kFrameMinBlocks) frame_kerne
             const int x0 = __double2int_rd(sx);  // floor; sx >= 0
             const int x1 = min(x0 + 1, w - 1);
             const double fx = sx - u32_to_d((unsigned)x0);
-            int ra[8], rb[8];
-            double fy[8];
+            int ra[kRowsL], rb[kRowsL];
+            double fy[kRowsL];
 #pragma unroll
-            for (int r = 0; r < 8; ++r) {
+            for (int r = 0; r < kRowsL; ++r) {
                 const double sy = clampd((yd0 + (double)r) + v_tile, 0.0, hm1);
                 const int y0 = __double2int_rd(sy);
                 ra[r] = y0 * w;
@@ -161,9 +174,9 @@ __global__ void __launch_bounds__(32 * kFrameWarps, kFrameMinBlocks) frame_kerne
 #pragma unroll
             for (int c = 0; c < C; ++c) {
                 const RT* __restrict__ p = reinterpret_cast<const RT*>(A.prev[c]);
-                RT t00[8], t01[8], t10[8], t11[8];
+                RT t00[kRowsL], t01[kRowsL], t10[kRowsL], t11[kRowsL];
 #pragma unroll
-                for (int r = 0; r < 8; ++r) {
+                for (int r = 0; r < kRowsL; ++r) {
                     if (r < rows) {
                         t00[r] = __ldg(p + ra[r] + x0);
                         t01[r] = __ldg(p + ra[r] + x1);
@@ -172,7 +185,7 @@ __global__ void __launch_bounds__(32 * kFrameWarps, kFrameMinBlocks) frame_kerne
                     }
                 }
 #pragma unroll
-                for (int r = 0; r < 8; ++r) {
+                for (int r = 0; r < kRowsL; ++r) {
                     if (r >= rows) break;
                     const double w00 = (1 - fy[r]) * (1 - fx), w01 = (1 - fy[r]) * fx, w10 = fy[r] * (1 - fx),
                                  w11 = fy[r] * fx;
@@ -183,9 +196,9 @@ __global__ void __launch_bounds__(32 * kFrameWarps, kFrameMinBlocks) frame_kerne
             // a tile on a leaf boundary: descend both trees for the 8 rows in
             // lockstep (one 8-byte node load per row and tree per level), then
             // the 8 rows' flow values and taps
-            int iu[8], iv[8];  // node -> (at the end) value index per row
+            int iu[kRowsL], iv[kRowsL];  // node -> (at the end) value index per row
 #pragma unroll
-            for (int r = 0; r < 8; ++r) {
+            for (int r = 0; r < kRowsL; ++r) {
                 iu[r] = mu ? su : -1;
                 iv[r] = mv ? sv : -1;
             }
@@ -194,14 +207,14 @@ __global__ void __launch_bounds__(32 * kFrameWarps, kFrameMinBlocks) frame_kerne
             bool more = true;
             while (more) {
                 more = false;
-                int2 e0[8], e1[8];
+                int2 e0[kRowsL], e1[kRowsL];
 #pragma unroll
-                for (int r = 0; r < 8; ++r) {
+                for (int r = 0; r < kRowsL; ++r) {
                     e0[r] = iu[r] >= 0 ? __ldg(n0 + iu[r]) : make_int2(0, 0);
                     e1[r] = iv[r] >= 0 ? __ldg(n1 + iv[r]) : make_int2(0, 0);
                 }
 #pragma unroll
-                for (int r = 0; r < 8; ++r) {
+                for (int r = 0; r < kRowsL; ++r) {
                     const int y = y_base + r;
                     if (iu[r] >= 0 && (e0[r].x & 3)) {  // split: x-split code 1, y-split code 2
                         const bool right = ((e0[r].x & 3) == 1 ? x : y) >= (e0[r].x >> 2);
@@ -216,12 +229,12 @@ __global__ void __launch_bounds__(32 * kFrameWarps, kFrameMinBlocks) frame_kerne
                 }
             }
 #pragma unroll
-            for (int r = 0; r < 8; ++r) {  // leaf node -> its value index
+            for (int r = 0; r < kRowsL; ++r) {  // leaf node -> its value index
                 iu[r] = iu[r] >= 0 ? __ldg(n0 + iu[r]).y : -1;
                 iv[r] = iv[r] >= 0 ? __ldg(n1 + iv[r]).y : -1;
             }
 #pragma unroll
-            for (int r = 0; r < 8; ++r) {
+            for (int r = 0; r < kRowsL; ++r) {
                 if (r >= rows) break;
                 // flow.py:94-127 — coordinates clamped before flooring, taps summed w00..w11
                 const double u = iu[r] >= 0 ? __ldg(vals0 + iu[r]) : u_tile;
@@ -243,7 +256,7 @@ __global__ void __launch_bounds__(32 * kFrameWarps, kFrameMinBlocks) frame_kerne
         }
     } else {
 #pragma unroll
-        for (int r = 0; r < 8; ++r)
+        for (int r = 0; r < kRowsL; ++r)
 #pragma unroll
             for (int c = 0; c < C; ++c)
                 pred[r][c] = (col_ok && r < rows) ? __ldg(A.u[c] + (size_t)(y_base + r) * w + x) : 0.0;
@@ -251,11 +264,11 @@ __global__ void __launch_bounds__(32 * kFrameWarps, kFrameMinBlocks) frame_kerne
     // pred_int = rint(pred) (codec.py:545) kept as packed int16 pairs while the
     // residual blocks are rebuilt (frees the 8*C doubles).  |pred_int| is held
     // below 2^14: beyond it the final clip to [-255, 255] decides the same way.
-    uint32_t pk[C][4];
+    uint32_t pk[C][kRowsL / 2];
 #pragma unroll
     for (int c = 0; c < C; ++c)
 #pragma unroll
-        for (int r2 = 0; r2 < 4; ++r2) {
+        for (int r2 = 0; r2 < kRowsL / 2; ++r2) {
             const double p0 = clampd(rint_clip(pred[2 * r2][c]), -16384.0, 16383.0);
             const double p1 = clampd(rint_clip(pred[2 * r2 + 1][c]), -16384.0, 16383.0);
             pk[c][r2] = ((uint32_t)d_to_int_exact(p0) & 0xFFFFu) | ((uint32_t)d_to_int_exact(p1) << 16);
@@ -264,13 +277,13 @@ __global__ void __launch_bounds__(32 * kFrameWarps, kFrameMinBlocks) frame_kerne
     bool coded[2] = {false, false};
     if (A.res.ngroups > 0 && tile_ok) {
         const int t = ty * nbx + tx;
-        const unsigned mask8 = 0xFFu << (8 * grp);
+        const unsigned mask8 = 0xFFu << (kLanesTile * grp);
         int chan = 0;
         for (int gi = 0; gi < A.res.ngroups; ++gi) {
             const ResGroupDev& G = A.res.g[gi];
             const uint64_t word = __ldg(G.tile_words + (t >> 6));
             coded[gi] = (word >> (t & 63)) & 1ull;
-            if (coded[gi]) {
+            if (coded[gi] && sub < 8) {
                 const int b = __ldg(G.word_prefix + (t >> 6)) + __popcll(word & ((1ull << (t & 63)) - 1ull));
                 for (int ci = 0; ci < G.nplanes; ++ci)
                     residual_block(A.res, G, b, ci, &s_res[wid][chan + ci][grp][0], gl, mask8);
@@ -281,14 +294,14 @@ __global__ void __launch_bounds__(32 * kFrameWarps, kFrameMinBlocks) frame_kerne
     __syncwarp();
     if (!col_ok) return;
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
+    for (int r = 0; r < kRowsL; ++r) {
         if (r >= rows) break;
         const size_t k = (size_t)(y_base + r) * w + x;
         int rec[C];
 #pragma unroll
         for (int c = 0; c < C; ++c) {
             const int gi = c == 0 ? 0 : 1;
-            const double res = coded[gi] ? s_res[wid][c][grp][r * 8 + gl] : 0.0;
+            const double res = coded[gi] ? s_res[wid][c][grp][(r0 + r) * 8 + gl] : 0.0;
             const int pi = (int)(int16_t)(pk[c][r >> 1] >> (16 * (r & 1)));
             double v = rint_clip(s32_to_d(pi) + res);
             const double lo = (C == 3 && c > 0) ? -255.0 : 0.0;
