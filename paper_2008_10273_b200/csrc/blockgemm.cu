@@ -15,6 +15,8 @@
 //     K-major no-swizzle UMMA layout (8-row x 16-byte core matrices).
 // (b) per-block masks: every block solves its own bordered system in shared
 //     memory (float64) and rebuilds G[:, pos] c + a.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -220,6 +222,188 @@ __global__ void __launch_bounds__(kThreadsG, 2)
         }
         asm volatile("tcgen05.fence::before_thread_sync;");
         __syncthreads();  // TMEM and smem reused by the next tile
+        asm volatile("tcgen05.fence::after_thread_sync;");
+    }
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kN));
+}
+
+// The same contraction fed by TMA, persistent, with the next tile's load in
+// flight while the current one is split, multiplied and stored.  The plane is
+// viewed as a rank-3 tensor (8 floats of a block row, blocks along the image
+// row at 32 B, image rows at w*4 B); ONE cp.async.bulk.tensor per tile brings
+// 128 consecutive blocks of a block row x 8 image rows (32 KB) into shared
+// memory with the 32-byte swizzle, which is the canonical K-major SW32 UMMA
+// layout for A (row = block, 32 B = the block's 8 pixels of one image row =
+// the 8 tf32 K-elements of one MMA): image row r feeds MMA k-step r with its
+// descriptor at tile + r * 4096 (SBO 256 B between 8-block groups).  Blocks
+// past the row end are zero-filled by TMA and not stored.  3xTF32 as above:
+// the split into A_hi / A_lo is an elementwise pass over the (swizzled) tile,
+// so both halves keep the layout.  Tiles: (block row, 128-block span).
+namespace {
+constexpr int kTmaTile = 128 * 64 * 4;  // bytes of one A tile (fp32)
+
+__device__ __forceinline__ uint64_t smem_desc_sw32(uint32_t addr, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((addr >> 4) & 0x3FFF);
+    d |= (uint64_t)1 << 16;  // LBO (unused for a swizzled K-major operand one atom wide)
+    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;  // descriptor version (Blackwell)
+    d |= (uint64_t)6 << 61;  // layout type SWIZZLE_32B
+    return d;
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}\n"
+            : "=r"(done)
+            : "r"(bar), "r"(parity)
+            : "memory");
+    }
+}
+
+__device__ __forceinline__ void tma_load_tile(const CUtensorMap* tmap, uint32_t dst, uint32_t bar, int bj0, int y0) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(kTmaTile) : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+            "r"(dst),
+        "l"(tmap), "r"(0), "r"(bj0), "r"(y0), "r"(bar)
+        : "memory");
+}
+}  // namespace
+
+__global__ void __launch_bounds__(kThreadsG, 1)
+    block_operator_tma_kernel(const __grid_constant__ CUtensorMap tmap, float* __restrict__ out, int h, int w,
+                              const float* __restrict__ r_hi, const float* __restrict__ r_lo) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* raw[2] = {smem, smem + kTmaTile};     // TMA destinations (fp32 tiles)
+    uint8_t* a_hi = smem + 2 * kTmaTile;           // split halves, same swizzled layout
+    uint8_t* a_lo = smem + 3 * kTmaTile;
+    uint8_t* b_hi = smem + 4 * kTmaTile;           // 64 x 64 operator, K-major, no swizzle
+    uint8_t* b_lo = b_hi + 16384;
+    __shared__ __align__(8) uint64_t full[2];
+    __shared__ __align__(8) uint64_t mma_bar;
+    __shared__ uint32_t tmem_base;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int nbx = w >> 3, nby = h >> 3;
+    const int spans = (nbx + kTileM - 1) / kTileM;
+    const int ntiles = nby * spans;
+    auto tile_coords = [&](int t, int& bj0, int& by) {
+        by = t / spans;
+        bj0 = (t - by * spans) * kTileM;
+    };
+    if (tid == 0) {
+        for (int s = 0; s < 2; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[s])));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mma_bar)));
+        asm volatile("fence.mbarrier_init.release.cluster;");
+        asm volatile("fence.proxy.async.shared::cta;");
+        // the first two tiles' loads go out before anything else
+        for (int s = 0; s < 2; ++s) {
+            const int t = blockIdx.x + s * gridDim.x;
+            if (t < ntiles) {
+                int bj0, by;
+                tile_coords(t, bj0, by);
+                tma_load_tile(&tmap, smem_u32(raw[s]), smem_u32(&full[s]), bj0, by * 8);
+            }
+        }
+    }
+    {  // operator halves, K-major no swizzle (as block_operator_tc_kernel)
+        float4 vh[8], vl[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            vh[i] = __ldg(reinterpret_cast<const float4*>(r_hi) + tid + kThreadsG * i);
+            vl[i] = __ldg(reinterpret_cast<const float4*>(r_lo) + tid + kThreadsG * i);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int e = 4 * (tid + kThreadsG * i), n = e / kK, k = e % kK;
+            *reinterpret_cast<float4*>(b_hi + kmajor_off(n, k)) = vh[i];
+            *reinterpret_cast<float4*>(b_lo + kmajor_off(n, k)) = vl[i];
+        }
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
+                     "r"(kN));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = tmem_base;
+    int it = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+        const int st = it & 1;
+        int bj0, by;
+        tile_coords(t, bj0, by);
+        mbar_wait(smem_u32(&full[st]), (uint32_t)((it >> 1) & 1));
+        // ---- split the landed tile into tf32 hi / lo halves (elementwise: the layout is kept)
+        {
+            const float4* src = reinterpret_cast<const float4*>(raw[st]);
+            float4* dh = reinterpret_cast<float4*>(a_hi);
+            float4* dl = reinterpret_cast<float4*>(a_lo);
+#pragma unroll 4
+            for (int i = tid; i < kTmaTile / 16; i += kThreadsG) {
+                const float4 v = src[i];
+                const float4 hv = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
+                dh[i] = hv;
+                dl[i] = make_float4(v.x - hv.x, v.y - hv.y, v.z - hv.z, v.w - hv.w);
+            }
+        }
+        asm volatile("fence.proxy.async.shared::cta;");
+        __syncthreads();
+        if (tid == 0) {
+            // raw[st] is consumed: the tile two ahead goes out now
+            const int tn = t + 2 * gridDim.x;
+            if (tn < ntiles) {
+                int nb0, nby2;
+                tile_coords(tn, nb0, nby2);
+                tma_load_tile(&tmap, smem_u32(raw[st]), smem_u32(&full[st]), nb0, nby2 * 8);
+            }
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const uint32_t ah = smem_u32(a_hi), al = smem_u32(a_lo), bh = smem_u32(b_hi), bl = smem_u32(b_lo);
+#pragma unroll
+            for (int kb = 0; kb < kK / 8; ++kb) {  // image row kb of the blocks = k 8kb .. 8kb+7
+                const uint64_t dah = smem_desc_sw32(ah + kb * 4096, 256), dal = smem_desc_sw32(al + kb * 4096, 256);
+                const uint32_t boff = kb * 2 * 128;
+                mma_tf32(tmem, dah, smem_desc(bh + boff, 128, 2048), kb > 0);
+                mma_tf32(tmem, dah, smem_desc(bl + boff, 128, 2048), 1);
+                mma_tf32(tmem, dal, smem_desc(bh + boff, 128, 2048), 1);
+            }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                smem_u32(&mma_bar)));
+        }
+        mbar_wait(smem_u32(&mma_bar), (uint32_t)(it & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        // ---- epilogue: warp w reads TMEM lanes 32w..32w+31 (= blocks), 64 columns (= pixels)
+        const int m = warp * 32 + lane;
+        const int bx = bj0 + m;
+#pragma unroll
+        for (int c0 = 0; c0 < kN; c0 += 16) {
+            uint32_t v[16];
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
+                "[%16];"
+                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                  "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+                : "r"(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0));
+            asm volatile("tcgen05.wait::ld.sync.aligned;");
+            if (bx < nbx) {
+#pragma unroll
+                for (int j = 0; j < 16; j += 4) {
+                    const int n = c0 + j;
+                    float4* dst = reinterpret_cast<float4*>(out + (size_t)(by * 8 + (n >> 3)) * w + bx * 8 + (n & 7));
+                    *dst = make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]), __uint_as_float(v[j + 2]),
+                                       __uint_as_float(v[j + 3]));
+                }
+            }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncthreads();  // TMEM and the split halves are reused by the next tile
         asm volatile("tcgen05.fence::after_thread_sync;");
     }
     __syncthreads();
@@ -505,6 +689,34 @@ void launch_block_operator_tc(const float* plane, float* out, int h, int w, cons
     const int ntiles = (nblocks + kTileM - 1) / kTileM;
     const size_t smem = 65536 + 32768;
     ensure_func_attr((const void*)block_operator_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // the TMA-fed persistent kernel: whole 8x8 blocks, 16-byte aligned rows
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            fn = nullptr;
+        cudaGetLastError();
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }();
+    if (encode && h % 8 == 0 && w % 8 == 0 && (uintptr_t)plane % 16 == 0 && (uintptr_t)out % 16 == 0) {
+        CUtensorMap tmap;
+        const cuuint64_t dims[3] = {8, (cuuint64_t)(w / 8), (cuuint64_t)h};
+        const cuuint64_t strides[2] = {32, (cuuint64_t)w * 4};
+        const cuuint32_t box[3] = {8, (cuuint32_t)kTileM, 8};
+        const cuuint32_t estr[3] = {1, 1, 1};
+        if (encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(plane), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS) {
+            const size_t tsmem = 4 * (size_t)kTmaTile + 32768 + 1024;
+            ensure_func_attr((const void*)block_operator_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)tsmem);
+            const int tiles = (h / 8) * ((w / 8 + kTileM - 1) / kTileM);
+            block_operator_tma_kernel<<<std::min(tiles, num_sms), kThreadsG, tsmem, s>>>(tmap, out, h, w, r_hi, r_lo);
+            CUDA_CHECK(cudaGetLastError());
+            return;
+        }
+    }
     const int vec = (w % 4 == 0) && ((uintptr_t)plane % 16 == 0) && ((uintptr_t)out % 16 == 0);
     // two CTAs per SM (96 KB smem, 64 TMEM columns each): one tile per CTA at 1080p, loads of one
     // CTA overlap the MMA / epilogue of the other
