@@ -362,14 +362,25 @@ int hivc_block_operator(hivc_ctx* ctx, const float* plane, int32_t h, int32_t w,
                 hi[i] = fh;
                 lo[i] = (float)(R[i] - (double)fh);
             }
-            if (!C.op_hi) CUDA_CHECK(cudaMalloc(&C.op_hi, 2 * 64 * 64 * sizeof(float)));
+            // row-major hi, lo; then both again in the canonical K-major UMMA layout
+            // (core matrix (n/8, k/4) at 128 B, rows 16 B apart) for a single bulk copy
+            std::vector<float> kl(2 * 64 * 64);
+            for (int n = 0; n < 64; ++n)
+                for (int k = 0; k < 64; ++k) {
+                    const size_t off = ((size_t)((n >> 3) * 16 + (k >> 2)) * 128 + (n & 7) * 16 + (k & 3) * 4) / 4;
+                    kl[off] = hi[n * 64 + k];
+                    kl[4096 + off] = lo[n * 64 + k];
+                }
+            if (!C.op_hi) CUDA_CHECK(cudaMalloc(&C.op_hi, 4 * 64 * 64 * sizeof(float)));
             CUDA_CHECK(cudaMemcpy(C.op_hi, hi.data(), hi.size() * 4, cudaMemcpyHostToDevice));
             CUDA_CHECK(cudaMemcpy(C.op_hi + 64 * 64, lo.data(), lo.size() * 4, cudaMemcpyHostToDevice));
+            CUDA_CHECK(cudaMemcpy(C.op_hi + 2 * 64 * 64, kl.data(), kl.size() * 4, cudaMemcpyHostToDevice));
             C.op_mask = mask;
         }
         int dev_sms = 0;
         CUDA_CHECK(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, C.device));
-        hivc::launch_block_operator_tc(plane, out, h, w, C.op_hi, C.op_hi + 64 * 64, dev_sms, C.stream);
+        hivc::launch_block_operator_tc(plane, out, h, w, C.op_hi, C.op_hi + 64 * 64, dev_sms, C.stream,
+                                       C.op_hi + 2 * 64 * 64);
         C.launches += 1;
         CUDA_CHECK(cudaStreamSynchronize(C.stream));
     });

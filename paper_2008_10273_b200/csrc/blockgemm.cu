@@ -278,7 +278,7 @@ __device__ __forceinline__ void tma_load_tile(const CUtensorMap* tmap, uint32_t 
 
 __global__ void __launch_bounds__(kThreadsG, 1)
     block_operator_tma_kernel(const __grid_constant__ CUtensorMap tmap, float* __restrict__ out, int h, int w,
-                              const float* __restrict__ r_hi, const float* __restrict__ r_lo) {
+                              const float* __restrict__ r_kl) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* raw[2] = {smem, smem + kTmaTile};     // TMA destinations (fp32 tiles)
@@ -288,6 +288,7 @@ __global__ void __launch_bounds__(kThreadsG, 1)
     uint8_t* b_lo = b_hi + 16384;
     __shared__ __align__(8) uint64_t full[2];
     __shared__ __align__(8) uint64_t mma_bar;
+    __shared__ __align__(8) uint64_t op_bar;
     __shared__ uint32_t tmem_base;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int nbx = w >> 3, nby = h >> 3;
@@ -300,8 +301,16 @@ __global__ void __launch_bounds__(kThreadsG, 1)
     if (tid == 0) {
         for (int s = 0; s < 2; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[s])));
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mma_bar)));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&op_bar)));
         asm volatile("fence.mbarrier_init.release.cluster;");
         asm volatile("fence.proxy.async.shared::cta;");
+        // the operator halves, already in the K-major layout (host), as one bulk copy
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&op_bar)), "r"(32768)
+                     : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         smem_u32(b_hi)),
+                     "l"(r_kl), "r"(32768), "r"(smem_u32(&op_bar))
+                     : "memory");
         // the first two tiles' loads go out before anything else
         for (int s = 0; s < 2; ++s) {
             const int t = blockIdx.x + s * gridDim.x;
@@ -310,20 +319,6 @@ __global__ void __launch_bounds__(kThreadsG, 1)
                 tile_coords(t, bj0, by);
                 tma_load_tile(&tmap, smem_u32(raw[s]), smem_u32(&full[s]), bj0, by * 8);
             }
-        }
-    }
-    {  // operator halves, K-major no swizzle (as block_operator_tc_kernel)
-        float4 vh[8], vl[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            vh[i] = __ldg(reinterpret_cast<const float4*>(r_hi) + tid + kThreadsG * i);
-            vl[i] = __ldg(reinterpret_cast<const float4*>(r_lo) + tid + kThreadsG * i);
-        }
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int e = 4 * (tid + kThreadsG * i), n = e / kK, k = e % kK;
-            *reinterpret_cast<float4*>(b_hi + kmajor_off(n, k)) = vh[i];
-            *reinterpret_cast<float4*>(b_lo + kmajor_off(n, k)) = vl[i];
         }
     }
     if (warp == 0) {
@@ -356,6 +351,7 @@ __global__ void __launch_bounds__(kThreadsG, 1)
         }
         asm volatile("fence.proxy.async.shared::cta;");
         __syncthreads();
+        if (it == 0) mbar_wait(smem_u32(&op_bar), 0);
         if (tid == 0) {
             // raw[st] is consumed: the tile two ahead goes out now
             const int tn = t + 2 * gridDim.x;
@@ -684,7 +680,7 @@ void shared_block_operator(uint64_t mask, std::vector<double>& R) {
 }
 
 void launch_block_operator_tc(const float* plane, float* out, int h, int w, const float* r_hi, const float* r_lo,
-                              int num_sms, cudaStream_t s) {
+                              int num_sms, cudaStream_t s, const float* r_kl) {
     const int nblocks = ((h + 7) / 8) * ((w + 7) / 8);
     const int ntiles = (nblocks + kTileM - 1) / kTileM;
     const size_t smem = 65536 + 32768;
@@ -699,7 +695,7 @@ void launch_block_operator_tc(const float* plane, float* out, int h, int w, cons
         cudaGetLastError();
         return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
     }();
-    if (encode && h % 8 == 0 && w % 8 == 0 && (uintptr_t)plane % 16 == 0 && (uintptr_t)out % 16 == 0) {
+    if (r_kl && encode && h % 8 == 0 && w % 8 == 0 && (uintptr_t)plane % 16 == 0 && (uintptr_t)out % 16 == 0) {
         CUtensorMap tmap;
         const cuuint64_t dims[3] = {8, (cuuint64_t)(w / 8), (cuuint64_t)h};
         const cuuint64_t strides[2] = {32, (cuuint64_t)w * 4};
@@ -712,7 +708,7 @@ void launch_block_operator_tc(const float* plane, float* out, int h, int w, cons
             ensure_func_attr((const void*)block_operator_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)tsmem);
             const int tiles = (h / 8) * ((w / 8 + kTileM - 1) / kTileM);
-            block_operator_tma_kernel<<<std::min(tiles, num_sms), kThreadsG, tsmem, s>>>(tmap, out, h, w, r_hi, r_lo);
+            block_operator_tma_kernel<<<std::min(tiles, num_sms), kThreadsG, tsmem, s>>>(tmap, out, h, w, r_kl);
             CUDA_CHECK(cudaGetLastError());
             return;
         }

@@ -12,8 +12,10 @@ namespace hivc {
 void shared_block_operator(uint64_t mask, std::vector<double>& R);
 
 // (a) rec = R f for every 8x8 block of a float32 plane, 3xTF32 tcgen05 GEMM.
+// r_kl (nullable): the two halves pre-laid in the K-major UMMA layout for the
+// TMA-fed kernel (planes of whole 8x8 blocks); else the generic kernel runs.
 void launch_block_operator_tc(const float* plane, float* out, int h, int w, const float* r_hi, const float* r_lo,
-                              int num_sms, cudaStream_t s);
+                              int num_sms, cudaStream_t s, const float* r_kl = nullptr);
 
 // (b) per-block masks (device uint64 per block), float64 shared-memory solves.
 void launch_block_perblock(const float* plane, float* out, int h, int w, const uint64_t* masks, int* status,
