@@ -509,7 +509,7 @@ __global__ void __launch_bounds__(kPbWarps * 32)
 // instead, up to kSchurMaxK (a block beyond that flags status 4: the host
 // reruns the warp-per-block kernel with wide systems).
 constexpr int kSchurThreads = 128;
-constexpr int kSchurSmemK = 12;
+constexpr int kSchurSmemK = 8;
 constexpr int kSchurMaxK = 24;
 constexpr int kSchurTri = kSchurSmemK * (kSchurSmemK + 1) / 2;
 

@@ -129,13 +129,17 @@ def reconstruct_plane_shared_mask(plane, mask=FLAT_BLOCK_MASK):
 
 
 def reconstruct_plane_masks(plane, masks):
-    """Per-tile mask layouts (raster tile order, (ntiles, 8, 8) bool or uint64 words):
-    each tile solves its own bordered system (float64, shared memory) and is rebuilt."""
+    """Per-tile mask layouts (raster tile order, (ntiles, 8, 8) bool or uint64 words,
+    or a CUDA int64 tensor of the words already on the device): each tile solves
+    its own bordered system (float64) and is rebuilt."""
     t = torch()
     pt = to_device(plane, t.float32)
     h, w = pt.shape
-    words = masks if (isinstance(masks, np.ndarray) and masks.dtype == np.uint64) else _mask_words(masks)
-    mw = to_device(np.asarray(words, dtype=np.uint64).view(np.int64), t.int64, pt.device)
+    if is_cuda_tensor(masks) and masks.dtype == t.int64:
+        mw = masks.contiguous()
+    else:
+        words = masks if (isinstance(masks, np.ndarray) and masks.dtype == np.uint64) else _mask_words(masks)
+        mw = to_device(np.asarray(words, dtype=np.uint64).view(np.int64), t.int64, pt.device)
     if mw.numel() != ((h + 7) // 8) * ((w + 7) // 8):
         raise PseudodiffError("one mask per 8x8 tile expected")
     out = t.empty_like(pt)

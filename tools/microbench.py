@@ -104,7 +104,7 @@ def config2(reps, cpu):
     from paper_2008_10273_b200.pseudodiff import _mask_words
 
     words = torch.from_numpy(_mask_words(masks).view(np.int64)).cuda()
-    dt = timed(lambda: reconstruct_plane_masks(rt, words.cpu().numpy().view(np.uint64)), reps)
+    dt = timed(lambda: reconstruct_plane_masks(rt, words), reps)  # masks resident on the device
     ks = masks.reshape(nblk, 64).sum(1)
     print(json.dumps({"config": "2b", "what": "per-block Bernoulli(0.05) masks, float64 smem bordered solves",
                       "blocks": nblk, "seconds": dt, "blocks_per_s": nblk / dt,
