@@ -193,32 +193,6 @@ __device__ __forceinline__ void sum_partials(const double* part, int n, double* 
     if (lane == 0) bc[wid] = s;
 }
 
-// Single-value grid sums (the two per CG iteration): after the wait every
-// warp loads the CTA partials and sums them itself, in the same fixed order
-// (lane l adds partials l, l + 32, ..., then the shuffle tree), so no
-// shared-memory broadcast and no third CTA barrier are needed.
-#ifndef HIVC_RED_ALLWARPS
-#define HIVC_RED_ALLWARPS 1
-#endif
-__device__ __forceinline__ double sum_partials_warp(const double* part, int n) {
-    const int lane = threadIdx.x & 31;
-    double s = 0.0;
-    if (n <= 32 * kSumPer) {
-        double vals[kSumPer];
-#pragma unroll
-        for (int j = 0; j < kSumPer; ++j) {
-            const int g = lane + 32 * j;
-            vals[j] = g < n ? __ldcg(part + g * 4) : 0.0;
-        }
-#pragma unroll
-        for (int j = 0; j < kSumPer; ++j)
-            if (lane + 32 * j < n) s += vals[j];
-    } else {
-        for (int g = lane; g < n; g += 32) s += __ldcg(part + g * 4);
-    }
-    return warp_sum(s);
-}
-
 // This CTA's partial of each value into part[0..NV): warp sums, one CTA
 // barrier, then lane k of warp 0 adds the warp partials of value k in warp
 // order (block_sum1's order, without every thread re-reading them).
@@ -256,10 +230,6 @@ __device__ __forceinline__ void grid_reduce(double (&v)[NV], double* sh, const C
     double* part = P.partials + ((st.epoch + 1) & 1) * kPartialBank;
     cta_partial<NV>(v, sh, st.par, part + idx * 4);
     grid_arrive_wait(P.bar, n, st.epoch);
-    if (HIVC_RED_ALLWARPS && NV == 1) {
-        v[0] = sum_partials_warp(part, n);
-        return;
-    }
     double* bc = sh + 2 * 4 * 32 + st.bpar * 4;
     st.bpar ^= 1;
     sum_partials<NV>(part, n, bc);
@@ -280,10 +250,6 @@ __device__ __forceinline__ void grid_reduce_finish(double (&v)[NV], double* sh, 
                                                    int n) {
     grid_wait(P.bar, n, st.epoch);
     const double* part = P.partials + (st.epoch & 1) * kPartialBank;
-    if (HIVC_RED_ALLWARPS && NV == 1) {
-        v[0] = sum_partials_warp(part, n);
-        return;
-    }
     double* bc = sh + 2 * 4 * 32 + st.bpar * 4;
     st.bpar ^= 1;
     sum_partials<NV>(part, n, bc);
