@@ -261,18 +261,13 @@ __global__ void __launch_bounds__(32 * kFrameWarps, kFrameMinBlocks) frame_kerne
             for (int c = 0; c < C; ++c)
                 pred[r][c] = (col_ok && r < rows) ? __ldg(A.u[c] + (size_t)(y_base + r) * w + x) : 0.0;
     }
-    // pred_int = rint(pred) (codec.py:545) kept as packed int16 pairs while the
-    // residual blocks are rebuilt (frees the 8*C doubles).  |pred_int| is held
-    // below 2^14: beyond it the final clip to [-255, 255] decides the same way.
-    uint32_t pk[C][kRowsL / 2];
+    // pred_int = rint(pred) (codec.py:545), in place: |pred| <= 255 for a P frame
+    // (a convex combination of frame values) and bounded by the inpainted plane
+    // for an I frame, so the 1.5 * 2^52 rounding is exact
 #pragma unroll
-    for (int c = 0; c < C; ++c)
+    for (int r = 0; r < kRowsL; ++r)
 #pragma unroll
-        for (int r2 = 0; r2 < kRowsL / 2; ++r2) {
-            const double p0 = clampd(rint_clip(pred[2 * r2][c]), -16384.0, 16383.0);
-            const double p1 = clampd(rint_clip(pred[2 * r2 + 1][c]), -16384.0, 16383.0);
-            pk[c][r2] = ((uint32_t)d_to_int_exact(p0) & 0xFFFFu) | ((uint32_t)d_to_int_exact(p1) << 16);
-        }
+        for (int c = 0; c < C; ++c) pred[r][c] = rint_clip(pred[r][c]);
     // ---- residual block(s): lanes 8g..8g+7 rebuild tile g's coded blocks
     bool coded[2] = {false, false};
     if (A.res.ngroups > 0 && tile_ok) {
@@ -302,8 +297,7 @@ __global__ void __launch_bounds__(32 * kFrameWarps, kFrameMinBlocks) frame_kerne
         for (int c = 0; c < C; ++c) {
             const int gi = c == 0 ? 0 : 1;
             const double res = coded[gi] ? s_res[wid][c][grp][(r0 + r) * 8 + gl] : 0.0;
-            const int pi = (int)(int16_t)(pk[c][r >> 1] >> (16 * (r & 1)));
-            double v = rint_clip(s32_to_d(pi) + res);
+            double v = rint_clip(pred[r][c] + res);
             const double lo = (C == 3 && c > 0) ? -255.0 : 0.0;
             v = clampd(v, lo, 255.0);
             rec[c] = d_to_int_exact(v);
