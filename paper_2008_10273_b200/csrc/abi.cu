@@ -391,12 +391,19 @@ int hivc_block_perblock(hivc_ctx* ctx, const float* plane, int32_t h, int32_t w,
         if (!ctx) hivc::fail(HIVC_E_ARGUMENT, "null context");
         hivc::Context& C = ctx->c;
         CUDA_CHECK(cudaSetDevice(C.device));
-        CUDA_CHECK(cudaMemsetAsync(C.d_status, 0, sizeof(int), C.stream));
+        CUDA_CHECK(cudaMemsetAsync(C.d_status, 0, 2 * sizeof(int), C.stream));
         hivc::launch_block_perblock(plane, out, h, w, masks, C.d_status, C.stream);
         C.launches += 1;
-        int st = 0;
-        CUDA_CHECK(cudaMemcpyAsync(&st, C.d_status, sizeof(int), cudaMemcpyDeviceToHost, C.stream));
+        int st2[2] = {0, 0};
+        CUDA_CHECK(cudaMemcpyAsync(st2, C.d_status, 2 * sizeof(int), cudaMemcpyDeviceToHost, C.stream));
         CUDA_CHECK(cudaStreamSynchronize(C.stream));
+        int st = st2[0];
+        if (st == 0 && st2[1]) {  // blocks with more than 8 points: the one-thread kernel for those
+            hivc::launch_block_perblock(plane, out, h, w, masks, C.d_status, C.stream, false, true);
+            C.launches += 1;
+            CUDA_CHECK(cudaMemcpyAsync(&st, C.d_status, sizeof(int), cudaMemcpyDeviceToHost, C.stream));
+            CUDA_CHECK(cudaStreamSynchronize(C.stream));
+        }
         if (st == 4) {  // a block has more than 16 points: the wide-system variant for all blocks
             CUDA_CHECK(cudaMemsetAsync(C.d_status, 0, sizeof(int), C.stream));
             hivc::launch_block_perblock(plane, out, h, w, masks, C.d_status, C.stream, true);

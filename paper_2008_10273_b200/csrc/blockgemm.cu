@@ -21,6 +21,8 @@
 
 #include <cstdint>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include "aan_constants.h"
@@ -417,7 +419,7 @@ constexpr int kPbWarps = 4;
 template <int LD>
 __global__ void __launch_bounds__(kPbWarps * 32)
     block_perblock_kernel(const float* __restrict__ plane, float* __restrict__ out, int h, int w,
-                          const uint64_t* __restrict__ masks, int nblocks, int* status) {
+                          const uint64_t* __restrict__ masks, int nblocks, int* status, int min_k) {
     extern __shared__ double sm[];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int b = blockIdx.x * kPbWarps + wid;
@@ -425,14 +427,15 @@ __global__ void __launch_bounds__(kPbWarps * 32)
     double* M = sm + (size_t)wid * (LD - 1) * LD;
     double* fb = sm + (size_t)kPbWarps * (LD - 1) * LD + wid * 64;
     int* pos = reinterpret_cast<int*>(sm + (size_t)kPbWarps * ((LD - 1) * LD + 64)) + wid * 64;
+    const uint64_t mask = masks[b];
+    const int K = __popcll(mask);
+    if (K > 0 && K <= min_k) return;  // (done by block_schur8_kernel)
     const int nbx = (w + 7) >> 3;
     const int by = b / nbx, bx = b % nbx;
     for (int k = lane; k < 64; k += 32) {
         int y = by * 8 + (k >> 3), x = bx * 8 + (k & 7);
         fb[k] = (y < h && x < w) ? (double)plane[(size_t)y * w + x] : 0.0;
     }
-    const uint64_t mask = masks[b];
-    const int K = __popcll(mask);
     if (K == 0) {
         if (lane == 0) atomicExch(status, 1);
         return;
@@ -495,145 +498,144 @@ __global__ void __launch_bounds__(kPbWarps * 32)
     }
 }
 
-// One THREAD per block: the bordered system [[G_KK, 1], [1^T, 0]] [c; a] =
-// [f_K; 0] solved through its Schur complement — G_KK (a principal submatrix
-// of the positive semi-definite Green's matrix whose null space is the
-// constant block, so positive definite for K < 64) is factored
+// Config 2b: the bordered system [[G_KK, 1], [1^T, 0]] [c; a] = [f_K; 0] of
+// every block solved through its Schur complement — G_KK (a principal
+// submatrix of the positive semi-definite Green's matrix whose null space is
+// the constant block, so positive definite for K < 64) is factored
 // G_KK = L L^T, then y = G_KK^-1 f, z = G_KK^-1 1, a = 1^T y / 1^T z and
 // c = y - a z (the unique solution of the reference's system,
 // pseudodiff.py:218-263; rounding differs from LAPACK's pivoted LU at the
-// 1e-13 level); rec = G[:, pos] c + a.  The 64x64 Green's matrix is staged
-// in shared memory per CTA; each thread's packed factor lives in shared
-// memory interleaved across the CTA's threads (conflict-free); the rare block
-// with more than kSchurSmemK points factors into a per-thread local array
-// instead, up to kSchurMaxK (a block beyond that flags status 4: the host
-// reruns the warp-per-block kernel with wide systems).
-constexpr int kSchurThreads = 128;
-constexpr int kSchurSmemK = 8;
-constexpr int kSchurMaxK = 24;
-constexpr int kSchurTri = kSchurSmemK * (kSchurSmemK + 1) / 2;
+// 1e-13 level); rec = G[:, pos] c + a.
+// Eight lanes per block (four blocks per warp) for blocks of up to kSL
+// points: lane j owns rows j and j + 8 of the Cholesky factor, which lives in
+// shared memory with the block's points and right-hand sides, and every loop
+// runs to K (no unrolling to the worst case: a typical block has 1-6
+// points).  G_KK = L L^T column by column, forward and backward substitution
+// for y = G^-1 f and z = G^-1 1, a = sum y / sum z, c = y - a z; lane j then
+// rebuilds pixel column j of the block, reading the symmetric Green's matrix
+// along rows (G[p][n] in place of G[n][p]: conflict-free).  Blocks with more
+// points are flagged (status[1]) for the warp-per-block kernel above.
+constexpr int kSL = 16;
+constexpr int kS8Warps = 8;
+constexpr int kSGroup = kSL * (kSL + 1) / 2 + 3 * kSL;  // doubles per block: packed L, y, z, positions
 
-__global__ void __launch_bounds__(kSchurThreads) block_schur_kernel(const float* __restrict__ plane,
-                                                                    float* __restrict__ out, int h, int w,
-                                                                    const uint64_t* __restrict__ masks,
-                                                                    int nblocks, int* status) {
-    extern __shared__ double sm[];
-    double* G = sm;                    // 64 x 64
-    double* Lt = sm + 4096;            // kSchurTri x kSchurThreads, thread-interleaved
-    for (int i = threadIdx.x; i < 4096; i += kSchurThreads) G[i] = kGreens64[i];
-    __syncthreads();
-    const int b = blockIdx.x * kSchurThreads + threadIdx.x;
-    if (b >= nblocks) return;
-    const uint64_t mask = masks[b];
+__global__ void __launch_bounds__(kS8Warps * 32) block_schur8_kernel(const float* __restrict__ plane,
+                                                                     float* __restrict__ out, int h, int w,
+                                                                     const uint64_t* __restrict__ masks,
+                                                                     int nblocks, int* status,
+                                                                     const double* __restrict__ G) {
+    // G: the 64 x 64 Green's matrix in global memory (L1-resident: 32 KB, read along rows)
+    extern __shared__ double s8[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, grp = lane >> 3, j = lane & 7;
+    const unsigned gm = 0xFFu << (8 * grp);
+    const int b = (blockIdx.x * kS8Warps + wid) * 4 + grp;
+    if (b >= nblocks) return;  // (whole 8-lane groups)
+    const uint64_t mask = __ldg(masks + b);
     const int K = __popcll(mask);
     if (K == 0) {
-        atomicExch(status, 1);
+        if (j == 0) atomicExch(status, 1);
         return;
     }
-    if (K > kSchurMaxK) {
-        atomicExch(status, 4);
+    if (K > kSL) {  // the one-thread kernel takes these
+        if (j == 0) atomicOr(status + 1, 1);
         return;
     }
-    double Lbig[kSchurMaxK * (kSchurMaxK + 1) / 2];  // (local memory; K > kSchurSmemK only)
-    const bool big = K > kSchurSmemK;
-    auto L = [&](int i, int j) -> double& {
-        return big ? Lbig[i * (i + 1) / 2 + j] : Lt[(i * (i + 1) / 2 + j) * kSchurThreads + threadIdx.x];
-    };
+    double* L = s8 + (size_t)(wid * 4 + grp) * kSGroup;
+    double* Y = L + kSL * (kSL + 1) / 2;
+    auto T = [](int i, int k) { return i * (i + 1) / 2 + k; };  // packed lower triangle
+    double* Z = Y + kSL;
+    int* P = reinterpret_cast<int*>(Z + kSL);
     const int nbx = (w + 7) >> 3;
     const int by = b / nbx, bx = b - by * nbx;
-    int pos[kSchurMaxK];
-    double f[kSchurMaxK];
-    {
+    for (int i = j; i < K; i += 8) {  // point i: the i-th set bit, its sample, rhs 1
         uint64_t m = mask;
-#pragma unroll
-        for (int i = 0; i < kSchurMaxK; ++i) {
-            pos[i] = 0;
-            f[i] = 0.0;
-            if (i < K) {
-                const int j = __ffsll((long long)m) - 1;
-                m &= m - 1;
-                pos[i] = j;
-                const int y = by * 8 + (j >> 3), x = bx * 8 + (j & 7);
-                f[i] = (y < h && x < w) ? (double)__ldg(plane + (size_t)y * w + x) : 0.0;
+        for (int t = 0; t < i; ++t) m &= m - 1;
+        const int p = __ffsll((long long)m) - 1;
+        P[i] = p;
+        const int yy = by * 8 + (p >> 3), xx = bx * 8 + (p & 7);
+        Y[i] = (yy < h && xx < w) ? (double)__ldg(plane + (size_t)yy * w + xx) : 0.0;
+        Z[i] = 1.0;
+    }
+    __syncwarp(gm);
+    // G_KK = L L^T, column by column
+    bool bad = false;
+    for (int c = 0; c < K; ++c) {
+        const int pc = P[c];
+        if (j == (c & 7)) {
+            double d = G[pc * 64 + pc];
+            for (int k = 0; k < c; ++k) d = d - L[T(c, k)] * L[T(c, k)];
+            bad |= !(d > 0.0);
+            L[T(c, c)] = sqrt(fmax(d, 1e-300));
+        }
+        __syncwarp(gm);
+        const double lcc = L[T(c, c)];
+        for (int i = j; i < K; i += 8)
+            if (i > c) {
+                double v = G[pc * 64 + P[i]];  // = G[p_i][p_c] (symmetric)
+                for (int k = 0; k < c; ++k) v = v - L[T(i, k)] * L[T(c, k)];
+                L[T(i, c)] = v / lcc;
             }
-        }
+        __syncwarp(gm);
     }
-    // G_KK = L L^T (column by column)
-    for (int j = 0; j < K; ++j) {
-        double d = G[pos[j] * 64 + pos[j]];
-        for (int k = 0; k < j; ++k) d = d - L(j, k) * L(j, k);
-        if (!(d > 0.0)) {
-            atomicExch(status, 2);
-            return;
-        }
-        const double ljj = sqrt(d);
-        L(j, j) = ljj;
-        for (int i = j + 1; i < K; ++i) {
-            double v = G[pos[i] * 64 + pos[j]];
-            for (int k = 0; k < j; ++k) v = v - L(i, k) * L(j, k);
-            L(i, j) = v / ljj;
-        }
+    if (__any_sync(gm, bad)) {
+        if (j == 0) atomicExch(status, 2);
+        return;
     }
-    // y = G^-1 f, z = G^-1 1: forward then backward substitution, both at once
-    double y[kSchurMaxK], z[kSchurMaxK];
-#pragma unroll
-    for (int i = 0; i < kSchurMaxK; ++i) {
-        if (i >= K) break;
-        double sy = f[i], sz = 1.0;
-        for (int k = 0; k < i; ++k) {
-            const double l = L(i, k);
-            sy = sy - l * y[k];
-            sz = sz - l * z[k];
+    // forward: L u = f (and 1), then backward: L^T x = u
+    for (int c = 0; c < K; ++c) {
+        const double lcc = L[T(c, c)];
+        if (j == (c & 7)) {
+            Y[c] = Y[c] / lcc;
+            Z[c] = Z[c] / lcc;
         }
-        const double d = L(i, i);
-        y[i] = sy / d;
-        z[i] = sz / d;
+        __syncwarp(gm);
+        const double yc = Y[c], zc = Z[c];
+        for (int i = j; i < K; i += 8)
+            if (i > c) {
+                const double l = L[T(i, c)];
+                Y[i] = Y[i] - l * yc;
+                Z[i] = Z[i] - l * zc;
+            }
+        __syncwarp(gm);
     }
-#pragma unroll
-    for (int i = kSchurMaxK - 1; i >= 0; --i) {
-        if (i >= K) continue;
-        double sy = y[i], sz = z[i];
-        for (int k = i + 1; k < K; ++k) {
-            const double l = L(k, i);
-            sy = sy - l * y[k];
-            sz = sz - l * z[k];
+    for (int c = K - 1; c >= 0; --c) {
+        const double lcc = L[T(c, c)];
+        if (j == (c & 7)) {
+            Y[c] = Y[c] / lcc;
+            Z[c] = Z[c] / lcc;
         }
-        const double d = L(i, i);
-        y[i] = sy / d;
-        z[i] = sz / d;
+        __syncwarp(gm);
+        const double yc = Y[c], zc = Z[c];
+        for (int i = j; i < c; i += 8) {
+            const double l = L[T(c, i)];
+            Y[i] = Y[i] - l * yc;
+            Z[i] = Z[i] - l * zc;
+        }
+        __syncwarp(gm);
     }
     double sy = 0.0, sz = 0.0;
-#pragma unroll
-    for (int i = 0; i < kSchurMaxK; ++i)
-        if (i < K) {
-            sy += y[i];
-            sz += z[i];
-        }
-    const double a = sy / sz;
-#pragma unroll
-    for (int i = 0; i < kSchurMaxK; ++i) y[i] = i < K ? y[i] - a * z[i] : 0.0;  // c
-    // rec = G[:, pos] c + a, one 8-pixel row at a time
-    for (int r = 0; r < 8; ++r) {
-        const int yy = by * 8 + r;
-        if (yy >= h) break;
-        float o[8];
-#pragma unroll
-        for (int xx = 0; xx < 8; ++xx) {
-            const double* g = G + (r * 8 + xx) * 64;
-            double acc = 0.0;
-#pragma unroll
-            for (int i = 0; i < kSchurMaxK; ++i)
-                if (i < K) acc = acc + g[pos[i]] * y[i];
-            o[xx] = (float)(acc + a);
-        }
-        float* dst = out + (size_t)yy * w + bx * 8;
-        if (bx * 8 + 8 <= w && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
-            reinterpret_cast<float4*>(dst)[0] = make_float4(o[0], o[1], o[2], o[3]);
-            reinterpret_cast<float4*>(dst)[1] = make_float4(o[4], o[5], o[6], o[7]);
-        } else {
-            for (int xx = 0; xx < 8 && bx * 8 + xx < w; ++xx) dst[xx] = o[xx];
-        }
+    for (int i = 0; i < K; ++i) {
+        sy += Y[i];
+        sz += Z[i];
     }
+    const double a = sy / sz;
+    // lane j rebuilds pixel column j: rec[r][j] = sum_i G[p_i][r*8 + j] (y_i - a z_i) + a
+    double acc[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) acc[r] = 0.0;
+    for (int i = 0; i < K; ++i) {
+        const double ci = Y[i] - a * Z[i];
+        const double* g = G + P[i] * 64 + j;
+#pragma unroll
+        for (int r = 0; r < 8; ++r) acc[r] = acc[r] + g[r * 8] * ci;
+    }
+    const int xx = bx * 8 + j;
+    if (xx < w)
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int yy = by * 8 + r;
+            if (yy < h) out[(size_t)yy * w + xx] = (float)(acc[r] + a);
+        }
 }
 
 // ---------------------------------------------------------------- host
@@ -721,23 +723,42 @@ void launch_block_operator_tc(const float* plane, float* out, int h, int w, cons
     CUDA_CHECK(cudaGetLastError());
 }
 
+// The Green's matrix in global memory, once per device.
+static const double* greens_device() {
+    static std::mutex mu;
+    static std::map<int, double*> per_dev;
+    int dev = 0;
+    CUDA_CHECK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    double*& p = per_dev[dev];
+    if (!p) {
+        CUDA_CHECK(cudaMalloc(&p, 4096 * sizeof(double)));
+        CUDA_CHECK(cudaMemcpy(p, kGreens64Host, 4096 * sizeof(double), cudaMemcpyHostToDevice));
+    }
+    return p;
+}
+
 void launch_block_perblock(const float* plane, float* out, int h, int w, const uint64_t* masks, int* status,
-                           cudaStream_t s, bool wide) {
+                           cudaStream_t s, bool wide, bool second_pass) {
     const int nblocks = ((h + 7) / 8) * ((w + 7) / 8);
-    auto go = [&](auto kernel, int ld) {
+    auto go = [&](auto kernel, int ld, int min_k) {
         const size_t smem =
             (size_t)kPbWarps * ((ld - 1) * ld + 64) * sizeof(double) + kPbWarps * 64 * sizeof(int);
         ensure_func_attr((const void*)kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kernel<<<(nblocks + kPbWarps - 1) / kPbWarps, kPbWarps * 32, smem, s>>>(plane, out, h, w, masks, nblocks,
-                                                                                  status);
+                                                                                  status, min_k);
     };
     if (wide) {
-        go(block_perblock_kernel<66>, 66);
+        go(block_perblock_kernel<66>, 66, 0);
+    } else if (second_pass) {  // the blocks block_schur8_kernel flagged (K > kSL): a warp each, K <= 16
+        go(block_perblock_kernel<18>, 18, kSL);
     } else {
-        const size_t smem = (size_t)(4096 + kSchurTri * kSchurThreads) * sizeof(double);
-        ensure_func_attr((const void*)block_schur_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        block_schur_kernel<<<(nblocks + kSchurThreads - 1) / kSchurThreads, kSchurThreads, smem, s>>>(
-            plane, out, h, w, masks, nblocks, status);
+        const size_t smem = (size_t)(kS8Warps * 4 * kSGroup) * sizeof(double);
+        ensure_func_attr((const void*)block_schur8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        const int per_cta = kS8Warps * 4;
+        block_schur8_kernel<<<(nblocks + per_cta - 1) / per_cta, kS8Warps * 32, smem, s>>>(plane, out, h, w, masks,
+                                                                                          nblocks, status,
+                                                                                          greens_device());
     }
     CUDA_CHECK(cudaGetLastError());
 }

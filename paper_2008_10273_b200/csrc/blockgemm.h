@@ -18,7 +18,9 @@ void launch_block_operator_tc(const float* plane, float* out, int h, int w, cons
                               int num_sms, cudaStream_t s, const float* r_kl = nullptr);
 
 // (b) per-block masks (device uint64 per block), float64 shared-memory solves.
+// status[0]: 1 empty mask, 2 singular, 4 a block needs the wide kernel;
+// status[1] != 0: blocks with more than 8 points await the second pass.
 void launch_block_perblock(const float* plane, float* out, int h, int w, const uint64_t* masks, int* status,
-                           cudaStream_t s, bool wide = false);
+                           cudaStream_t s, bool wide = false, bool second_pass = false);
 
 }  // namespace hivc
