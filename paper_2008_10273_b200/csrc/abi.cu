@@ -202,7 +202,7 @@ int hivc_homog_solve(hivc_ctx* ctx, const double* f, const uint8_t* mask, int32_
                 if (nk) fprintf(stderr, "[cg trace] arrival spread %.0f ns | last arrival -> CTA0 released+summed %.0f ns\n",
                                 spread / nk, rel / nk);
             }
-            double acc[6] = {0, 0, 0, 0, 0, 0}, acc6 = 0;
+            double acc[6] = {0, 0, 0, 0, 0, 0}, acc6 = 0, acc7 = 0;
             int n = 0;
             for (int k = 2; k < 255 && tr[(k + 1) * 8] != 0; ++k, ++n) {
                 const unsigned long long* t = &tr[k * 8];
@@ -213,12 +213,13 @@ int hivc_homog_solve(hivc_ctx* ctx, const double* f, const uint8_t* mask, int32_
                 acc[4] += (double)(t[5] - t[4]);
                 acc[5] += (double)(tr[(k + 1) * 8] - t[5]);
                 if (t[6]) acc6 += (double)(t[6] - t[4]);
+                if (t[7]) acc7 += (double)(t[7] - t[0]);
             }
             if (n)
                 fprintf(stderr,
                         "[cg trace] %d iters: halo+p %.0f ns | stencil %.0f | reduce1 %.0f | phase2 %.0f | reduce2 %.0f "
-                        "(arrive + x update %.0f) | tail %.0f\n",
-                        n, acc[0] / n, acc[1] / n, acc[2] / n, acc[3] / n, acc[4] / n, acc6 / n, acc[5] / n);
+                        "(arrive + x update %.0f) | tail %.0f | halo loads+stores %.0f\n",
+                        n, acc[0] / n, acc[1] / n, acc[2] / n, acc[3] / n, acc[4] / n, acc6 / n, acc[5] / n, acc7 / n);
         }
         if (nlevels) *nlevels = L;
         for (int i = 0; i < L && i < 32; ++i) {

@@ -2,9 +2,9 @@
 // cluster level sets whose bands are at most kColRows rows of at most
 // kClThreads columns (every level of a 1080p / 540p pyramid up to 270x480).
 //
-// Same data placement and exchange as cg_cluster_kernel (one 16-CTA cluster
-// per solve; DSMEM reductions and halo rows; x and the padded p in shared
-// memory), but thread c owns column c of its band for every row: r and A p
+// Same data placement as cg_cluster_kernel (one 16-CTA cluster per solve;
+// DSMEM reductions and halo rows; x and the padded p in shared memory; only
+// the r edge rows are exchanged, see phase 1), but thread c owns column c of its band for every row: r and A p
 // stay in registers (phase 2 reuses the stencil of phase 1), the mask is one
 // bit word per thread, and the 5-point stencil walks the column reading 3
 // shared values per pixel.  Per-pixel float64 expressions are those of
@@ -77,11 +77,10 @@ __global__ void __launch_bounds__(kClThreads, 1) cg_cluster_col_kernel(const __g
         const bool top = y0 == 0, bottom = y0 + rows == h;
         const int c = tid;
         const bool act = c < w && rows > 0;
-        // shared layout: padded p (band_rows+2) x (w+2) | x (band_rows*w) | ex_r 2w | ex_p 2x2w
+        // shared layout: padded p (band_rows+2) x (w+2) | x (band_rows*w) | ex_r 2w
         double* sp = smem_cl;
         double* sx = sp + (size_t)(band_rows + 2) * W2;
         double* exr = sx + (size_t)band_rows * w;
-        double* exp_ = exr + 2 * w;
 
         if (coarsest) {  // x0 = mean(f[mask]), numpy pairwise order; every CTA computes it
             const bool in = tid < h * w;
@@ -180,30 +179,23 @@ __global__ void __launch_bounds__(kClThreads, 1) cg_cluster_col_kernel(const __g
                     if (row >= rows) break;
                     put(row, r[row]);
                 }
-                exr[c] = exp_[c] = r[0];
+                exr[c] = r[0];
 #pragma unroll
                 for (int row = 0; row < kColRows; ++row)
-                    if (row == rows - 1) exr[w + c] = exp_[w + c] = r[row];
+                    if (row == rows - 1) exr[w + c] = r[row];
             }
             cluster.sync();
             double beta = 0.0;
             for (int k = 1; k <= S.max_iter; ++k) {
                 it = k;
-                const int pp = (k - 1) & 1, cp = k & 1;  // ex_p parity read / written this iteration
                 const bool tr = S.trace && li == S.nlev - 1 && rank == 0 && tid == 0 && k < 256;
                 if (tr) S.trace[k * 8 + 0] = globaltimer_ns();
-                // ---- phase 1: halo p = r + beta p from the neighbours' edge rows (DSMEM), own p update
+                // ---- phase 1: own p = r + beta p, then the halo rows: a halo cell already
+                // holds the neighbour's previous p edge (computed here with the
+                // neighbour's operands), so only its r edge row is read (DSMEM)
                 if (act) {
-                    if (!top) {
-                        const double* up_r = cluster.map_shared_rank(exr, rank - 1);
-                        const double* up_p = cluster.map_shared_rank(exp_, rank - 1);
-                        sp[c + 1] = up_r[w + c] + beta * up_p[pp * 2 * w + w + c];
-                    }
-                    if (!bottom) {
-                        const double* dn_r = cluster.map_shared_rank(exr, rank + 1);
-                        const double* dn_p = cluster.map_shared_rank(exp_, rank + 1);
-                        sp[(rows + 1) * W2 + c + 1] = dn_r[c] + beta * dn_p[pp * 2 * w + c];
-                    }
+                    const double hr_up = top ? 0.0 : cluster.map_shared_rank(exr, rank - 1)[w + c];
+                    const double hr_dn = bottom ? 0.0 : cluster.map_shared_rank(exr, rank + 1)[c];
                     if (k > 1) {
 #pragma unroll
                         for (int row = 0; row < kColRows; ++row) {
@@ -211,6 +203,8 @@ __global__ void __launch_bounds__(kClThreads, 1) cg_cluster_col_kernel(const __g
                             put(row, r[row] + beta * sp[(row + 1) * W2 + c + 1]);
                         }
                     }
+                    if (!top) sp[c + 1] = hr_up + beta * (k == 1 ? 0.0 : sp[c + 1]);
+                    if (!bottom) sp[(rows + 1) * W2 + c + 1] = hr_dn + beta * (k == 1 ? 0.0 : sp[(rows + 1) * W2 + c + 1]);
                 }
                 __syncthreads();
                 if (tr) S.trace[k * 8 + 1] = globaltimer_ns();
@@ -229,8 +223,6 @@ __global__ void __launch_bounds__(kClThreads, 1) cg_cluster_col_kernel(const __g
                         up = cur;
                         cur = dn;
                     }
-                    exp_[cp * 2 * w + c] = sp[W2 + c + 1];  // publish p edge rows
-                    exp_[cp * 2 * w + w + c] = sp[rows * W2 + c + 1];
                 }
                 if (tr) S.trace[k * 8 + 2] = globaltimer_ns();
                 creduce(d, 1);

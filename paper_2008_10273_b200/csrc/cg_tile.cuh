@@ -8,11 +8,13 @@
 // full-width bands (cg_band2), a tile exchanges ~4x fewer halo values per
 // iteration (its perimeter instead of two plane-wide rows) and keeps ~all of
 // x on chip, and the tile grid can use every SM (1080x1920: 36 x 4 tiles of
-// 30 x 480).  Per iteration: halo rows/columns rebuilt from the neighbours'
-// published edges of r and p (global exchange buffers, p double-buffered by
-// parity), p = r + beta p, A p and p.Ap, grid reduction, r -= alpha A p and
-// r.r, grid reduction (x += alpha p overlapped with its wait).  Float64
-// expressions and the per-CTA summation order match cg_band2's column walk.
+// 30 x 480).  Per iteration: p = r + beta p on the own rows and on the halo
+// cells (each halo cell already holds the neighbour's previous p edge, so only
+// the neighbours' published r edges are loaded, through a global exchange
+// buffer), A p and p.Ap, grid reduction, r -= alpha A p and r.r, grid
+// reduction (x += alpha p overlapped with its wait).  Float64 expressions and
+// the per-CTA summation order are those of the column walk in every level
+// kernel (cg_cluster_col.cuh), so a level solves identically in either.
 #pragma once
 
 constexpr int kTileRows = 32;
@@ -90,8 +92,6 @@ __global__ void __launch_bounds__(kTileThreads, 1) cg_tile_kernel(const __grid_c
         }
     }
     double* ex_r = P.ex_r;
-    double* ex_p = P.ex_p;
-    const size_t pstride = (size_t)nt * E;
     const size_t mine = (size_t)tile * E;
     int it = 0;
     double margin = 1e300;
@@ -99,64 +99,56 @@ __global__ void __launch_bounds__(kTileThreads, 1) cg_tile_kernel(const __grid_c
         double beta = 0.0;
         for (int k = 1; k <= P.max_iter; ++k) {
             it = k;
-            const size_t prev_par = (size_t)((k - 1) & 1) * pstride, cur_par = (size_t)(k & 1) * pstride;
             HIVC_TRACE(0);
-            // ---- phase 1a: halo rows / columns (neighbours' edges of r and p), own p = r + beta p
+            // ---- phase 1a: own p = r + beta p, then the halo rows / columns.  A halo
+            // cell already holds the neighbour's previous p edge (it was computed here
+            // last iteration with the neighbour's own operands and expression), so only
+            // the neighbours' r edges are loaded; the loads are in flight while the
+            // own rows are updated.
             {
-                double tr = 0, tp = 0, br = 0, bp = 0, lr = 0, lp = 0, rr_ = 0, rp = 0;
+                double tr = 0, br = 0, lr = 0, rr_ = 0;
                 const bool hc = tid < rows;  // this thread also rebuilds row tid of the side halos
-                if (act && !top) {
-                    if (k == 1) {
-                        tr = tp = __ldcg(P.r + (size_t)(y0 - 1) * w + gc);
-                    } else {
-                        const size_t e = (size_t)(tile - ntc) * E + tcols + c;  // upper tile's bottom row
-                        tr = __ldcg(ex_r + e);
-                        tp = __ldcg(ex_p + prev_par + e);
+                if (act && !top)
+                    tr = k == 1 ? __ldcg(P.r + (size_t)(y0 - 1) * w + gc)
+                                : __ldcg(ex_r + (size_t)(tile - ntc) * E + tcols + c);  // upper tile's bottom row
+                if (act && !bottom)
+                    br = k == 1 ? __ldcg(P.r + (size_t)(y0 + rows) * w + gc)
+                                : __ldcg(ex_r + (size_t)(tile + ntc) * E + c);  // lower tile's top row
+                if (hc && !left)
+                    lr = k == 1 ? __ldcg(P.r + (size_t)(y0 + tid) * w + x0 - 1)
+                                : __ldcg(ex_r + (size_t)(tile - 1) * E + 2 * tcols + trows + tid);  // left tile's right column
+                if (hc && !right)
+                    rr_ = k == 1 ? __ldcg(P.r + (size_t)(y0 + tid) * w + x0 + cols)
+                                 : __ldcg(ex_r + (size_t)(tile + 1) * E + 2 * tcols + tid);  // right tile's left column
+                if (act) {
+#pragma unroll
+                    for (int row = 0; row < ROWS; ++row) {
+                        if (row >= rows) break;
+                        double* q = sp + (row + 1) * W2 + c + 1;
+                        const double pn = r[row] + beta * (k == 1 ? 0.0 : *q);
+                        *q = pn;
+                        if (left && c == 0) q[-1] = pn;  // reflecting plane edges
+                        if (right && c == cols - 1) q[1] = pn;
+                        if (top && row == 0) q[-W2] = pn;
+                        if (bottom && row == rows - 1) q[W2] = pn;
                     }
+                }
+                HIVC_TRACE(7);
+                if (act && !top) {
+                    double* q = sp + c + 1;
+                    *q = tr + beta * (k == 1 ? 0.0 : *q);
                 }
                 if (act && !bottom) {
-                    if (k == 1) {
-                        br = bp = __ldcg(P.r + (size_t)(y0 + rows) * w + gc);
-                    } else {
-                        const size_t e = (size_t)(tile + ntc) * E + c;  // lower tile's top row
-                        br = __ldcg(ex_r + e);
-                        bp = __ldcg(ex_p + prev_par + e);
-                    }
+                    double* q = sp + (rows + 1) * W2 + c + 1;
+                    *q = br + beta * (k == 1 ? 0.0 : *q);
                 }
                 if (hc && !left) {
-                    if (k == 1) {
-                        lr = lp = __ldcg(P.r + (size_t)(y0 + tid) * w + x0 - 1);
-                    } else {
-                        const size_t e = (size_t)(tile - 1) * E + 2 * tcols + trows + tid;  // left tile's right column
-                        lr = __ldcg(ex_r + e);
-                        lp = __ldcg(ex_p + prev_par + e);
-                    }
+                    double* q = sp + (tid + 1) * W2;
+                    *q = lr + beta * (k == 1 ? 0.0 : *q);
                 }
                 if (hc && !right) {
-                    if (k == 1) {
-                        rr_ = rp = __ldcg(P.r + (size_t)(y0 + tid) * w + x0 + cols);
-                    } else {
-                        const size_t e = (size_t)(tile + 1) * E + 2 * tcols + tid;  // right tile's left column
-                        rr_ = __ldcg(ex_r + e);
-                        rp = __ldcg(ex_p + prev_par + e);
-                    }
-                }
-                if (act && !top) sp[c + 1] = tr + beta * tp;
-                if (act && !bottom) sp[(rows + 1) * W2 + c + 1] = br + beta * bp;
-                if (hc && !left) sp[(tid + 1) * W2] = lr + beta * lp;
-                if (hc && !right) sp[(tid + 1) * W2 + cols + 1] = rr_ + beta * rp;
-            }
-            if (act) {
-#pragma unroll
-                for (int row = 0; row < ROWS; ++row) {
-                    if (row >= rows) break;
-                    double* q = sp + (row + 1) * W2 + c + 1;
-                    const double pn = r[row] + beta * (k == 1 ? 0.0 : *q);
-                    *q = pn;
-                    if (left && c == 0) q[-1] = pn;  // reflecting plane edges
-                    if (right && c == cols - 1) q[1] = pn;
-                    if (top && row == 0) q[-W2] = pn;
-                    if (bottom && row == rows - 1) q[W2] = pn;
+                    double* q = sp + (tid + 1) * W2 + cols + 1;
+                    *q = rr_ + beta * (k == 1 ? 0.0 : *q);
                 }
             }
             __syncthreads();
@@ -177,13 +169,6 @@ __global__ void __launch_bounds__(kTileThreads, 1) cg_tile_kernel(const __grid_c
                     up = cur;
                     cur = dn;
                 }
-                // publish p's edges: own column's top / bottom value, and the tile's side columns
-                ex_p[cur_par + mine + c] = sp[W2 + c + 1];
-                ex_p[cur_par + mine + tcols + c] = sp[rows * W2 + c + 1];
-            }
-            if (tid < rows) {
-                ex_p[cur_par + mine + 2 * tcols + tid] = sp[(tid + 1) * W2 + 1];
-                ex_p[cur_par + mine + 2 * tcols + trows + tid] = sp[(tid + 1) * W2 + cols];
             }
             HIVC_TRACE(2);
             if (P.trace && tid == 0 && k < 256) P.trace[2048 + k * 160 + (tile < 160 ? tile : 159)] = globaltimer_ns();
@@ -225,30 +210,40 @@ __global__ void __launch_bounds__(kTileThreads, 1) cg_tile_kernel(const __grid_c
             }
             HIVC_TRACE(4);
             grid_reduce_arrive<1>(e1, sh, P, red, tile);
-            // x += alpha p while the other CTAs arrive (x is not read until the level ends)
+            // x += alpha p while the other CTAs arrive (x is not read until the level ends);
+            // the first streamed rows' loads go out before the resident rows are updated
             if (act) {
+                constexpr int kPre = 4;
+                double xv[kPre];
+#pragma unroll
+                for (int j = 0; j < kPre; ++j) {
+                    const int row = xr + j;
+                    xv[j] = row < rows ? P.x[(size_t)(y0 + row) * w + gc] : 0.0;
+                }
 #pragma unroll
                 for (int row = 0; row < ROWS; ++row) {
                     if (row >= xr || row >= rows) break;
                     double& xs = sx[row * tcols + c];
                     xs = xs + alpha * sp[(row + 1) * W2 + c + 1];
                 }
-                // streamed rows, 8 at a time with the loads issued first
 #pragma unroll
-                for (int g = 0; g < ROWS; g += 8) {
-                    if (g + 8 <= xr || g >= rows) continue;
-                    double xv[8];
+                for (int j = 0; j < kPre; ++j) {
+                    const int row = xr + j;
+                    if (row < rows) P.x[(size_t)(y0 + row) * w + gc] = xv[j] + alpha * sp[(row + 1) * W2 + c + 1];
+                }
+                // further streamed rows, 8 at a time with the loads issued first
+#pragma unroll 1
+                for (int g = xr + kPre; g < rows; g += 8) {
+                    double xw[8];
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
                         const int row = g + j;
-                        xv[j] = 0.0;
-                        if (row >= xr && row < rows) xv[j] = P.x[(size_t)(y0 + row) * w + gc];
+                        xw[j] = row < rows ? P.x[(size_t)(y0 + row) * w + gc] : 0.0;
                     }
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
                         const int row = g + j;
-                        if (row >= xr && row < rows)
-                            P.x[(size_t)(y0 + row) * w + gc] = xv[j] + alpha * sp[(row + 1) * W2 + c + 1];
+                        if (row < rows) P.x[(size_t)(y0 + row) * w + gc] = xw[j] + alpha * sp[(row + 1) * W2 + c + 1];
                     }
                 }
             }

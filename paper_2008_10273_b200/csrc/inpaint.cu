@@ -101,7 +101,6 @@ struct CgParams {
     // band kernel: CTA b owns rows [b*band_rows, min(h, (b+1)*band_rows))
     int band_rows;
     double* ex_r;  // [nbands][2][w]: first/last owned row of r
-    double* ex_p;  // [2 parity][nbands][2][w]: first/last owned row of p
     int x_rows = 0;  // tile: leading rows whose x lives in shared memory (the rest streams)
     // tile kernel: tiles of band_rows x tile_cols, ntc tiles per row of tiles
     int tile_cols = 0, ntc = 1;
@@ -518,7 +517,7 @@ namespace {
 struct TilePlan {
     bool ok = false;
     int trows = 0, tcols = 0, ntc = 0, nt = 0, xr = 0;
-    size_t smem = 0, ex = 0;  // dynamic smem bytes, exchange doubles (r + 2 parities of p)
+    size_t smem = 0, ex = 0;  // dynamic smem bytes, exchange doubles (the tiles' r edges)
 };
 TilePlan plan_tiles(int h, int w, int budget) {
     TilePlan T;
@@ -539,7 +538,7 @@ TilePlan plan_tiles(int h, int w, int budget) {
     T.nt = ntr * tc;
     T.xr = xr;
     T.smem = p_bytes + (size_t)xr * tcols * sizeof(double);
-    T.ex = 3 * (size_t)T.nt * (2 * (size_t)tcols + 2 * (size_t)trows);
+    T.ex = (size_t)T.nt * (2 * (size_t)tcols + 2 * (size_t)trows);
     return T;
 }
 
@@ -768,7 +767,6 @@ int solve_batch_async(const SolveJob* jobs, int K, int h, int w, double tol, int
                 P[j].ntc = TP.ntc;
                 P[j].x_rows = TP.xr;
                 P[j].ex_r = ws.ex;
-                P[j].ex_p = ws.ex + (size_t)TP.nt * E;
                 SB.P[j] = P[j];
                 SB.partials[j] = ws.partials + 4096;
                 TB.P[j] = P[j];
@@ -903,7 +901,6 @@ int solve_poisson_interior(InpaintWorkspace& ws, cudaStream_t s, const double* r
     P.ntc = TP.ntc;
     P.x_rows = TP.xr;
     P.ex_r = ws.ex;
-    P.ex_p = ws.ex + (size_t)TP.nt * E;
     double* setup = ws.partials + 4096;
     cg_setup_rhs_kernel<<<kSetupCtas, 512, 0, s>>>(P, rhs, setup);
     TileBatch one{};
