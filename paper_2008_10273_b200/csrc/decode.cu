@@ -11,6 +11,8 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <condition_variable>
+#include <functional>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -878,6 +880,92 @@ void frame_task(CallState& cs, Item& it, int fi) {
 
 }  // namespace
 
+// Persistent decode workers: created once, parked between calls, so a call's
+// parse workers all start within microseconds instead of one thread creation
+// after another (the first I-frame parses gate the first solve batch).  A pool
+// thread may lower its scheduling priority during a call (frame tasks); it
+// returns to nice 0 before the next call, and when the process is not allowed
+// to raise it back, `renice_ok()` turns false and later calls keep it.
+class WorkerPool {
+   public:
+    static WorkerPool& get() {
+        static WorkerPool p;
+        return p;
+    }
+    static std::atomic<bool>& renice_ok() {
+        static std::atomic<bool> ok{true};
+        return ok;
+    }
+    // fn(true) on n - 1 pool threads and fn(false) on the caller; false when
+    // the pool is busy with another call (the caller then makes its own threads)
+    bool run(int n, const std::function<void(bool)>& fn) {
+        if (getpid() != pid_) return false;  // a forked child has none of the parent's threads
+        std::unique_lock<std::mutex> busy(run_mu_, std::try_to_lock);
+        if (!busy.owns_lock()) return false;
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            while ((int)th_.size() < n - 1) {
+                const int idx = (int)th_.size();
+                th_.emplace_back([this, idx]() { loop(idx); });
+            }
+            job_ = &fn;
+            want_ = n - 1;
+            pending_ = n - 1;
+            ++gen_;
+        }
+        cv_.notify_all();
+        fn(false);
+        std::unique_lock<std::mutex> lk(mu_);
+        done_cv_.wait(lk, [&]() { return pending_ == 0; });
+        job_ = nullptr;
+        return true;
+    }
+    ~WorkerPool() {
+        if (getpid() != pid_) {  // not ours to join
+            for (auto& t : th_) t.detach();
+            return;
+        }
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : th_) t.join();
+    }
+
+   private:
+    void loop(int idx) {
+        uint64_t seen = 0;
+        for (;;) {
+            const std::function<void(bool)>* job;
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&]() { return stop_ || (gen_ != seen && idx < want_); });
+                if (stop_) return;
+                seen = gen_;
+                job = job_;
+            }
+            (*job)(true);
+            // back to the default priority for the next call's I-frame parses
+            const pid_t tid = (pid_t)syscall(SYS_gettid);
+            if (getpriority(PRIO_PROCESS, (id_t)tid) != 0 && setpriority(PRIO_PROCESS, (id_t)tid, 0) != 0)
+                renice_ok() = false;
+            {
+                std::lock_guard<std::mutex> lk(mu_);
+                if (--pending_ == 0) done_cv_.notify_all();
+            }
+        }
+    }
+    std::mutex run_mu_, mu_;
+    std::condition_variable cv_, done_cv_;
+    std::vector<std::thread> th_;
+    const std::function<void(bool)>* job_ = nullptr;
+    int want_ = 0, pending_ = 0;
+    uint64_t gen_ = 0;
+    bool stop_ = false;
+    const pid_t pid_ = getpid();
+};
+
 void decode_streams(Context& ctx, int nstreams, const uint8_t* const* data, const size_t* len, const int* gop_begin,
                     const int* gop_end, uint8_t* const* out, int out_mode, double* stage_seconds) {
     const bool out_on_device = out_mode == 1;
@@ -991,7 +1079,7 @@ void decode_streams(Context& ctx, int nstreams, const uint8_t* const* data, cons
             if (fi == 0) {
                 intra_phase(cs, items[i]);
             } else {
-                if (pool && !low) {
+                if (pool && !low && WorkerPool::renice_ok()) {
                     setpriority(PRIO_PROCESS, (id_t)syscall(SYS_gettid), 10);
                     low = true;
                 }
@@ -1009,7 +1097,7 @@ void decode_streams(Context& ctx, int nstreams, const uint8_t* const* data, cons
     const int nworkers = std::max(1, std::min(ntasks, kMaxWorkers));
     if (nworkers == 1 || n == 0) {
         worker(false);
-    } else {
+    } else if (!WorkerPool::get().run(nworkers, worker)) {
         std::vector<std::thread> th;
         for (int l = 0; l < nworkers; ++l) th.emplace_back(worker, true);
         for (auto& t : th) t.join();
