@@ -225,9 +225,10 @@ __device__ __forceinline__ void block_reconstruct_8lanes(double* t, int j, const
     aan_fwd(v);
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-        double c = v[i] * kFwdScale2[i * 8 + j];  // dct2: * _FSCALE2
-        c = eig[i * 8 + j] * c;                   // eig * dct2(mc)
-        v[i] = c * kInvScale2[i * 8 + j];         // idct2: coef * _ISCALE2
+        // (lane-indexed tables: global memory through L1, see aan_constants.h)
+        double c = v[i] * __ldg(kFwdScale2 + i * 8 + j);  // dct2: * _FSCALE2
+        c = __ldg(eig + i * 8 + j) * c;                   // eig * dct2(mc)
+        v[i] = c * __ldg(kInvScale2 + i * 8 + j);         // idct2: coef * _ISCALE2
     }
 #pragma unroll
     for (int i = 0; i < 8; ++i) t[i * 8 + j] = v[i];
