@@ -990,6 +990,12 @@ void CgProbe::harvest(CgTotals& t) {
     // after the stream synchronised: accumulate iteration-weighted pixel counts
     // and the grid-mode launches' device time
     std::vector<int> it_of_solve_level;
+    if (!marks.empty())
+        for (const Solve& sv : solves) {  // level iterations per solve, coarsest first
+            std::string line = "[batch] solve " + std::to_string(sv.pixels[0]) + " px levels:";
+            for (int l = 0; l < sv.nlevels; ++l) line += " " + std::to_string(sv.host_iters ? sv.host_iters[l] : -1);
+            std::fprintf(stderr, "%s\n", line.c_str());
+        }
     for (const Solve& sv : solves) {
         t.solves += 1;
         for (int l = 0; l < sv.nlevels; ++l) {
