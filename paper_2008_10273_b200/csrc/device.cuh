@@ -96,20 +96,20 @@ __device__ __forceinline__ void grid_arrive_wait(unsigned int* bar, unsigned int
         unsigned int old;
         asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(bar) : "memory");
         const unsigned int target = epoch * nblocks;
-        while (ld_acquire_gpu(bar) < target) {
-        }
+        if (old + 1 != target)  // the last arrival knows from its own atomic (no poll round trip)
+            while (ld_acquire_gpu(bar) < target) {
+            }
     }
     __syncthreads();
 }
 
 // Split form: arrive (after a CTA barrier that ordered the CTA's global
 // writes), independent work, then wait.
+// The arrival is a release reduction: nothing waits for its round trip, so
+// the work between arrive and wait (its loads included) starts at once.
 __device__ __forceinline__ void grid_arrive(unsigned int* bar, unsigned int& epoch) {
     ++epoch;
-    if (threadIdx.x == 0) {
-        unsigned int old;
-        asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(bar) : "memory");
-    }
+    if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
 }
 __device__ __forceinline__ void grid_wait(const unsigned int* bar, unsigned int nblocks, unsigned int epoch) {
     if (threadIdx.x == 0) {
