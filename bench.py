@@ -32,6 +32,9 @@ import threading
 import time
 from pathlib import Path
 
+# before the CUDA context exists (see paper_2008_10273_b200/__init__.py)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 import numpy as np
 
 REPO = Path(__file__).resolve().parent
