@@ -231,7 +231,14 @@ void Slot::init(int dev) {
     device = dev;
     // (a higher priority for the P-frame streams than for the solver stream
     // measured slower: 4270 vs 4400 frames/s)
-    CUDA_CHECK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    static const bool prio = debug_opt("p_prio") != nullptr;
+    if (prio) {
+        int lo = 0, hi = 0;
+        CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        CUDA_CHECK(cudaStreamCreateWithPriority(&stream, cudaStreamNonBlocking, hi));
+    } else {
+        CUDA_CHECK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    }
     CUDA_CHECK(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking));
     CUDA_CHECK(cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking));
     for (auto& e : up_ev) CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
