@@ -736,7 +736,8 @@ void try_launch(CallState& cs, Item& it) {
                 finalize_intra(cs, it, A, fi);
                 it.intra_frames += 1;
             } else {
-                launch_frame(A, true, L.stream);
+                static const int prep = debug_opt("p_repeat") ? std::atoi(debug_opt("p_repeat")) : 1;
+                for (int rep = 0; rep < prep; ++rep) launch_frame(A, true, L.stream);
                 cs.ctx.launches += 1;
                 it.inter_frames += 1;
             }

@@ -87,6 +87,20 @@ __device__ __forceinline__ unsigned int ld_acquire_gpu(const unsigned int* p) {
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ unsigned int ld_relaxed_gpu(const unsigned int* p) {
+    unsigned int v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+// Wait until *bar >= target.  The spin uses relaxed loads: an acquire load
+// invalidates the SM's L1 (CCTL.IVALL) every time, which stalls the other
+// warps' shared-memory traffic for as long as the poll runs; one acquire
+// load of the final value then orders the caller's later reads.
+__device__ __forceinline__ void wait_geq_acquire(const unsigned int* bar, unsigned int target) {
+    while (ld_relaxed_gpu(bar) < target) {
+    }
+    (void)ld_acquire_gpu(bar);
+}
 // Barrier tail for callers that already synchronised the CTA after their last
 // global writes (e.g. through block_sum1): thread 0 arrives and waits, then
 // the CTA is released.
@@ -97,8 +111,7 @@ __device__ __forceinline__ void grid_arrive_wait(unsigned int* bar, unsigned int
         asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(bar) : "memory");
         const unsigned int target = epoch * nblocks;
         if (old + 1 != target)  // the last arrival knows from its own atomic (no poll round trip)
-            while (ld_acquire_gpu(bar) < target) {
-            }
+            wait_geq_acquire(bar, target);
     }
     __syncthreads();
 }
@@ -114,8 +127,7 @@ __device__ __forceinline__ void grid_arrive(unsigned int* bar, unsigned int& epo
 __device__ __forceinline__ void grid_wait(const unsigned int* bar, unsigned int nblocks, unsigned int epoch) {
     if (threadIdx.x == 0) {
         const unsigned int target = epoch * nblocks;
-        while (ld_acquire_gpu(bar) < target) {
-        }
+        wait_geq_acquire(bar, target);
     }
     __syncthreads();
 }
@@ -127,8 +139,7 @@ __device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int nbl
         unsigned int old;
         asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(bar) : "memory");
         const unsigned int target = epoch * nblocks;
-        while (ld_acquire_gpu(bar) < target) {
-        }
+        wait_geq_acquire(bar, target);
     }
     __syncthreads();
 }

@@ -104,6 +104,8 @@ struct CgParams {
     int x_rows = 0;  // tile: leading rows whose x lives in shared memory (the rest streams)
     // tile kernel: tiles of band_rows x tile_cols, ntc tiles per row of tiles
     int tile_cols = 0, ntc = 1;
+    unsigned long long* flags = nullptr;  // tile kernel: per-tile tags (nonce << 32 | iteration) of published r edges
+    unsigned int nonce = 0;
     unsigned long long* trace = nullptr;  // diagnostics: per-iteration phase timestamps of CTA 0
     unsigned long long* stamp = nullptr;  // probe: globaltimer at kernel entry / exit (CTA 0)
 };
@@ -449,6 +451,8 @@ void InpaintWorkspace::reserve(int h, int w, int dev) {
     CUDA_CHECK(cudaMalloc(&partials, (size_t)(4096 + kSetupCtas * 4 + 64) * sizeof(double)));
     CUDA_CHECK(cudaMalloc(&bar, 64 * sizeof(unsigned int)));
     CUDA_CHECK(cudaMemset(bar, 0, 64 * sizeof(unsigned int)));
+    CUDA_CHECK(cudaMalloc(&flags, 512 * sizeof(unsigned long long)));
+    CUDA_CHECK(cudaMemset(flags, 0, 512 * sizeof(unsigned long long)));
     CUDA_CHECK(cudaMalloc(&iters, 64 * sizeof(int)));
     CUDA_CHECK(cudaMalloc(&margins, 64 * sizeof(double)));
     // tile-kernel edge exchange: r + 2 parities of p, every tile's perimeter
@@ -457,7 +461,9 @@ void InpaintWorkspace::reserve(int h, int w, int dev) {
     cap_px = n;
     cap_w = w;
     cap_coarse = coarse;
-    CUDA_CHECK(cudaFuncSetAttribute(cg_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmem));
+    for (TileKernelFn fn : {tile_kernel_for(30, 480), tile_kernel_for(23, 480), tile_kernel_for(15, 480),
+                            tile_kernel_for(0, 0)})
+        CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kTileSmem));
     // 16-CTA clusters (non-portable size) for the coarse/mid levels, when this device can host one
     cluster_ok = cudaFuncSetAttribute(cg_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
                      cudaSuccess &&
@@ -491,6 +497,8 @@ void InpaintWorkspace::release() {
     if (bytes) cudaFree(bytes);
     if (partials) cudaFree(partials);
     if (bar) cudaFree(bar);
+    if (flags) cudaFree(flags);
+    flags = nullptr;
     if (iters) cudaFree(iters);
     if (margins) cudaFree(margins);
     if (ex) cudaFree(ex);
@@ -577,6 +585,7 @@ CgParams level_params(const JobLevels& J, InpaintWorkspace& ws, const std::vecto
     P.finest = l == 0;
     P.partials = ws.partials;
     P.bar = ws.bar;
+    P.flags = ws.flags;
     P.iters = ws.iters + (L - 1 - l);
     P.margin = ws.margins + (L - 1 - l);
     return P;
@@ -767,6 +776,7 @@ int solve_batch_async(const SolveJob* jobs, int K, int h, int w, double tol, int
                 P[j].ntc = TP.ntc;
                 P[j].x_rows = TP.xr;
                 P[j].ex_r = ws.ex;
+                P[j].nonce = ++ws.nonce;
                 SB.P[j] = P[j];
                 SB.partials[j] = ws.partials + 4096;
                 TB.P[j] = P[j];
@@ -792,7 +802,8 @@ int solve_batch_async(const SolveJob* jobs, int K, int h, int w, double tol, int
             TB.nt = TP.nt;
             if (ticketed) {
                 TB.ticket = ticket;
-                cg_tile_kernel<<<TP.nt * K, kTileThreads, TP.smem, s>>>(TB);
+                tile_kernel_for(TP.trows, TP.tcols)<<<TP.nt * K, kTileThreads,
+                                                            TP.smem, s>>>(TB);
                 ++*launches;
             } else {
                 for (int j = 0; j < K; ++j) {
@@ -802,8 +813,10 @@ int solve_batch_async(const SolveJob* jobs, int K, int h, int w, double tol, int
                     one.nt = TP.nt;
                     one.ticket = nullptr;
                     void* args[] = {&one};
-                    CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)cg_tile_kernel, dim3(TP.nt),
-                                                           dim3(kTileThreads), args, TP.smem, s));
+                    CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)tile_kernel_for(TP.trows, TP.tcols),
+                                                           dim3(TP.nt),
+                                                           dim3(kTileThreads), args,
+                                                           TP.smem, s));
                     ++*launches;
                     if (l == 0 && jobs[j].done) {
                         CUDA_CHECK(cudaEventRecord(jobs[j].done, s));
@@ -891,6 +904,7 @@ int solve_poisson_interior(InpaintWorkspace& ws, cudaStream_t s, const double* r
     P.finest = 0;  // denominator ||b||
     P.partials = ws.partials;
     P.bar = ws.bar;
+    P.flags = ws.flags;
     P.iters = ws.iters;
     P.margin = ws.margins;
     const TilePlan TP = plan_tiles(h, w, ws.num_sms);
@@ -901,6 +915,7 @@ int solve_poisson_interior(InpaintWorkspace& ws, cudaStream_t s, const double* r
     P.ntc = TP.ntc;
     P.x_rows = TP.xr;
     P.ex_r = ws.ex;
+    P.nonce = ++ws.nonce;
     double* setup = ws.partials + 4096;
     cg_setup_rhs_kernel<<<kSetupCtas, 512, 0, s>>>(P, rhs, setup);
     TileBatch one{};
@@ -909,7 +924,8 @@ int solve_poisson_interior(InpaintWorkspace& ws, cudaStream_t s, const double* r
     one.nt = TP.nt;
     one.ticket = nullptr;
     void* args[] = {&one};
-    CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)cg_tile_kernel, dim3(TP.nt), dim3(kTileThreads), args,
+    CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)tile_kernel_for(TP.trows, TP.tcols), dim3(TP.nt),
+                                           dim3(kTileThreads), args,
                                            TP.smem, s));
     *launches += 3;
     CUDA_CHECK(cudaGetLastError());
