@@ -104,8 +104,6 @@ struct CgParams {
     int x_rows = 0;  // tile: leading rows whose x lives in shared memory (the rest streams)
     // tile kernel: tiles of band_rows x tile_cols, ntc tiles per row of tiles
     int tile_cols = 0, ntc = 1;
-    unsigned long long* flags = nullptr;  // tile kernel: per-tile tags (nonce << 32 | iteration) of published r edges
-    unsigned int nonce = 0;
     unsigned long long* trace = nullptr;  // diagnostics: per-iteration phase timestamps of CTA 0
     unsigned long long* stamp = nullptr;  // probe: globaltimer at kernel entry / exit (CTA 0)
 };
@@ -451,8 +449,6 @@ void InpaintWorkspace::reserve(int h, int w, int dev) {
     CUDA_CHECK(cudaMalloc(&partials, (size_t)(4096 + kSetupCtas * 4 + 64) * sizeof(double)));
     CUDA_CHECK(cudaMalloc(&bar, 64 * sizeof(unsigned int)));
     CUDA_CHECK(cudaMemset(bar, 0, 64 * sizeof(unsigned int)));
-    CUDA_CHECK(cudaMalloc(&flags, 512 * sizeof(unsigned long long)));
-    CUDA_CHECK(cudaMemset(flags, 0, 512 * sizeof(unsigned long long)));
     CUDA_CHECK(cudaMalloc(&iters, 64 * sizeof(int)));
     CUDA_CHECK(cudaMalloc(&margins, 64 * sizeof(double)));
     // tile-kernel edge exchange: r + 2 parities of p, every tile's perimeter
@@ -497,8 +493,6 @@ void InpaintWorkspace::release() {
     if (bytes) cudaFree(bytes);
     if (partials) cudaFree(partials);
     if (bar) cudaFree(bar);
-    if (flags) cudaFree(flags);
-    flags = nullptr;
     if (iters) cudaFree(iters);
     if (margins) cudaFree(margins);
     if (ex) cudaFree(ex);
@@ -585,7 +579,6 @@ CgParams level_params(const JobLevels& J, InpaintWorkspace& ws, const std::vecto
     P.finest = l == 0;
     P.partials = ws.partials;
     P.bar = ws.bar;
-    P.flags = ws.flags;
     P.iters = ws.iters + (L - 1 - l);
     P.margin = ws.margins + (L - 1 - l);
     return P;
@@ -776,7 +769,6 @@ int solve_batch_async(const SolveJob* jobs, int K, int h, int w, double tol, int
                 P[j].ntc = TP.ntc;
                 P[j].x_rows = TP.xr;
                 P[j].ex_r = ws.ex;
-                P[j].nonce = ++ws.nonce;
                 SB.P[j] = P[j];
                 SB.partials[j] = ws.partials + 4096;
                 TB.P[j] = P[j];
@@ -904,7 +896,6 @@ int solve_poisson_interior(InpaintWorkspace& ws, cudaStream_t s, const double* r
     P.finest = 0;  // denominator ||b||
     P.partials = ws.partials;
     P.bar = ws.bar;
-    P.flags = ws.flags;
     P.iters = ws.iters;
     P.margin = ws.margins;
     const TilePlan TP = plan_tiles(h, w, ws.num_sms);
@@ -915,7 +906,6 @@ int solve_poisson_interior(InpaintWorkspace& ws, cudaStream_t s, const double* r
     P.ntc = TP.ntc;
     P.x_rows = TP.xr;
     P.ex_r = ws.ex;
-    P.nonce = ++ws.nonce;
     double* setup = ws.partials + 4096;
     cg_setup_rhs_kernel<<<kSetupCtas, 512, 0, s>>>(P, rhs, setup);
     TileBatch one{};

@@ -40,8 +40,6 @@ struct InpaintWorkspace {
     uint8_t* bytes = nullptr;
     double* partials = nullptr;
     unsigned int* bar = nullptr;
-    unsigned long long* flags = nullptr;  // tile kernel: per-tile "r edges published" tags (kMaxTiles)
-    unsigned int nonce = 0;               // host: tile launches so far (tags of a launch never match an older one's)
     int* iters = nullptr;      // device: per level (coarse -> fine) CG iterations
     double* margins = nullptr; // device: per level min relative stop-test margin
     cudaEvent_t pre_done = nullptr;  // solve_batch_async: side-stream levels done
