@@ -28,7 +28,9 @@ void set_last_error(const std::string& msg);
 // Keys: timeline, cg_trace, cg_trace_cluster, batch_trace (diagnostic dumps);
 // workers, min_batch, tree_threads, tree_threads_small, enc_threads (host
 // threading); brox_graph, brox_jc_max, brox_j2_min (Brox launch paths, for the
-// bit-identity tests).  Absent keys return nullptr; no key changes a result.
+// bit-identity tests); p_repeat=N (each P-frame kernel launched N times: the
+// step's sensitivity to that kernel).  Absent keys return nullptr; no key
+// changes a result.
 inline const char* debug_opt(const char* key) {
     static const std::vector<std::pair<std::string, std::string>> opts = [] {
         std::vector<std::pair<std::string, std::string>> v;
