@@ -39,17 +39,15 @@ struct RestrictBatch {  // blockIdx.y = solve
     uint8_t* mc[16];
 };
 
-__global__ void restrict_kernel(const __grid_constant__ RestrictBatch B, int h, int w, int hc, int wc) {
-    const double* __restrict__ f = B.f[blockIdx.y];
-    const uint8_t* __restrict__ m = B.m[blockIdx.y];
-    double* __restrict__ fc = B.fc[blockIdx.y];
-    uint8_t* __restrict__ mc = B.mc[blockIdx.y];
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= hc * wc) return;
+// One coarse pixel i of a 2x restriction (homogeneous.py:110-130): mask = any
+// fine mask pixel, f = mean of the masked fine values (else of all of them);
+// np.add.reduceat over rows, then over columns (homogeneous.py:121-122).
+__device__ __forceinline__ void restrict_px(const double* __restrict__ f, const uint8_t* __restrict__ m,
+                                            double* __restrict__ fc, uint8_t* __restrict__ mc, int h, int w, int wc,
+                                            int i) {
     int cy = i / wc, cx = i % wc;
     int r0 = 2 * cy, c0 = 2 * cx;
     bool hr = r0 + 1 < h, hcol = c0 + 1 < w;
-    // np.add.reduceat over rows, then over columns (homogeneous.py:121-122)
     auto at = [&](int r, int c, int kind) -> double {
         size_t k = (size_t)r * w + c;
         bool mk = m[k] != 0;
@@ -75,6 +73,38 @@ __global__ void restrict_kernel(const __grid_constant__ RestrictBatch B, int h, 
     bool cm = tot[0] > 0.0;
     fc[i] = cm ? tot[1] / fmax(tot[0], 1.0) : avg;
     mc[i] = cm ? 1 : 0;
+}
+
+__global__ void restrict_kernel(const __grid_constant__ RestrictBatch B, int h, int w, int hc, int wc) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= hc * wc) return;
+    restrict_px(B.f[blockIdx.y], B.m[blockIdx.y], B.fc[blockIdx.y], B.mc[blockIdx.y], h, w, wc, i);
+}
+
+// The small levels of the pyramid in one launch: one 8-CTA cluster per solve
+// (blockIdx.y) restricts level after level, a cluster barrier between them
+// (release / acquire at cluster scope: the level just written is visible to
+// every CTA of the cluster).  Replaces one ~5 us latency-bound launch per level.
+constexpr int kRestrictChainMax = 8;
+constexpr int kRestrictCluster = 8;
+constexpr int kRestrictChainMaxPx = 8192;  // coarse pixels of the largest chained level
+struct RestrictChain {
+    int nlev;  // restrictions: level l -> l + 1 for l < nlev
+    int h[kRestrictChainMax + 1], w[kRestrictChainMax + 1];
+    const double* f[kMaxBatch][kRestrictChainMax + 1];
+    const uint8_t* m[kMaxBatch][kRestrictChainMax + 1];
+};
+__global__ void __cluster_dims__(kRestrictCluster, 1, 1) __launch_bounds__(512)
+    restrict_chain_kernel(const __grid_constant__ RestrictChain C) {
+    const int j = blockIdx.y;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x, nth = kRestrictCluster * blockDim.x;
+    for (int l = 0; l < C.nlev; ++l) {
+        const int nc = C.h[l + 1] * C.w[l + 1];
+        for (int i = t; i < nc; i += nth)
+            restrict_px(C.f[j][l], C.m[j][l], const_cast<double*>(C.f[j][l + 1]), const_cast<uint8_t*>(C.m[j][l + 1]),
+                        C.h[l], C.w[l], C.w[l + 1], i);
+        if (l + 1 < C.nlev) cooperative_groups::this_cluster().sync();
+    }
 }
 
 // ---------------------------------------------------------------- CG level kernel
@@ -635,7 +665,12 @@ int solve_batch_async(const SolveJob* jobs, int K, int h, int w, double tol, int
     };
     // ---- pyramid (homogeneous.py:96-130): one launch per level for the whole batch
     mb("restrict", sp);
-    for (int l = 1; l < L; ++l) {
+    int l_chain = L;  // levels >= l_chain - 1 restricted by the chained cluster launch
+    while (l_chain - 1 >= 1 && L - (l_chain - 1) <= kRestrictChainMax &&
+           (size_t)shapes[l_chain - 1].first * shapes[l_chain - 1].second <= (size_t)kRestrictChainMaxPx)
+        --l_chain;
+    if (L - l_chain < 2) l_chain = L;  // a single small level: the plain launch
+    for (int l = 1; l < l_chain; ++l) {
         RestrictBatch RB{};
         for (int j = 0; j < K; ++j) {
             RB.f[j] = J[j].f[l - 1];
@@ -646,6 +681,20 @@ int solve_batch_async(const SolveJob* jobs, int K, int h, int w, double tol, int
         const size_t nl = (size_t)shapes[l].first * shapes[l].second;
         restrict_kernel<<<dim3((unsigned)((nl + 255) / 256), K), 256, 0, sp>>>(
             RB, shapes[l - 1].first, shapes[l - 1].second, shapes[l].first, shapes[l].second);
+        ++*launches;
+    }
+    if (l_chain < L) {
+        RestrictChain RC{};
+        RC.nlev = L - l_chain;
+        for (int q = 0; q <= RC.nlev; ++q) {
+            RC.h[q] = shapes[l_chain - 1 + q].first;
+            RC.w[q] = shapes[l_chain - 1 + q].second;
+            for (int j = 0; j < K; ++j) {
+                RC.f[j][q] = J[j].f[l_chain - 1 + q];
+                RC.m[j][q] = J[j].m[l_chain - 1 + q];
+            }
+        }
+        restrict_chain_kernel<<<dim3(kRestrictCluster, K), 512, 0, sp>>>(RC);
         ++*launches;
     }
     me(sp);
@@ -783,7 +832,7 @@ int solve_batch_async(const SolveJob* jobs, int K, int h, int w, double tol, int
             const bool ticketed = pack_t && K > 1;
             SB.ticket = ticketed ? ticket : nullptr;
             mb("setup l=" + std::to_string(l), s);
-            cg_setup_x_kernel<<<dim3(kSetupCtas, K), 512, 0, s>>>(SB);
+            cg_setup_x_kernel<<<dim3((unsigned)(ww + 255) / 256, (unsigned)(hh + kSetupXRows - 1) / kSetupXRows, K), 256, 0, s>>>(SB);
             cg_setup_kernel<<<dim3(kSetupCtas, K), 512, 0, s>>>(SB);
             me(s);
             *launches += 2;
