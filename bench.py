@@ -267,7 +267,7 @@ def reference_arm(args, rank):
 # ----------------------------------------------------------------------------- rooflines
 
 ONCHIP = REPO / "profiles" / "r02_onchip_peaks.json"     # tools/onchip_peaks.py on this pool's B200
-KMETRICS = REPO / "profiles" / "r02_kernel_metrics.json"  # ncu capture of this bench's own launches
+KMETRICS = REPO / "profiles" / "r02h_kernel_metrics.json"  # ncu capture of this bench's own launches
 # shared-memory bytes per pixel per CG iteration in cg_tile_kernel (counted from the code,
 # 8-byte accesses): p = r + beta p (load + store), A p (3 loads: row below + 2 sides; the
 # rows above / here ride in registers), r -= alpha A p (3 loads again), x += alpha p (3)
@@ -297,13 +297,13 @@ def roofline_rows(gsec, glaunch, gpix_it, gpix, pix_it, peaks):
     px_per_launch = gpix / glaunch if glaunch else None
     smem_bytes = SMEM_B_PX_IT * gpix_it / glaunch if glaunch else None
     achieved = smem_bytes / t_launch / 1e9 if t_launch else None
-    name, kt = _kernel_row(km, r"cg_tile_kernel")
+    name, kt = _kernel_row(km, r"cg_tile_kernel<30, 480>")
     floor = None
     if t_launch and smem_peak and sum_us and it_per_launch:
         floor = smem_bytes / (smem_peak * 1e9) + it_per_launch * 2 * sum_us * 1e-6
     top = {
-        "kernel": "cg_tile_kernel (CG level on chip: 30x480 tiles, r in registers, p + ~all of x in shared memory, "
-                  "two fixed-order grid sums per iteration; float64)",
+        "kernel": "cg_tile_kernel<30, 480> (CG level on chip: 30x480 tiles, r in registers, p + ~all of x in shared "
+                  "memory, two fixed-order grid sums per iteration, the second run by the idle 16th warp; float64)",
         "bound": "smem",
         "achieved": achieved,
         "peak": smem_peak,
@@ -334,11 +334,14 @@ def roofline_rows(gsec, glaunch, gpix_it, gpix, pix_it, peaks):
         "peak_source": f"{ONCHIP.name} smem_load_GBps (measured)" if smem_peak else "missing",
     }
     rows = []
-    for label, pat, bound in [("cg_tile_kernel", r"cg_tile_kernel", "smem"),
+    for label, pat, bound in [("cg_tile_kernel<30, 480>", r"cg_tile_kernel<30, 480>", "smem"),
+                              ("cg_tile_kernel<23, 480>", r"cg_tile_kernel<23, 480>", "smem"),
+                              ("cg_tile_kernel<15, 480>", r"cg_tile_kernel<15, 480>", "smem"),
                               ("cg_cluster_col_kernel", r"cg_cluster_col_kernel", "smem"),
                               ("frame_kernel P (fused warp + residual + rint/clip)", r"frame_kernel<(1|true), 1", "latency"),
                               ("frame_kernel I (finalize)", r"frame_kernel<(0|false), 1", "latency"),
-                              ("restrict_kernel", r"restrict_kernel", "hbm")]:
+                              ("restrict_kernel", r"restrict_kernel", "hbm"),
+                              ("cg_setup_kernel", r"cg_setup_kernel", "hbm")]:
         n, r = _kernel_row(km, pat)
         if not r:
             continue
