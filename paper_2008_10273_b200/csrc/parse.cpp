@@ -620,6 +620,69 @@ static size_t intra_tree_par(const uint8_t* d, size_t pos, uint32_t nbits, int32
     return nleaves;
 }
 
+// A medium gray plane's tree walked by the parse thread and the value-decode
+// helper together: the parse thread cuts the tree into subtrees and starts
+// walking them while the helper decodes the entropy-coded values
+// (decode_vals), after which the helper takes the remaining subtrees.  The two
+// sections of a 540p I-frame (~0.2 ms of values, ~0.5 ms of tree) then end
+// together instead of the tree alone gating the solve.  Any failure reruns the
+// sequential walk (the reference's error, in stream order).
+template <class V>
+static size_t intra_tree_coop(const uint8_t* d, size_t pos, uint32_t nbits, int32_t h, int32_t w,
+                              std::vector<uint64_t>& bits, std::vector<uint64_t>& local, int depth, V&& decode_vals) {
+    const uint8_t* tb = d + pos + 4;
+    const size_t nbytes = ((size_t)nbits + 7) / 8;
+    std::vector<TreeTask> tasks;
+    std::atomic<int> state{0};  // 0: cutting, 1: tasks ready, 2: cut failed
+    std::atomic<int> next{0};
+    std::atomic<bool> bad{false};
+    auto run = [&]() {
+        for (int i; (i = next.fetch_add(1)) < (int)tasks.size();) {
+            TreeTask& t = tasks[i];
+            try {
+                t.end = intra_tree_walk(tb, nbytes, nbits, t.start, t.x, t.y, t.w, t.h, t.x, t.y, t.stride,
+                                        local.data() + t.off, t.nleaves);
+            } catch (const Error&) {
+                bad = true;
+            }
+        }
+    };
+    std::thread helper([&]() {
+        decode_vals();
+        int st;
+        while ((st = state.load(std::memory_order_acquire)) == 0) std::this_thread::yield();
+        if (st == 1) run();
+    });
+    bool cut = true;
+    try {
+        tree_tasks(tb, nbits, 0, 0, 0, w, h, depth, tasks);
+    } catch (const Error&) {
+        cut = false;
+    }
+    if (cut) {
+        size_t words = 0;
+        for (TreeTask& t : tasks) {
+            t.stride = ((size_t)t.w + 63) / 64 * 64;
+            t.off = words;
+            words += (size_t)t.h * (t.stride / 64);
+        }
+        local.assign(words, 0);
+        state.store(1, std::memory_order_release);
+        run();
+    } else {
+        state.store(2, std::memory_order_release);
+    }
+    helper.join();
+    if (!cut || bad) return intra_tree_seq(d, pos, nbits, h, w, bits);
+    bits.assign(((size_t)h * w + 63) / 64, 0);
+    size_t nleaves = 0;
+    for (const TreeTask& t : tasks) {
+        merge_rect_bits(local.data() + t.off, t.stride, t.x, t.y, t.w, t.h, w, bits.data(), bits.size());
+        nleaves += t.nleaves;
+    }
+    return nleaves;
+}
+
 // Raster-ordered mask points (flat indices) of a bitmap; `threads` ranges in parallel.
 static void intra_points(const std::vector<uint64_t>& bits, size_t nleaves, std::vector<int32_t>& pts, int threads) {
     const size_t nw = bits.size();
@@ -748,6 +811,20 @@ size_t parse_intra(const uint8_t* d, size_t len, size_t pos, int32_t h, int32_t 
     };
     std::thread helper;
     const bool par = npx >= (1u << 18) && kHw > 1;
+    if (par && ntrees == 1 && tree_threads == 1) {
+        // a medium gray plane: tree and values on the same two threads (intra_tree_coop)
+        try {
+            const size_t nl = intra_tree_coop(d, tpos[0], tbits[0], h, w, bits, job.local, 3, decode_vals);
+            intra_points(bits, nl, job.pts[0], 1);
+        } catch (...) {
+            terr[0] = std::current_exception();
+        }
+        if (terr[0]) std::rethrow_exception(terr[0]);
+        if (verr[0]) std::rethrow_exception(verr[0]);
+        intra_dequantize(d, vpos[0], levels, idx[0], job.pts[0].size(), job.vals[0]);
+        job.nchan = 1;
+        return end;
+    }
     if (par)
         helper = std::thread([&]() {
             helper_priority();

@@ -157,3 +157,77 @@ def test_byte_flip_fuzz_matches_oracle_error_class(payloads):
         else:
             with pytest.raises(kinds.get(ref_err, ValueError)):
                 entropy.decode_signed_values(b, 0)
+
+
+def _parse_stream_stats(data):
+    """hivc_parse_stream's per-frame stats rows (type, intra points, ...)."""
+    import ctypes as C
+
+    cap = 8 * 4096
+    stats = (C.c_int64 * cap)()
+    nf = C.c_int64()
+    secs = C.c_double()
+    buf = C.create_string_buffer(data, len(data))
+    N.check(N.lib.hivc_parse_stream(buf, len(data), stats, cap, C.byref(nf), C.byref(secs)))
+    return np.array(stats[: 8 * nf.value], dtype=np.int64).reshape(-1, 8)
+
+
+def _first_intra_tree(stream):
+    """(offset of the tree's u32 bit count in the stream, nbits) of GOP 0's I-frame."""
+    hdr = bitstream.read_stream(stream)
+    gop0 = 22 + 4  # header, then the first GOP's u32 length
+    off = gop0 + 2 + 5  # frame count, record type + prediction length
+    (nbits,) = struct.unpack_from("<I", stream, off)
+    return hdr, off, nbits
+
+
+def test_medium_gray_tree_two_thread_walk_matches_oracle():
+    """540p gray I-frames take the two-thread walk (tree subtrees shared with
+    the value-decode helper): mask point counts equal the oracle's leaves."""
+    from pathlib import Path
+
+    data = (Path(__file__).parent / "golden" / "streams" / "cfg3_Cb.hivc").read_bytes()
+    rows = _parse_stream_stats(data)
+    _, off, nbits = _first_intra_tree(data)
+    nb = (nbits + 7) // 8
+    ref = P.tree_leaves(P.Bits(data[off + 4 : off + 4 + nb], nbits), 960, 540)
+    assert rows[0, 0] == 0 and rows[0, 1] == len(ref)
+
+
+@pytest.mark.parametrize("seed", [5, 9, 10, 11])
+def test_medium_gray_tree_corruption_matches_oracle_error_class(seed):
+    """Corrupt 540p trees (seeds whose flips the oracle rejects) raise the
+    oracle's class through the two-thread walk (its failure path reruns the
+    sequential walk for the first error in stream order)."""
+    from pathlib import Path
+
+    data = bytearray((Path(__file__).parent / "golden" / "streams" / "cfg3_Cb.hivc").read_bytes())
+    _, off, nbits = _first_intra_tree(bytes(data))
+    nb = (nbits + 7) // 8
+    rng = np.random.default_rng(seed)
+    for _ in range(3):  # flip bytes inside the tree
+        i = off + 4 + int(rng.integers(nb))
+        data[i] ^= int(rng.integers(1, 256))
+    try:
+        P.tree_leaves(P.Bits(bytes(data[off + 4 : off + 4 + nb]), nbits), 960, 540)
+        ref_err = None
+    except P.OracleError as e:
+        ref_err = e.kind
+    assert ref_err is not None
+    kinds = {"Truncated": errors.TruncatedStream, "SubdivisionError": errors.SubdivisionError}
+    with pytest.raises(kinds[ref_err]):
+        _parse_stream_stats(bytes(data))
+
+
+def test_medium_gray_tree_truncated_raises_truncated():
+    from pathlib import Path
+
+    data = bytearray((Path(__file__).parent / "golden" / "streams" / "cfg3_Cb.hivc").read_bytes())
+    _, off, nbits = _first_intra_tree(bytes(data))
+    nb = (nbits + 7) // 8
+    tail = bytes(data[off + 4 + nb // 2 : off + 4 + nb])
+    data[off + 4 + nb // 2 : off + 4 + nb] = bytes(len(tail))  # the tree's second half all splits? no: zeros = leaves
+    for k in range(off + 4 + nb // 2, off + 4 + nb):
+        data[k] = 0xFF  # all splits: the tree runs out of bits
+    with pytest.raises((errors.TruncatedStream, errors.SubdivisionError)):
+        _parse_stream_stats(bytes(data))
