@@ -484,9 +484,11 @@ struct Item {
 };
 
 // Same-shape items whose I-frame solves are issued as batches: as soon as
-// kMinBatch of them are parsed (a packed band level runs 4 side by side), and
-// the rest when the last one is.
-constexpr int kMinBatch = 4;
+// kMinBatch of them are parsed (a packed band level runs up to 4 side by
+// side), and the rest when the last one is.  3 measured better than 4 for
+// config 3 (three runs each on one box: 5828-5912 vs 5679-5770 frames/s,
+// e2e 5337-5454 vs 4915-5012; profiles/r02_summary.md).
+constexpr int kMinBatch = 3;
 struct Group {
     int h = 0, w = 0, c = 0;
     std::vector<int> items;
