@@ -175,13 +175,32 @@ __global__ void __launch_bounds__(32 * kFrameWarps, kFrameMinBlocks) frame_kerne
             for (int c = 0; c < C; ++c) {
                 const RT* __restrict__ p = reinterpret_cast<const RT*>(A.prev[c]);
                 RT t00[kRowsL], t01[kRowsL], t10[kRowsL], t11[kRowsL];
+                if (sizeof(RT) == 1) {
+                    // gray: one address per tap row, the right taps at +1.  Where the
+                    // reference clamps x1 = x0 (x0 = w-1) the coordinate was clamped to
+                    // exactly w-1, so fx = 0 and w01 = w11 = 0 multiply whatever byte
+                    // follows (the next row's first, or the first byte of the frame
+                    // after the previous one in the GOP buffer): the sum is unchanged.
 #pragma unroll
-                for (int r = 0; r < kRowsL; ++r) {
-                    if (r < rows) {
-                        t00[r] = __ldg(p + ra[r] + x0);
-                        t01[r] = __ldg(p + ra[r] + x1);
-                        t10[r] = __ldg(p + rb[r] + x0);
-                        t11[r] = __ldg(p + rb[r] + x1);
+                    for (int r = 0; r < kRowsL; ++r) {
+                        if (r < rows) {
+                            const RT* qa = p + (ra[r] + x0);
+                            const RT* qb = p + (rb[r] + x0);
+                            t00[r] = __ldg(qa);
+                            t01[r] = __ldg(qa + 1);
+                            t10[r] = __ldg(qb);
+                            t11[r] = __ldg(qb + 1);
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int r = 0; r < kRowsL; ++r) {
+                        if (r < rows) {
+                            t00[r] = __ldg(p + ra[r] + x0);
+                            t01[r] = __ldg(p + ra[r] + x1);
+                            t10[r] = __ldg(p + rb[r] + x0);
+                            t11[r] = __ldg(p + rb[r] + x1);
+                        }
                     }
                 }
 #pragma unroll
