@@ -181,16 +181,16 @@ __global__ void __launch_bounds__(32 * kFrameWarps, kFrameMinBlocks) frame_kerne
                     // exactly w-1, so fx = 0 and w01 = w11 = 0 multiply whatever byte
                     // follows (the next row's first, or the first byte of the frame
                     // after the previous one in the GOP buffer): the sum is unchanged.
+                    // (rows past the plane's bottom edge load clamped, in-plane taps and are
+                    // never stored: no per-row branch)
 #pragma unroll
                     for (int r = 0; r < kRowsL; ++r) {
-                        if (r < rows) {
-                            const RT* qa = p + (ra[r] + x0);
-                            const RT* qb = p + (rb[r] + x0);
-                            t00[r] = __ldg(qa);
-                            t01[r] = __ldg(qa + 1);
-                            t10[r] = __ldg(qb);
-                            t11[r] = __ldg(qb + 1);
-                        }
+                        const RT* qa = p + (ra[r] + x0);
+                        const RT* qb = p + (rb[r] + x0);
+                        t00[r] = __ldg(qa);
+                        t01[r] = __ldg(qa + 1);
+                        t10[r] = __ldg(qb);
+                        t11[r] = __ldg(qb + 1);
                     }
                 } else {
 #pragma unroll
@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(32 * kFrameWarps, kFrameMinBlocks) frame_kerne
                 }
 #pragma unroll
                 for (int r = 0; r < kRowsL; ++r) {
-                    if (r >= rows) break;
+                    if (sizeof(RT) != 1 && r >= rows) break;
                     const double w00 = (1 - fy[r]) * (1 - fx), w01 = (1 - fy[r]) * fx, w10 = fy[r] * (1 - fx),
                                  w11 = fy[r] * fx;
                     pred[r][c] = ((w00 * to_d(t00[r]) + w01 * to_d(t01[r])) + w10 * to_d(t10[r])) + w11 * to_d(t11[r]);
@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(32 * kFrameWarps, kFrameMinBlocks) frame_kerne
     if (!col_ok) return;
 #pragma unroll
     for (int r = 0; r < kRowsL; ++r) {
-        if (r >= rows) break;
+        if (r >= rows) continue;  // (predicated, no loop exit)
         const size_t k = (size_t)(y_base + r) * w + x;
         int rec[C];
 #pragma unroll
