@@ -216,23 +216,25 @@ __device__ __forceinline__ void aan_inv(double (&v)[8]) {
 }
 
 // One 8x8 block reconstruction u = IDCT(eig * DCT(mc)) + a, computed by the
-// 8 lanes [lane0, lane0+8) of a warp on the shared tile `t` (64 doubles,
-// row-major y*8+x).  On entry t holds mc; on exit the reconstruction.
+// 8 lanes [lane0, lane0+8) of a warp on the shared tile `t` (row-major, row
+// stride LD doubles: 8, or 9 so the row passes of 8 lanes hit 8 different
+// bank pairs instead of 4-way conflicts).  On entry t holds mc; on exit the reconstruction.
 // Mirrors dct2_aan_8x8 / idct2_aan_8x8 / reconstruct_blocks operation by
 // operation (pseudodiff.py:141-152, 275-279).
+template <int LD = 8>
 __device__ __forceinline__ void block_reconstruct_8lanes(double* t, int j, const double* eig, double a,
                                                          unsigned mask8) {
     double v[8];
     // forward pass along x for row j
 #pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = t[j * 8 + i];
+    for (int i = 0; i < 8; ++i) v[i] = t[j * LD + i];
     aan_fwd(v);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) t[j * 8 + i] = v[i];
+    for (int i = 0; i < 8; ++i) t[j * LD + i] = v[i];
     __syncwarp(mask8);
     // forward pass along y for column j, scale, eigenvalues, inverse scale
 #pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = t[i * 8 + j];
+    for (int i = 0; i < 8; ++i) v[i] = t[i * LD + j];
     aan_fwd(v);
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
@@ -242,21 +244,21 @@ __device__ __forceinline__ void block_reconstruct_8lanes(double* t, int j, const
         v[i] = c * __ldg(kInvScale2 + i * 8 + j);         // idct2: coef * _ISCALE2
     }
 #pragma unroll
-    for (int i = 0; i < 8; ++i) t[i * 8 + j] = v[i];
+    for (int i = 0; i < 8; ++i) t[i * LD + j] = v[i];
     __syncwarp(mask8);
     // inverse pass along x for row j
 #pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = t[j * 8 + i];
+    for (int i = 0; i < 8; ++i) v[i] = t[j * LD + i];
     aan_inv(v);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) t[j * 8 + i] = v[i];
+    for (int i = 0; i < 8; ++i) t[j * LD + i] = v[i];
     __syncwarp(mask8);
     // inverse pass along y for column j, + a
 #pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = t[i * 8 + j];
+    for (int i = 0; i < 8; ++i) v[i] = t[i * LD + j];
     aan_inv(v);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) t[i * 8 + j] = v[i] + a;
+    for (int i = 0; i < 8; ++i) t[i * LD + j] = v[i] + a;
     __syncwarp(mask8);
 }
 

@@ -68,6 +68,10 @@ __device__ __forceinline__ double dequant(const ResDev& R, int sym, double scale
     return (double)sym * R.dz_step / 127.0 * scale;
 }
 
+// Row stride of the residual tiles in shared memory: 9 doubles, so the AAN
+// row passes (lane j reads row j) spread over all banks.
+constexpr int kResLd = 9;
+
 // Residual block of coded block b, plane ci of group G, built by lanes 0..7.
 __device__ __forceinline__ void residual_block(const ResDev& R, const ResGroupDev& G, int b, int ci, double* t,
                                                int lane, unsigned mask8) {
@@ -84,11 +88,11 @@ __device__ __forceinline__ void residual_block(const ResDev& R, const ResGroupDe
             ++rank;
             v = dequant(R, sym, R.c_scale);
         }
-        t[lane * 8 + x] = v;
+        t[lane * kResLd + x] = v;
     }
     double a = dequant(R, __ldg(G.a_sym + ci * G.nblocks + b), R.a_scale);
     __syncwarp(mask8);
-    block_reconstruct_8lanes(t, lane, kGreensEig, a, mask8);
+    block_reconstruct_8lanes<kResLd>(t, lane, kGreensEig, a, mask8);
 }
 
 // min(max(v, lo), hi) for finite v (np.clip; the flow values are checked finite)
@@ -121,7 +125,7 @@ constexpr int kFrameMinBlocks = HIVC_FRAME_MIN_BLOCKS;
 
 template <bool kInter, int C, typename RT>
 __global__ void __launch_bounds__(32 * kFrameWarps, kFrameMinBlocks) frame_kernel(FrameArgs A) {
-    __shared__ double s_res[kFrameWarps][C][kWarpTiles][64];
+    __shared__ double s_res[kFrameWarps][C][kWarpTiles][8 * kResLd];
     const int h = A.h, w = A.w;
     const int nbx = (w + 7) >> 3;
     const int ty = blockIdx.y;
@@ -315,7 +319,7 @@ __global__ void __launch_bounds__(32 * kFrameWarps, kFrameMinBlocks) frame_kerne
 #pragma unroll
         for (int c = 0; c < C; ++c) {
             const int gi = c == 0 ? 0 : 1;
-            const double res = coded[gi] ? s_res[wid][c][grp][(r0 + r) * 8 + gl] : 0.0;
+            const double res = coded[gi] ? s_res[wid][c][grp][(r0 + r) * kResLd + gl] : 0.0;
             double v = rint_clip(pred[r][c] + res);
             const double lo = (C == 3 && c > 0) ? -255.0 : 0.0;
             v = clampd(v, lo, 255.0);

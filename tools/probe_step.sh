@@ -1,7 +1,7 @@
 python -m pytest tests/test_gpu_bench_pins.py tests/test_gpu_parity.py tests/test_gpu_edge_sizes.py -x -q -m gpu > gpurun_out/pt.log 2>&1; tail -1 gpurun_out/pt.log
 L=paper_2008_10273_b200/libhivc_b200.so
 cp $L /tmp/new.so
-for rep in 1 2; do
+for rep in 1 2 3; do
 for v in base new; do
   if [ $v = base ]; then cp ab_base.so $L; else cp /tmp/new.so $L; fi
   for opt in "p_repeat=4"; do
