@@ -138,6 +138,9 @@ __global__ void __launch_bounds__(32 * kFrameWarps, kFrameMinBlocks) frame_kerne
     const bool col_ok = tile_ok && x < w;
     const int y_base = ty * 8 + r0;
     const int rows = min(kRowsL, h - y_base);  // (<= 0: no rows of this lane in a bottom edge tile)
+    // gray: one residual group (see the residual section)
+    const bool res_on = C == 1 && A.res.ngroups > 0 && tile_ok;
+    const int t_res = ty * nbx + (tile_ok ? tx : 0);
     double pred[kRowsL][C];
     // ---- prediction
     if (kInter) {
@@ -293,7 +296,21 @@ __global__ void __launch_bounds__(32 * kFrameWarps, kFrameMinBlocks) frame_kerne
         for (int c = 0; c < C; ++c) pred[r][c] = rint_clip(pred[r][c]);
     // ---- residual block(s): lanes 8g..8g+7 rebuild tile g's coded blocks
     bool coded[2] = {false, false};
-    if (A.res.ngroups > 0 && tile_ok) {
+    if (C == 1) {
+        // gray: one group with a static index, so `coded` stays in registers (a
+        // runtime group index put it in local memory, read back in the epilogue);
+        // loading the tile word ahead of the prediction measured no better
+        if (res_on) {
+            const unsigned mask8 = 0xFFu << (kLanesTile * grp);
+            const ResGroupDev& G = A.res.g[0];
+            const uint64_t word0 = __ldg(G.tile_words + (t_res >> 6));
+            coded[0] = (word0 >> (t_res & 63)) & 1ull;
+            if (coded[0] && sub < 8) {
+                const int b = __ldg(G.word_prefix + (t_res >> 6)) + __popcll(word0 & ((1ull << (t_res & 63)) - 1ull));
+                residual_block(A.res, G, b, 0, &s_res[wid][0][grp][0], gl, mask8);
+            }
+        }
+    } else if (A.res.ngroups > 0 && tile_ok) {
         const int t = ty * nbx + tx;
         const unsigned mask8 = 0xFFu << (kLanesTile * grp);
         int chan = 0;
