@@ -620,16 +620,18 @@ static size_t intra_tree_par(const uint8_t* d, size_t pos, uint32_t nbits, int32
     return nleaves;
 }
 
-// A medium gray plane's tree walked by the parse thread and the value-decode
-// helper together: the parse thread cuts the tree into subtrees and starts
-// walking them while the helper decodes the entropy-coded values
-// (decode_vals), after which the helper takes the remaining subtrees.  The two
-// sections of a 540p I-frame (~0.2 ms of values, ~0.5 ms of tree) then end
-// together instead of the tree alone gating the solve.  Any failure reruns the
-// sequential walk (the reference's error, in stream order).
+// A gray plane's tree walked by the parse thread (+ `extra` tree threads for
+// large planes) and the value-decode helper together: the parse thread cuts
+// the tree into subtrees and starts walking them while the helper decodes the
+// entropy-coded values (decode_vals), after which the helper takes the
+// remaining subtrees.  The two sections of a 540p I-frame (~0.2 ms of values,
+// ~0.5 ms of tree) then end together instead of the tree alone gating the
+// solve.  Any failure reruns the sequential walk (the reference's error, in
+// stream order).
 template <class V>
 static size_t intra_tree_coop(const uint8_t* d, size_t pos, uint32_t nbits, int32_t h, int32_t w,
-                              std::vector<uint64_t>& bits, std::vector<uint64_t>& local, int depth, V&& decode_vals) {
+                              std::vector<uint64_t>& bits, std::vector<uint64_t>& local, int depth, int extra,
+                              bool renice, V&& decode_vals) {
     const uint8_t* tb = d + pos + 4;
     const size_t nbytes = ((size_t)nbits + 7) / 8;
     std::vector<TreeTask> tasks;
@@ -647,12 +649,22 @@ static size_t intra_tree_coop(const uint8_t* d, size_t pos, uint32_t nbits, int3
             }
         }
     };
-    std::thread helper([&]() {
-        decode_vals();
+    auto wait_run = [&]() {
         int st;
         while ((st = state.load(std::memory_order_acquire)) == 0) std::this_thread::yield();
         if (st == 1) run();
+    };
+    std::thread helper([&]() {
+        if (renice) helper_priority();
+        decode_vals();
+        wait_run();
     });
+    std::vector<std::thread> more;  // tree threads from the start (large planes)
+    for (int e = 0; e < extra; ++e)
+        more.emplace_back([&]() {
+            helper_priority();
+            wait_run();
+        });
     bool cut = true;
     try {
         tree_tasks(tb, nbits, 0, 0, 0, w, h, depth, tasks);
@@ -673,6 +685,7 @@ static size_t intra_tree_coop(const uint8_t* d, size_t pos, uint32_t nbits, int3
         state.store(2, std::memory_order_release);
     }
     helper.join();
+    for (auto& t : more) t.join();
     if (!cut || bad) return intra_tree_seq(d, pos, nbits, h, w, bits);
     bits.assign(((size_t)h * w + 63) / 64, 0);
     size_t nleaves = 0;
@@ -811,11 +824,13 @@ size_t parse_intra(const uint8_t* d, size_t len, size_t pos, int32_t h, int32_t 
     };
     std::thread helper;
     const bool par = npx >= (1u << 18) && kHw > 1;
-    if (par && ntrees == 1 && tree_threads == 1) {
-        // a medium gray plane: tree and values on the same two threads (intra_tree_coop)
+    if (par && ntrees == 1) {
+        // gray: the value-decode helper joins the tree walk once the values are done
+        // (540p: the parse thread + the helper; >= 1 Mpx: tree_threads from the start)
         try {
-            const size_t nl = intra_tree_coop(d, tpos[0], tbits[0], h, w, bits, job.local, 3, decode_vals);
-            intra_points(bits, nl, job.pts[0], 1);
+            const size_t nl = intra_tree_coop(d, tpos[0], tbits[0], h, w, bits, job.local, tree_threads > 1 ? 5 : 3,
+                                              tree_threads - 1, tree_threads > 1, decode_vals);
+            intra_points(bits, nl, job.pts[0], tree_threads);
         } catch (...) {
             terr[0] = std::current_exception();
         }
