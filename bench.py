@@ -267,7 +267,7 @@ def reference_arm(args, rank):
 # ----------------------------------------------------------------------------- rooflines
 
 ONCHIP = REPO / "profiles" / "r02_onchip_peaks.json"     # tools/onchip_peaks.py on this pool's B200
-KMETRICS = REPO / "profiles" / "r02i_kernel_metrics.json"  # ncu capture of this bench's own launches
+KMETRICS = REPO / "profiles" / "r02k_kernel_metrics.json"  # ncu capture of this bench's own launches
 # shared-memory bytes per pixel per CG iteration in cg_tile_kernel (counted from the code,
 # 8-byte accesses): p = r + beta p (load + store), A p (3 loads: row below + 2 sides; the
 # rows above / here ride in registers), r -= alpha A p (3 loads again), x += alpha p (3)

@@ -1,10 +1,3 @@
-python -m pytest tests/test_gpu_bench_pins.py tests/test_gpu_parity.py -x -q -m gpu > gpurun_out/pt.log 2>&1; tail -1 gpurun_out/pt.log
-L=paper_2008_10273_b200/libhivc_b200.so
-cp $L /tmp/new.so
-for rep in 1 2 3; do
-for v in base new; do
-  if [ $v = base ]; then cp ab_base.so $L; else cp /tmp/new.so $L; fi
-  python bench.py --steps 10 --warmup 3 --no-cpu 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$v', round(d['value']), round(d['ms_per_step'],3), 'e2e', round(d['e2e']['value']), d['stages_ms_per_step']['device_span'])"
-done
-done
-cp /tmp/new.so $L
+python bench.py > gpurun_out/r02k_bench_line.json 2> gpurun_out/r02k_bench.err
+python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/r02k_bench_reference_line.json 2>/dev/null
+for i in 1 2 3; do python bench.py --steps 10 --warmup 3 --no-cpu 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['value']), round(d['ms_per_step'],3), 'e2e', round(d['e2e']['value']), d['stages_ms_per_step']['device_span'])"; done
