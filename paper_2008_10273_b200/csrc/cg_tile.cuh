@@ -151,12 +151,19 @@ __global__ void __launch_bounds__(kTileThreads, 1) cg_tile_kernel(const __grid_c
                         for (int row = 0; row < ROWS; ++row)
                             if (kExact || row < rows) col[row * W2] = r[row];
                     } else {
+                        // 8 rows at a time: their loads in flight together, then the updates
+                        constexpr int kChunk = 8;
 #pragma unroll
-                        for (int row = 0; row < ROWS; ++row)
-                            if (kExact || row < rows) {
-                                double* q = col + row * W2;
-                                *q = r[row] + beta * *q;
-                            }
+                        for (int r0 = 0; r0 < ROWS; r0 += kChunk) {
+                            double pv[kChunk];
+#pragma unroll
+                            for (int j = 0; j < kChunk; ++j)
+                                if (r0 + j < ROWS && (kExact || r0 + j < rows)) pv[j] = col[(r0 + j) * W2];
+#pragma unroll
+                            for (int j = 0; j < kChunk; ++j)
+                                if (r0 + j < ROWS && (kExact || r0 + j < rows))
+                                    col[(r0 + j) * W2] = r[r0 + j] + beta * pv[j];
+                        }
                     }
                     // reflecting plane edges (own values, re-read: only the edge threads)
                     if (top) col[-W2] = col[0];
