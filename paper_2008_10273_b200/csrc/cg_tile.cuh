@@ -151,8 +151,9 @@ __global__ void __launch_bounds__(kTileThreads, 1) cg_tile_kernel(const __grid_c
                         for (int row = 0; row < ROWS; ++row)
                             if (kExact || row < rows) col[row * W2] = r[row];
                     } else {
-                        // 8 rows at a time: their loads in flight together, then the updates
-                        constexpr int kChunk = 8;
+                        // every row's p load in flight before the first update (measured: chunks of
+                        // 8 / 15 / 20 rows were slower in the later phases of the iteration)
+                        constexpr int kChunk = kExact ? ROWS : 8;  // (the generic 32-row kernel spills at 32)
 #pragma unroll
                         for (int r0 = 0; r0 < ROWS; r0 += kChunk) {
                             double pv[kChunk];
