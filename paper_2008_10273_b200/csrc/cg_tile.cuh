@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) cg_tile_kernel(const __grid_c
                     } else {
                         // every row's p load in flight before the first update (measured: chunks of
                         // 8 / 15 / 20 rows were slower in the later phases of the iteration)
-                        constexpr int kChunk = kExact ? ROWS : 8;  // (the generic 32-row kernel spills at 32)
+                        constexpr int kChunk = kExact ? ROWS : 1;  // (the generic 32-row kernel spills with chunks)
 #pragma unroll
                         for (int r0 = 0; r0 < ROWS; r0 += kChunk) {
                             double pv[kChunk];
