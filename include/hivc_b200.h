@@ -141,6 +141,21 @@ int hivc_poisson_interior(hivc_ctx* ctx, const double* w_full, const uint8_t* ma
 int hivc_mask_adjoint(hivc_ctx* ctx, const double* w_full, const double* z, const int32_t* pts, int32_t npts,
                       int32_t h, int32_t w, double* out);
 
+/* ------------------------------------------------------------------ flow component decode
+ * Replaces flow._decompress_plane (flow.py:343-356) with its
+ * uniform_dequantize (quantize.py:78-82) and paint_leaf_values
+ * (subdivision.py:162-170): reads f32 lo/hi, u32 nbits, the subdivision tree
+ * and the tANS leaf indices at `pos`, and paints each leaf's value on the
+ * (h x w) float64 plane `out`.  ctx == NULL: `out` is host memory (painted by
+ * the calling thread); else `out` is a device pointer on ctx's device (one
+ * kernel launch on ctx's stream, synchronised).  *next_pos: the position
+ * after the component.  Errors in the reference's order and classes:
+ * HIVC_E_TRUNCATED_STREAM, tree/entropy errors, HIVC_E_QUANTIZE (lo >= hi),
+ * HIVC_E_SUBDIVISION (leaf value count mismatch).
+ */
+int hivc_flow_component(hivc_ctx* ctx, const uint8_t* data, size_t len, size_t pos, int32_t h, int32_t w,
+                        int32_t levels, double* out, size_t* next_pos);
+
 /* ------------------------------------------------------------------ warp
  * Replaces flow.warp_planes (flow.py:94-127): every plane sampled at
  * (x+u, y+v), clamped bilinear, float64.  src/dst: host arrays of `nplanes`

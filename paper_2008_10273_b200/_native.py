@@ -65,6 +65,8 @@ _proto("hivc_poisson_interior", C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c
        C.c_int32, C.c_void_p, c_int_p)
 _proto("hivc_mask_adjoint", C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
        C.c_void_p)
+_proto("hivc_flow_component", C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_size_t, C.c_int32, C.c_int32,
+       C.c_int32, C.c_void_p, c_size_p)
 _proto("hivc_warp", C.c_int, C.c_void_p, C.POINTER(C.c_void_p), C.c_int32, C.c_void_p, C.c_void_p, C.c_int32,
        C.c_int32, C.POINTER(C.c_void_p))
 _proto("hivc_block_reconstruct", C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p)

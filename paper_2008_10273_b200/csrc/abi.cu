@@ -267,6 +267,37 @@ int hivc_mask_adjoint(hivc_ctx* ctx, const double* w_full, const double* z, cons
     });
 }
 
+int hivc_flow_component(hivc_ctx* ctx, const uint8_t* data, size_t len, size_t pos, int32_t h, int32_t w,
+                        int32_t levels, double* out, size_t* next_pos) {
+    return guarded([&] {
+        if (h < 1 || w < 1 || levels < 2) hivc::fail(HIVC_E_ARGUMENT, "bad flow plane shape or levels");
+        std::vector<hivc::Rect> leaves;
+        std::vector<double> vals;
+        const size_t next = hivc::parse_flow_component(data, len, pos, h, w, levels, leaves, vals);
+        static_assert(sizeof(hivc::Rect) == 16, "Rect is four int32");
+        if (!ctx) {  // host plane
+            for (size_t i = 0; i < leaves.size(); ++i) {
+                const hivc::Rect& r = leaves[i];
+                for (int32_t y = r.y; y < r.y + r.h; ++y) std::fill_n(out + (size_t)y * w + r.x, r.w, vals[i]);
+            }
+        } else {  // device plane: one upload, one launch
+            hivc::Context& C = ctx->c;
+            CUDA_CHECK(cudaSetDevice(C.device));
+            const size_t n = leaves.size(), rb = n * sizeof(hivc::Rect);
+            void* tmp = nullptr;
+            CUDA_CHECK(cudaMallocAsync(&tmp, rb + n * sizeof(double), C.stream));
+            CUDA_CHECK(cudaMemcpyAsync(tmp, leaves.data(), rb, cudaMemcpyHostToDevice, C.stream));
+            CUDA_CHECK(cudaMemcpyAsync((char*)tmp + rb, vals.data(), n * sizeof(double), cudaMemcpyHostToDevice,
+                                       C.stream));
+            hivc::launch_paint_leaves((const int32_t*)tmp, (const double*)((char*)tmp + rb), (int)n, w, out, C.stream);
+            C.launches += 1;
+            CUDA_CHECK(cudaFreeAsync(tmp, C.stream));
+            CUDA_CHECK(cudaStreamSynchronize(C.stream));
+        }
+        if (next_pos) *next_pos = next;
+    });
+}
+
 int hivc_warp(hivc_ctx* ctx, const double* const* src, int32_t nplanes, const double* u, const double* v, int32_t h,
               int32_t w, double* const* dst) {
     return guarded([&] {

@@ -906,6 +906,32 @@ size_t parse_flow(const uint8_t* d, size_t len, size_t pos, int32_t h, int32_t w
     return pos;
 }
 
+size_t parse_flow_component(const uint8_t* d, size_t len, size_t pos, int32_t h, int32_t w, int levels,
+                            std::vector<Rect>& leaves, std::vector<double>& vals) {
+    if (pos + 12 > len) fail(HIVC_E_TRUNCATED_STREAM, "flow payload truncated");
+    float lo, hi;
+    std::memcpy(&lo, d + pos, 4);
+    std::memcpy(&hi, d + pos + 4, 4);
+    uint32_t nbits = rd_u32(d + pos + 8);
+    pos += 12;
+    size_t nbytes = ((size_t)nbits + 7) / 8;
+    if (pos + nbytes > len) fail(HIVC_E_TRUNCATED_STREAM, "flow payload truncated");
+    BitReader rd(d + pos, nbytes, nbits);
+    leaves.clear();
+    parse_tree_leaves(rd, w, h, leaves);  // deserialize_tree (flow.py:351-352)
+    pos += nbytes;
+    std::vector<int32_t> idx;
+    pos = decode_symbols(d, len, pos, idx);
+    double flo = lo, fhi = hi;
+    if (!(flo < fhi)) fail(HIVC_E_QUANTIZE, "need lo < hi");  // uniform_dequantize (quantize.py:78-82)
+    const double step = (fhi - flo) / (double)(levels - 1);
+    // paint_leaf_values (subdivision.py:162-170)
+    if (idx.size() != leaves.size()) fail(HIVC_E_SUBDIVISION, "leaf value count mismatch");
+    vals.resize(idx.size());
+    for (size_t i = 0; i < idx.size(); ++i) vals[i] = flo + (double)idx[i] * step;
+    return pos;
+}
+
 // ---------------------------------------------------------------- residual payload
 
 size_t parse_residual(const uint8_t* d, size_t len, size_t pos, int32_t h, int32_t w, int channels, ResidualJob& job) {

@@ -148,6 +148,12 @@ void parse_tree_leaves(BitReader& rd, int32_t w, int32_t h, std::vector<Rect>& l
 void parse_flow_tree(BitReader& rd, int32_t w, int32_t h, std::vector<int32_t>& nodes, int32_t& nleaves,
                      std::vector<Rect>* leaves = nullptr);
 
+// One flow component (flow._decompress_plane, flow.py:343-356): leaf
+// rectangles in preorder and their dequantised values (quantize.py:78-82),
+// with the reference's error classes in its order; returns the next position.
+size_t parse_flow_component(const uint8_t* d, size_t len, size_t pos, int32_t h, int32_t w, int levels,
+                            std::vector<Rect>& leaves, std::vector<double>& vals);
+
 struct StreamHeader {
     int32_t width, height, frame_count, fps_num, fps_den, gop_size, channels;
     int32_t intra_levels, flow_levels, residual_levels;

@@ -433,6 +433,28 @@ void launch_warp(const double* const* src, int nplanes, const double* u, const d
     }
 }
 
+// ---------------------------------------------------------------- leaf painting
+
+// One CTA column per leaf (blockIdx.x), blockIdx.y strides the leaf's rows; a
+// row is written by consecutive threads (coalesced 8-byte stores).  Leaves
+// tile the plane, so every pixel is written exactly once.
+__global__ void paint_leaves_kernel(const int4* __restrict__ rects, const double* __restrict__ vals, int pw,
+                                    double* __restrict__ out) {
+    const int4 r = rects[blockIdx.x];
+    const double v = vals[blockIdx.x];
+    for (int y = blockIdx.y; y < r.w; y += gridDim.y) {
+        double* row = out + (size_t)(r.y + y) * pw + r.x;
+        for (int x = threadIdx.x; x < r.z; x += blockDim.x) row[x] = v;
+    }
+}
+
+void launch_paint_leaves(const int32_t* rects, const double* vals, int nleaves, int pw, double* out, cudaStream_t s) {
+    if (nleaves <= 0) return;
+    // rect fields are (x, y, w, h): int4 .x=x .y=y .z=w .w=h
+    paint_leaves_kernel<<<dim3(nleaves, 8), 128, 0, s>>>(reinterpret_cast<const int4*>(rects), vals, pw, out);
+    CUDA_CHECK(cudaGetLastError());
+}
+
 // ---------------------------------------------------------------- standalone block reconstruct
 
 __global__ void block_reconstruct_kernel(const double* __restrict__ mc, const double* __restrict__ a,

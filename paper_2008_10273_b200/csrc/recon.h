@@ -52,6 +52,10 @@ void launch_frame(const FrameArgs& a, bool inter, cudaStream_t s);
 // f.ravel()[pts] = vals; mask.ravel()[pts] = 1 (prediction.py:203-208) after zero fill.
 void launch_scatter(const int32_t* pts, const double* vals, int npts, double* f, uint8_t* m, cudaStream_t s);
 
+// subdivision.paint_leaf_values (subdivision.py:162-170): out[y:y+h, x:x+w] = vals[i]
+// for every preorder leaf rect i (x, y, w, h int32 quadruples), plane width `pw`.
+void launch_paint_leaves(const int32_t* rects, const double* vals, int nleaves, int pw, double* out, cudaStream_t s);
+
 // flow.warp_planes on float64 planes (flow.py:94-127).
 void launch_warp(const double* const* src, int nplanes, const double* u, const double* v, int h, int w,
                  double* const* dst, cudaStream_t s);

@@ -17,7 +17,7 @@ import numpy as np
 
 from paper_2008_10273_b200 import _native as N
 from paper_2008_10273_b200._tensors import back, is_cuda_tensor, ptr, to_device, torch
-from paper_2008_10273_b200.errors import FlowError, QuantizeError, SubdivisionError, TruncatedStream
+from paper_2008_10273_b200.errors import FlowError
 
 
 @dataclass(frozen=True)
@@ -151,59 +151,27 @@ def _tree_leaves(data: bytes, pos: int, nbits: int, width: int, height: int, bit
     return (out, int(used.value)) if with_used else out
 
 
-def _decode_symbols(data: bytes, pos: int):
-    from paper_2008_10273_b200.entropy import decode_symbols
-
-    return decode_symbols(data, pos)
-
-
 def _decompress_plane(data: bytes, pos: int, shape, levels: int):
-    if pos + 12 > len(data):  # flow.py:343-356
-        raise TruncatedStream("flow payload truncated")
-    lo, hi, nbits = struct.unpack_from("<ffI", data, pos)
-    pos += 12
-    nbytes = (nbits + 7) // 8
-    if pos + nbytes > len(data):
-        raise TruncatedStream("flow payload truncated")
-    leaves = _tree_leaves(data, pos, nbits, shape[1], shape[0])
-    pos += nbytes
-    idx, pos = _decode_symbols(data, pos)
-    lo, hi = float(lo), float(hi)
-    if not lo < hi:
-        raise QuantizeError("need lo < hi")
-    vals = lo + idx.astype(np.float64) * ((hi - lo) / (levels - 1))
-    if len(vals) != len(leaves):
-        raise SubdivisionError("leaf value count mismatch")
-    out = np.empty(shape, dtype=np.float64)
-    for (x, y, w, h), val in zip(leaves.tolist(), vals):
-        out[y : y + h, x : x + w] = val
-    return out, pos
+    """One flow component painted on a host float64 plane (flow.py:343-356,
+    quantize.py:78-82, subdivision.py:162-170) by one native call."""
+    h, w = shape
+    out = np.empty((h, w), dtype=np.float64)
+    nxt = C.c_size_t()
+    N.check(N.lib.hivc_flow_component(None, bytes(data), len(data), pos, h, w, levels,
+                                      out.ctypes.data_as(C.c_void_p), C.byref(nxt)))
+    return out, int(nxt.value)
 
 
 def _decompress_plane_device(data: bytes, pos: int, shape, levels: int, device):
-    """_decompress_plane painting the leaf values on the GPU (the encoder's closed
-    loop keeps the dense flow on the device for the warp)."""
-    if pos + 12 > len(data):
-        raise TruncatedStream("flow payload truncated")
-    lo, hi, nbits = struct.unpack_from("<ffI", data, pos)
-    pos += 12
-    nbytes = (nbits + 7) // 8
-    if pos + nbytes > len(data):
-        raise TruncatedStream("flow payload truncated")
-    leaves = _tree_leaves(data, pos, nbits, shape[1], shape[0])
-    pos += nbytes
-    idx, pos = _decode_symbols(data, pos)
-    lo, hi = float(lo), float(hi)
-    if not lo < hi:
-        raise QuantizeError("need lo < hi")
-    vals = lo + idx.astype(np.float64) * ((hi - lo) / (levels - 1))
-    if len(vals) != len(leaves):
-        raise SubdivisionError("leaf value count mismatch")
+    """_decompress_plane with the leaves painted on the GPU by one launch (the
+    encoder's closed loop keeps the dense flow on the device for the warp)."""
+    h, w = shape
     t = torch()
-    out = t.empty(shape, dtype=t.float64, device=device)
-    for (x, y, w, h), val in zip(leaves.tolist(), vals.tolist()):
-        out[y : y + h, x : x + w] = val
-    return out, pos
+    out = t.empty((h, w), dtype=t.float64, device=device)
+    nxt = C.c_size_t()
+    N.check(N.lib.hivc_flow_component(N.context(out.device.index).handle, bytes(data), len(data), pos, h, w, levels,
+                                      ptr(out), C.byref(nxt)))
+    return out, int(nxt.value)
 
 
 def decompress_flow(data: bytes, pos: int, shape, quant_levels: int):
