@@ -167,3 +167,28 @@ def test_decompress_flow_device_paint_matches_reference(wg):
         v, pos = _decompress_plane_device(pred, pos, shape, fl, torch.device("cuda:0"))
         assert pos == len(pred) and u.is_cuda
         assert np.array_equal(np.stack([u.cpu().numpy(), v.cpu().numpy()]), wg[key + "_flow"])
+
+
+def test_decompress_flow_error_classes():
+    """Corrupt flow payloads raise the reference's classes in its order
+    (flow.py:343-356, quantize.py:78-82, subdivision.py:162-170)."""
+    from paper_2008_10273_b200 import errors
+    from paper_2008_10273_b200.flow import decompress_flow
+
+    hdr, recs = _records("cfg0")
+    shape, _, _, fl, _ = _hdr(hdr)
+    _, pred, _ = recs["cfg0_g0_f1"]
+    with pytest.raises(errors.TruncatedStream):
+        decompress_flow(pred[:11], 0, shape, fl)  # no room for lo/hi/nbits
+    lo, hi, nbits = struct.unpack_from("<ffI", pred, 0)
+    with pytest.raises(errors.TruncatedStream):
+        decompress_flow(pred[: 12 + (nbits + 7) // 8 - 1], 0, shape, fl)  # tree cut short
+    swapped = struct.pack("<ff", hi, lo) + pred[8:]
+    with pytest.raises(errors.QuantizeError):
+        decompress_flow(swapped, 0, shape, fl)  # lo >= hi
+    # the tree followed by a 3-value symbol block: more leaves than values
+    from paper_2008_10273_b200.entropy import encode_symbols
+
+    short = pred[: 12 + (nbits + 7) // 8] + encode_symbols(np.array([1, 2, 3]), table_log=8)
+    with pytest.raises(errors.SubdivisionError, match="leaf value count mismatch"):
+        decompress_flow(short, 0, shape, fl)
