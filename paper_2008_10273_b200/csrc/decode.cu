@@ -230,7 +230,8 @@ void Slot::init(int dev) {
     if (stream) return;
     device = dev;
     // (a higher priority for the P-frame streams than for the solver stream
-    // measured slower: 4270 vs 4400 frames/s)
+    // measured slower: 4270 vs 4400 frames/s; a higher priority for the solver
+    // (and pre) streams measured no faster: profiles/r02n_ab_prio.txt)
     static const bool prio = debug_opt("p_prio") != nullptr;
     if (prio) {
         int lo = 0, hi = 0;
@@ -1099,7 +1100,10 @@ void decode_streams(Context& ctx, int nstreams, const uint8_t* const* data, cons
     };
     static const int kMaxWorkers = [] {
         const char* e = debug_opt("workers");
-        const int hw = (int)std::max(2u, std::thread::hardware_concurrency());
+        // one process per GPU (torchrun): the ranks of a node share its cores
+        const char* lws = std::getenv("LOCAL_WORLD_SIZE");
+        const int ranks = lws ? std::max(1, std::atoi(lws)) : 1;
+        const int hw = std::max(2, (int)std::thread::hardware_concurrency() / ranks);
         // half the hardware threads: each large I-frame parse also runs tree
         // and value helper threads (measured on 16 cores: 8 workers beat 16 by 3 %)
         return e ? std::max(1, std::min(64, std::atoi(e))) : std::max(2, std::min(hw / 2, 32));
