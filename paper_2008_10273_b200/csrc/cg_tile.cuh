@@ -399,8 +399,6 @@ __global__ void __launch_bounds__(kTileThreads, 1) cg_tile_kernel(const __grid_c
 
 // The instantiation for a tile plan: exact shapes of the benchmark pyramids
 // (1080x1920: 30x480; 540x960: 30x480, 23x480, 15x480), else the generic one.
-// The instantiation for a tile plan: exact shapes of the benchmark pyramids
-// (1080x1920: 30x480; 540x960: 30x480, 23x480, 15x480), else the generic one.
 using TileKernelFn = void (*)(TileBatch);
 inline TileKernelFn tile_kernel_for(int trows, int tcols) {
     if (tcols == 480) {
