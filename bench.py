@@ -267,11 +267,12 @@ def reference_arm(args, rank):
 # ----------------------------------------------------------------------------- rooflines
 
 ONCHIP = REPO / "profiles" / "r02_onchip_peaks.json"     # tools/onchip_peaks.py on this pool's B200
-KMETRICS = REPO / "profiles" / "r02k_kernel_metrics.json"  # ncu capture of this bench's own launches
-# shared-memory bytes per pixel per CG iteration in cg_tile_kernel (counted from the code,
-# 8-byte accesses): p = r + beta p (load + store), A p (3 loads: row below + 2 sides; the
-# rows above / here ride in registers), r -= alpha A p (3 loads again), x += alpha p (3)
-SMEM_B_PX_IT = 88
+KMETRICS = REPO / "profiles" / "r02o_kernel_metrics.json"  # ncu capture of this bench's own launches
+# shared-memory bytes per pixel per CG iteration in cg_tile_kernel<30, 480> (counted from
+# the code, 8-byte accesses): p = r + beta p (load + store), A p (3 loads: row below + 2
+# sides; the rows above / here ride in registers), r -= alpha A p (3 loads again, but only
+# for the 16 of 30 rows whose A p is not kept in registers), x += alpha p (3)
+SMEM_B_PX_IT = 8 * (2 + 3 + 3 * 16 / 30 + 3)  # 76.8
 
 
 def _kernel_row(km, pattern):
@@ -310,7 +311,7 @@ def roofline_rows(gsec, glaunch, gpix_it, gpix, pix_it, peaks):
         "unit": "GB/s",
         "frac": achieved / smem_peak if achieved and smem_peak else None,
         "traffic": kt["dram_bytes"] if kt else None,
-        "algorithmic": f"shared-memory bytes = {SMEM_B_PX_IT} B x pixels x iterations per level launch "
+        "algorithmic": f"shared-memory bytes = {SMEM_B_PX_IT:.1f} B x pixels x iterations per level launch "
                        f"(= {smem_bytes / 1e9:.2f} GB/launch)" if smem_bytes else None,
         "live_timing": "in-kernel globaltimer span per launch, instrumented bench steps",
         "avg_launch_us": 1e6 * t_launch if t_launch else None,

@@ -31,6 +31,17 @@
 #pragma once
 
 constexpr int kTileRows = 32;
+// rows of A p kept in registers between the two stencil phases, per exact tile height
+// (as many as the register file takes without spills at 512 threads x 128 registers)
+#ifndef HIVC_CG_KEEP30
+#define HIVC_CG_KEEP30 14
+#endif
+#ifndef HIVC_CG_KEEP23
+#define HIVC_CG_KEEP23 16
+#endif
+#ifndef HIVC_CG_KEEP15
+#define HIVC_CG_KEEP15 15
+#endif
 constexpr int kTileThreads = 512;
 constexpr int kTileCols = kTileThreads;  // thread c owns column c of its tile
 
@@ -47,6 +58,11 @@ __global__ void __launch_bounds__(kTileThreads, 1) cg_tile_kernel(const __grid_c
     // exact tiles of <= 480 columns leave the last warp without a column: it runs the
     // second grid sum of each iteration
     constexpr bool kSyncWarp = kExact && TC <= kTileThreads - 32;
+    // A p of the first kKeep rows stays in registers from the p.Ap walk to the r update
+    // (the registers that hold the p loads of phase 1a are free then); the r update
+    // recomputes it only for the rows below.  Same values either way.
+    constexpr int kKeep = !kExact ? 0 : ROWS == 30 ? HIVC_CG_KEEP30 : ROWS == 23 ? HIVC_CG_KEEP23 : HIVC_CG_KEEP15;
+    static_assert(kKeep >= 0 && kKeep <= ROWS, "kept rows");
     constexpr int kSyncWid = kTileThreads / 32 - 1;
     extern __shared__ double sp[];  // (trows + 2) x (tcols + 2), then x_rows x tcols
     __shared__ double sh[2 * 4 * 32 + 8];
@@ -207,6 +223,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) cg_tile_kernel(const __grid_c
             HIVC_TRACE(1);
             // ---- phase 1b: A p and p.Ap walking the own column top to bottom
             double d[1] = {0.0};
+            double ap[kKeep > 0 ? kKeep : 1];
             if (act) {
                 double up = col[-W2], cur = col[0];
 #pragma unroll
@@ -217,6 +234,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) cg_tile_kernel(const __grid_c
                     // -lap, (((-4 c + N) + S) + W) + E negated term by term (exact: round-to-nearest is symmetric)
                     const double nlap = (((cur * 4.0 - up) - dn) - q[-1]) - q[1];
                     const double api = ((mbits >> row) & 1u) ? 0.0 : nlap;
+                    if (row < kKeep) ap[row] = api;
                     d[0] += cur * api;
                     up = cur;
                     cur = dn;
@@ -232,9 +250,19 @@ __global__ void __launch_bounds__(kTileThreads, 1) cg_tile_kernel(const __grid_c
             // ---- phase 2: r -= alpha A p, r.r; publish r's edges
             double e1[1] = {0.0};
             if (act) {
-                double up = col[-W2], cur = col[0];
 #pragma unroll
-                for (int row = 0; row < ROWS; ++row) {
+                for (int row = 0; row < kKeep; ++row) {
+                    double& rr = r[row];
+                    rr = rr - alpha * ap[row];
+                    e1[0] += rr * rr;
+                }
+                double up = 0.0, cur = 0.0;
+                if (kKeep < ROWS) {
+                    up = col[(kKeep - 1) * W2];
+                    cur = col[kKeep * W2];
+                }
+#pragma unroll
+                for (int row = kKeep; row < ROWS; ++row) {
                     if (!kExact && row >= rows) break;
                     const double* q = col + row * W2;
                     const double dn = q[W2];
